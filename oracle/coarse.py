@@ -1,0 +1,112 @@
+"""Stage I: coarse candidate generation by collision voting (PAPER §4.2.2 (1); §5.4).
+
+* schedule(n, k)        adaptive (rho, beta) vs KV length (reading AMB-11 = SPEC S:329 in basis points)
+* query_bonus_tables    per subspace, bonus of every centroid id for one query (P:477 + P:865, AMB-8/9/10)
+* collision_scores      score_i = sum_b bonus_b(id_{i,b})  in [0, B * max bonus]
+* bucket_topk           C = ceil(beta n) highest integer scores by counting;
+                        ties in the threshold bucket: newest (larger index) first (AMB-12)
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import codebook, transform
+
+# (min_length, rho, beta) in basis points (AMB-11)
+SCHEDULE_BP = ((0, 1500, 1000), (20000, 1200, 800), (60000, 1000, 600), (200000, 800, 500))
+
+
+def schedule(n: int, top_k: int, n_centroids: int = 256, table=SCHEDULE_BP):
+    """Returns (T probes per subspace, C candidates) for a retrieval zone of n keys (integer arithmetic)."""
+    rho_bp, beta_bp = table[0][1], table[0][2]
+    for min_len, r_bp, b_bp in table:
+        if n >= min_len:
+            rho_bp, beta_bp = r_bp, b_bp
+    T = (rho_bp * n_centroids + 9999) // 10000
+    C = min(n, max(min(top_k, n), (beta_bp * n + 9999) // 10000))
+    return int(T), int(C)
+
+
+def query_bonus_tables(q: np.ndarray, rot_sign_bits: np.ndarray, T: int, B: int = 16,
+                       tier_bonus=(6, 5, 4, 3, 2, 1)) -> np.ndarray:
+    """bonus[b, c] for one query q [D] (fp64 values of the bf16 query). AMB-8/9/10."""
+    y = transform.rotate_unscaled(q, rot_sign_bits)
+    yb = transform.split(y, B)
+    out = np.zeros((B, 2 ** yb.shape[-1]), dtype=np.int64)
+    for b in range(B):
+        s = codebook.centroid_scores(yb[b])
+        rank = codebook.rank_centroids(s)
+        out[b] = codebook.tier_bonus_of_rank(rank, T, tier_bonus)
+    return out
+
+
+def collision_scores(ids: np.ndarray, bonus: np.ndarray) -> np.ndarray:
+    """score_i = sum_b bonus[b, ids[i, b]]. ids [n, B] -> int64 [n]."""
+    ids = np.asarray(ids).astype(np.int64)
+    n, B = ids.shape
+    score = np.zeros(n, dtype=np.int64)
+    for b in range(B):
+        score = score + bonus[b, ids[:, b]]
+    return score
+
+
+def collision_scores_naive(ids: np.ndarray, q: np.ndarray, rot_sign_bits: np.ndarray, T: int,
+                           tier_bonus=(6, 5, 4, 3, 2, 1)) -> np.ndarray:
+    """Naive per-key loop (S:311's oracle): for every key and subspace, decode the key's centroid,
+    rank it against all 2^m centroids by <q_b, omega> and look up its tier. Pure Python; tiny n only."""
+    ids = np.asarray(ids).astype(np.int64)
+    n, B = ids.shape
+    D = len(q)
+    m = D // B
+    y = transform.rotate_unscaled(q, rot_sign_bits)
+    W = codebook.all_centroids(m) * np.sqrt(m)   # +-1 entries
+    n_tiers = len(tier_bonus)
+    chunk = max(1, T // n_tiers)
+    out = np.zeros(n, dtype=np.int64)
+    for i in range(n):
+        tot = 0
+        for b in range(B):
+            yb = y[b * m:(b + 1) * m]
+            c = ids[i, b]
+            sc = W @ yb
+            # rank of c: number of centroids strictly better, ties broken by smaller id
+            rk = int(np.sum(sc > sc[c]) + np.sum((sc == sc[c]) & (np.arange(2 ** m) < c)))
+            if rk < T:
+                tot += tier_bonus[min(rk // chunk, n_tiers - 1)]
+        out[i] = tot
+    return out
+
+
+def threshold(score: np.ndarray, C: int, max_score: int = 96):
+    """s* = max{s : #(score >= s) >= C}; returns (s*, #(score > s*)). C == 0 -> (max+1, 0)."""
+    counts = np.bincount(np.asarray(score, dtype=np.int64), minlength=max_score + 1)
+    if C <= 0:
+        return max_score + 1, 0
+    ge = 0
+    for s in range(max_score, -1, -1):
+        if ge + counts[s] >= C:
+            return s, ge
+        ge += counts[s]
+    raise ValueError("C exceeds n")
+
+
+def bucket_topk(score: np.ndarray, C: int, max_score: int = 96) -> np.ndarray:
+    """Top-C keys by integer score via a counting histogram; threshold-bucket ties newest first.
+
+    Returns the sorted candidate index array (a set: the order carries no meaning)."""
+    score = np.asarray(score, dtype=np.int64)
+    if C <= 0:
+        return np.zeros(0, dtype=np.int64)
+    s_star, n_gt = threshold(score, C, max_score)
+    gt = np.nonzero(score > s_star)[0]
+    eq = np.nonzero(score == s_star)[0]
+    take = C - n_gt
+    chosen = np.concatenate([gt, eq[len(eq) - take:]]) if take > 0 else gt
+    return np.sort(chosen)
+
+
+def bucket_topk_by_sort(score: np.ndarray, C: int) -> np.ndarray:
+    """Independent sort-based oracle: sort by (score desc, index desc), keep C."""
+    score = np.asarray(score, dtype=np.int64)
+    order = sorted(range(len(score)), key=lambda i: (-score[i], -i))
+    return np.sort(np.array(order[:C], dtype=np.int64))
