@@ -1,0 +1,452 @@
+"""Decode-step benchmark of the ParisKV retrieval hot path on B200 (BASELINE.json metric).
+
+A step = one decode step of a Llama-3.1-8B-shaped model (32 q / 8 KV heads, d = 128, 32 layers, each layer
+with its own index and K/V so > L2 is touched per step): per layer retrieve_topk (query prep, collision
+scan, bucket_topk, RSQ-IP rerank, top-k) + sparse_attend (hot rows U top-k rows). Inputs are synthetic
+(synth/, recipe in DESIGN.md), resident in HBM before the timed region. value = device time per layer.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 128k|32k_bs8]
+
+N > 1 (torchrun): the retrieval zone of every layer is sequence-sharded over the ranks (NCCL exchanges
+inside the library); value = the max-over-ranks time per layer of the whole job (strong scaling).
+--impl reference: the CPU oracle (oracle/) timed on a bounded sample on the host cores (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "decode retrieval+attn µs/layer at 128K & 1M ctx; scan HBM GB/s vs 8 TB/s peak"
+UNIT = "us/layer"
+N_LAYERS = 32
+N_Q, N_KV, D = 32, 8, 128
+TOP_K = 100
+N_SINK, N_LOCAL = 16, 256  # hot rows (Table 1 AIME row; sink 16 per S:452)
+
+CONFIGS = {
+    # BASELINE configs[1]: bs=1, 128K context, 1 decode step, all 32 layers
+    "128k": dict(batch=1, context=131072, workload="llama3.1-8b-shape bs1 ctx131072 decode step, 32 layers"),
+    # BASELINE configs[2]: bs=8 at 32K
+    "32k_bs8": dict(batch=8, context=32768, workload="llama3.1-8b-shape bs8 ctx32768 decode step, 32 layers"),
+}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "20", "-i", str(self.device)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.3)
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.05)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ----------------------------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_2602_07721_b200 import build as pbuild
+    pbuild.build()
+    from paper_2602_07721_b200 import pariskv as pkv
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfgw = CONFIGS[args.config]
+    batch, ctx = cfgw["batch"], cfgw["context"]
+    n_hot = N_SINK + N_LOCAL
+    n = ctx - n_hot                               # retrieval zone (AMB-22)
+    lo, hi = rank * n // world, (rank + 1) * n // world
+    n_loc = hi - lo
+    T, C = pkv.schedule(n, TOP_K)
+    cfg = pkv.config_init(N_Q, N_KV, synth.rotation_sign_bits())
+    L = args.layers
+
+    # ---- synthetic inputs (HBM resident), per layer distinct buffers ----
+    layers = []
+    for l in range(L):
+        seed = 1000 * l
+        stats = synth.head_stats(seed, N_KV, device=dev)
+        K = synth.llm_keys(seed, batch, N_KV, n, device=dev, stats=stats)
+        q = synth.llm_queries(seed, batch, N_Q, N_KV, device=dev, stats=stats)
+        synth.plant(K, q, seed)
+        V = synth.values(seed, batch, N_KV, n, device=dev)
+        Kl, Vl = K[:, :, lo:hi].contiguous(), V[:, :, lo:hi].contiguous()
+        del K, V
+        Kh = synth.isotropic(seed + 7, (batch, N_KV, n_hot, D), device=dev)
+        Vh = synth.isotropic(seed + 8, (batch, N_KV, n_hot, D), device=dev)
+        ix = pkv.Index(cfg, batch, n_loc, device=local)
+        if layers:
+            ix.share_workspace(layers[0]["ix"])
+        layers.append(dict(ix=ix, K=Kl, V=Vl, Kh=Kh, Vh=Vh, q=q.contiguous(),
+                           idx=torch.empty(batch, N_Q, TOP_K, dtype=torch.int32, device=dev),
+                           est=torch.empty(batch, N_Q, TOP_K, dtype=torch.float32, device=dev),
+                           out=torch.empty(batch, N_Q, D, dtype=torch.bfloat16, device=dev),
+                           lse=torch.empty(batch, N_Q, dtype=torch.float32, device=dev)))
+    torch.cuda.synchronize()
+    if world > 1:
+        uid = [pkv.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        pkv.comm_init(layers[0]["ix"], uid[0], rank, world, lo)
+        for ly in layers[1:]:
+            pkv.comm_share(ly["ix"], layers[0]["ix"], lo)
+
+    # ---- encode (prefill key summarisation), timed separately ----
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for ly in layers:
+        pkv.encode_keys(ly["ix"], ly["K"])
+    e1.record()
+    torch.cuda.synchronize()
+    enc_ms_layer = e0.elapsed_time(e1) / L
+
+    def step():
+        for ly in layers:
+            pkv.retrieve_topk(ly["ix"], ly["q"], TOP_K, probes_T=T, n_cand=C, n_global=n, out_idx=ly["idx"],
+                              out_est=ly["est"])
+            pkv.sparse_attend(ly["ix"], ly["q"], ly["K"], ly["V"], ly["idx"], ly["Kh"], ly["Vh"], out=ly["out"],
+                              lse=ly["lse"])
+
+    # warm-up (eager) + launch accounting
+    for _ in range(max(1, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    c0 = pkv.launch_count()
+    step()
+    torch.cuda.synchronize()
+    launches_per_step = pkv.launch_count() - c0
+
+    use_graph = not args.no_graph
+    graph = None
+    if use_graph:
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            step()
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        torch.cuda.synchronize()
+        run = graph.replay
+    else:
+        run = step
+    for _ in range(args.warmup):
+        run()
+    torch.cuda.synchronize()
+
+    def timed(fn, k):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(k):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ms = a.elapsed_time(b)
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    with ClockSampler(local) as clk:
+        total_ms = timed(run, args.steps)
+    ms_step = total_ms / args.steps
+    us_layer = ms_step * 1000.0 / L
+
+    # ---- per-kernel device times (CUDA events on the launch stream, eager replay of the same step) ----
+    prof_steps = max(3, min(args.steps, 20))
+    pkv.profile_enable(True)
+    for _ in range(prof_steps):
+        step()
+    torch.cuda.synchronize()
+    prof = pkv.profile_read()
+    pkv.profile_enable(False)
+
+    # ---- end to end through the public API with host buffers (pinned H2D q, D2H attention output) ----
+    q_host = [ly["q"].cpu().pin_memory() for ly in layers]
+    o_host = [torch.empty_like(ly["out"], device="cpu").pin_memory() for ly in layers]
+
+    def step_e2e():
+        for ly, qh, oh in zip(layers, q_host, o_host):
+            ly["q"].copy_(qh, non_blocking=True)
+            pkv.retrieve_topk(ly["ix"], ly["q"], TOP_K, probes_T=T, n_cand=C, n_global=n, out_idx=ly["idx"],
+                              out_est=ly["est"])
+            pkv.sparse_attend(ly["ix"], ly["q"], ly["K"], ly["V"], ly["idx"], ly["Kh"], ly["Vh"], out=ly["out"],
+                              lse=ly["lse"])
+            oh.copy_(ly["out"], non_blocking=True)
+
+    if use_graph:
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            step_e2e()
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        g2 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g2):
+            step_e2e()
+        run2 = g2.replay
+    else:
+        run2 = step_e2e
+    for _ in range(args.warmup):
+        run2()
+    e2e_ms = timed(run2, args.steps) / args.steps
+    e2e_eager_ms = timed(step_e2e, max(3, min(args.steps, 20))) / max(3, min(args.steps, 20))
+
+    # ---- roofline of the dominant kernel (algorithmic bytes / measured average launch time) ----
+    hbm_peak, peak_kind = peaks()
+    alg = {
+        "scan": batch * N_KV * n_loc * 16,                                    # 16 B ids per key per KV head
+        "rerank": batch * N_Q * min(C, n_loc) * (128 + 8),                    # 128 B record + id/est per cand
+        "attend": batch * (N_Q * TOP_K * 512 + (N_KV * n_hot * 512 if rank == world - 1 else 0)),
+        "topk": batch * N_Q * min(C, n_loc) * 8,
+        "compact": batch * N_KV * n_loc * 4,
+    }
+    kern = {}
+    for name, (cnt, ms) in prof.items():
+        avg_us = ms * 1000.0 / cnt
+        ent = {"launches": cnt, "avg_us": round(avg_us, 3), "share": round(ms / sum(v[1] for v in prof.values()), 4)}
+        if name in alg:
+            ent["alg_bytes"] = alg[name]
+            ent["gbs"] = round(alg[name] / (avg_us * 1e-6) / 1e9, 1)
+        kern[name] = ent
+    dom = max((k for k in kern if k in alg), key=lambda k: prof[k][1])
+    traffic = None
+    tr_file = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tr_file):
+        try:
+            traffic = json.load(open(tr_file)).get(args.config, {}).get(dom)
+        except Exception:
+            traffic = None
+    roof = {"bound": "hbm", "kernel": dom, "achieved": kern[dom]["gbs"], "peak": hbm_peak, "unit": "GB/s",
+            "frac": round(kern[dom]["gbs"] / hbm_peak, 4), "traffic": traffic, "peak_source": peak_kind}
+    scan_gbs = kern.get("scan", {}).get("gbs")
+
+    # ---- CPU oracle baseline (rank 0, N = 1 only) ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(args.config, budget_s=args.cpu_budget)
+
+    if rank == 0:
+        res = {
+            "metric": METRIC, "value": round(us_layer, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": False,
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "u8/f32 (bf16 K,V,q)",
+            "data": "synthetic (LLM-like keys with planted top-k; DESIGN.md recipe), random-init, no weights",
+            "config": {"workload": cfgw["workload"], "batch": batch, "context": ctx, "retrieval_n": n,
+                       "hot_rows": n_hot, "top_k": TOP_K, "probes_T": T, "n_cand": C, "layers": L,
+                       "parallelism": f"seq-shard{world}" if world > 1 else "single",
+                       "l2": "inputs > L2: 32 layer-distinct indices + K/V touched per step",
+                       "cuda_graph": use_graph},
+            "roofline": roof,
+            "scan_gbs": scan_gbs,
+            "kernels": kern,
+            "encode_us_per_layer": round(enc_ms_layer * 1000.0, 2),
+            "encode_gbs": round(batch * N_KV * n_loc * 400 / (enc_ms_layer * 1e-3) / 1e9, 1),
+            "e2e": {"value": round(e2e_ms * 1000.0 / L, 3), "unit": UNIT, "h2d_bytes_per_step": L * batch * N_Q * D * 2,
+                    "d2h_bytes_per_step": L * batch * N_Q * D * 2, "cuda_graph": use_graph,
+                    "eager_value": round(e2e_eager_ms * 1000.0 / L, 3)},
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(res))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# ----------------------------------------------------------------------------------------------- oracle arm
+def oracle_unit(config: str):
+    """One (layer, KV group) unit of the workload for the CPU oracle: returns a callable doing the oracle's
+    decode step (a1, a3-a7) for the G = 4 query heads of one KV head, plus its description."""
+    import torch
+
+    import synth
+    from oracle import levels, pipeline, quantizer
+
+    cfgw = CONFIGS[config]
+    n = cfgw["context"] - (N_SINK + N_LOCAL)
+    seed = 0
+    stats = synth.head_stats(seed, N_KV)
+    K = synth.llm_keys(seed, 1, N_KV, n, stats=stats)
+    q = synth.llm_queries(seed, 1, N_Q, N_KV, stats=stats)
+    synth.plant(K, q, seed)
+    V = synth.values(seed, 1, N_KV, n)
+    Kh = synth.isotropic(seed + 7, (1, N_KV, N_SINK + N_LOCAL, D))
+    Vh = synth.isotropic(seed + 8, (1, N_KV, N_SINK + N_LOCAL, D))
+    sb = synth.rotation_sign_bits()
+    L32 = levels.levels_f32(8)
+    Kf = synth.to_f64(K[0, 0])
+    meta = quantizer.encode_keys(Kf, sb, L32, levels.mid_sq(L32))
+    Q = synth.to_f64(q[0, :4])
+    Vf, Khf, Vhf = synth.to_f64(V[0, 0]), synth.to_f64(Kh[0, 0]), synth.to_f64(Vh[0, 0])
+    del torch
+
+    def unit():
+        res = pipeline.decode_step(meta, Q, sb, TOP_K)
+        for h, r in enumerate(res):
+            pipeline.attend(Q[h], Kf, Vf, r["idx"], Khf, Vhf)
+
+    return unit, f"1 KV group (4 q heads) x 1 layer of {config} (n={n}), x{N_KV} groups -> us/layer (extrapolated)"
+
+
+def cpu_baseline(config: str, budget_s: float = 20.0):
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(1):
+        unit, desc = oracle_unit(config)
+        unit()  # warm
+        t0 = time.perf_counter()
+        reps = 0
+        while True:
+            unit()
+            reps += 1
+            if time.perf_counter() - t0 > budget_s / 2 or reps >= 20:
+                break
+        dt = (time.perf_counter() - t0) / reps
+    return {"value": round(dt * N_KV * 1e6, 1), "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{desc}; {reps} reps, numpy/BLAS limited to 1 thread",
+            "cpu": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(1):
+        unit, desc = oracle_unit(args.config)
+        for _ in range(args.warmup):
+            unit()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            unit()
+        dt = (time.perf_counter() - t0) / args.steps
+    v = round(dt * N_KV * 1e6, 1)
+    cfgw = CONFIGS[args.config]
+    res = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(dt * N_KV * N_LAYERS * 1e3, 3), "higher_is_better": False,
+           "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (same recipe as the GPU arm)",
+           "config": {"workload": cfgw["workload"], "batch": cfgw["batch"], "context": cfgw["context"],
+                      "top_k": TOP_K, "layers": N_LAYERS},
+           "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                            "sample": f"each step: {desc}", "cpu": _cpu_model()},
+           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(res))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="128k", choices=sorted(CONFIGS))
+    ap.add_argument("--layers", type=int, default=N_LAYERS)
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup) if args.impl == "ours" else args.warmup
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,213 @@
+/*
+ * pariskv.h — C ABI of the B200 (sm_100a) ParisKV decode-time KV-cache retrieval hot path.
+ *
+ * ParisKV: "Fast and Drift-Robust KV-Cache Retrieval for Long-Context LLMs" (arXiv 2602.07721).
+ * Citations: P:n = PAPER.md line n (section / equation), S:n = SPEC.md line n, AMB-x = a reading of
+ * the paper listed in DESIGN.md.
+ *
+ * The four calls of the hot path:
+ *   encode_keys          prefill key summarisation (§4.1)
+ *   append_decode_keys   sliding-window flush: encode evicted keys and append them
+ *   retrieve_topk        per decode step: query prep, collision voting, bucket_topk, RSQ-IP rerank,
+ *                        final top-k (Eq. 10)
+ *   sparse_attend        attention over hot rows U retrieved rows, K/V in HBM or pinned host memory
+ *                        read through UVA (Eq. 2-3)
+ *
+ * Conventions shared by every entry point
+ *   - Every function returns pkv_status (0 = PKV_OK). No C++ exception crosses the ABI.
+ *     pkv_last_error() returns a thread-local message for the last non-OK status.
+ *   - Argument errors (PKV_ERR_INVALID_ARG, PKV_ERR_CAPACITY) are detected on the host before any work
+ *     is enqueued: a failing call has no side effect.
+ *   - Ownership: the caller owns every input and output buffer (q, K, V, hot rows, idx, est, out, lse) and
+ *     keeps it alive until the stream work completes. The library owns the index metadata (centroid ids,
+ *     4-bit codes, weights), the per-index workspace and the NCCL communicator.
+ *   - Streams: all device work is enqueued on the caller's stream. retrieve_topk and sparse_attend perform
+ *     no host synchronisation and no allocation, so they can be captured in a CUDA graph.
+ *     Asynchronous device faults surface at the caller's next synchronisation (PKV_ERR_CUDA is returned
+ *     only for launch-time errors).
+ *   - Dtypes: K, V, q and hot rows are bf16 (reading AMB-21). Head dim D = 128, B = 16 subspaces of
+ *     m = 8 dimensions, 256 centroids per subspace (the paper's default).
+ *   - Strided K/V layout: element (b, h, t, d) of a [batch][n_kv][tokens][D] tensor is at
+ *     base + b*sb + h*sh + t*st + d (strides in ELEMENTS; d is contiguous). sb, sh, st must be multiples
+ *     of 8 and base 16-byte aligned (16-byte vector loads).
+ *   - GQA: query head h reads KV head h / (n_q_heads / n_kv_heads); retrieval is per query head (AMB-13).
+ */
+#ifndef PARISKV_H
+#define PARISKV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* cudaStream_t;
+
+typedef enum {
+  PKV_OK = 0,
+  PKV_ERR_INVALID_ARG = -1, /* bad pointer, shape, stride, alignment or parameter                 */
+  PKV_ERR_CAPACITY = -2,    /* append would exceed the index capacity (no partial append)          */
+  PKV_ERR_CUDA = -3,        /* CUDA runtime / launch error                                         */
+  PKV_ERR_UNSUPPORTED = -4, /* configuration this build does not implement (e.g. D != 128)         */
+  PKV_ERR_NCCL = -5         /* NCCL error in a sequence-sharded call                                */
+} pkv_status;
+
+#define PKV_HEAD_DIM 128
+#define PKV_SUBSPACES 16
+#define PKV_SUBSPACE_DIM 8
+#define PKV_CENTROIDS 256
+#define PKV_MAX_TIERS 8
+
+/* Offline constants ("an analytic centroid codebook and a quantization configuration").
+ * Fill with pkv_config_init; fields may then be edited (tiers) before pkv_index_create copies it. */
+typedef struct {
+  int32_t head_dim;                  /* D = 128 (only value supported)                                   */
+  int32_t n_subspaces;               /* B = 16                                            */
+  int32_t subspace_dim;              /* m = D/B = 8                                                      */
+  int32_t n_q_heads;                 /* query heads per sequence (e.g. 32)                               */
+  int32_t n_kv_heads;                /* KV heads per sequence (e.g. 8); n_q_heads % n_kv_heads == 0, the  */
+                                     /* GQA group G = n_q/n_kv must be <= 4 (4 heads share a packed u32) */
+  int32_t n_tiers;                   /* multi-tier collision bonus: 6                             */
+  int32_t tier_bonus[PKV_MAX_TIERS]; /* bonus per tier, strictly decreasing, e.g. {6,5,4,3,2,1} (AMB-10) */
+  float mag_levels[8];               /* Prop. 1 magnitude levels L0<...<L7 (AMB-5), fp32       */
+  double mag_mid_sq[7];              /* M_t = ((L_{t-1}+L_t)/2)^2 in fp64, exact from the fp32 levels     */
+  uint8_t rot_sign[PKV_HEAD_DIM];    /* SRHT sign diagonal s_j: 0 -> +1, 1 -> -1 (AMB-1)          */
+  int32_t rot_rounds;                /* 1 (only value supported)                                         */
+} pkv_config;
+
+/* Fill cfg with the paper defaults: D=128, B=16, m=8, 6 tiers {6..1}, Prop. 1 levels for m=8 computed on
+ * the host (conditional means of |u_j| over 8 equal-probability bins of u_j^2 ~ Beta(1/2,(m-1)/2)),
+ * the given head counts and the caller's 128 rotation sign bits (the harness draws them from a seed).
+ * Host-only; no device is touched. */
+pkv_status pkv_config_init(pkv_config* cfg, int32_t n_q_heads, int32_t n_kv_heads, const uint8_t* rot_sign);
+
+/* Adaptive (rho, beta) schedule vs retrieval-zone length n (reading AMB-11 = S:329 in basis points):
+ * T = ceil(rho*256) probes per subspace, C = min(n, max(min(top_k, n), ceil(beta*n))). Host-only. */
+pkv_status pkv_schedule(int64_t n, int32_t top_k, int32_t* probes_T, int64_t* n_cand);
+
+/* ---------------------------------------------------------------------------------------------------
+ * Index: GPU-resident key summaries of the retrieval zone of `batch` sequences x n_kv_heads KV heads
+ * (centroid ids, 4-bit codes, w). Per key and KV head: 16 B of centroid ids + a 128 B rerank
+ * record (64 B packed nibbles + 16 fp32 weights). Device memory is allocated on `device` at creation for
+ * `capacity` keys per (sequence, KV head), together with the retrieval workspace.
+ * ------------------------------------------------------------------------------------------------- */
+typedef struct pkv_index pkv_index;
+
+pkv_status pkv_index_create(const pkv_config* cfg, int32_t batch, int64_t capacity, int32_t device,
+                            pkv_index** out);
+pkv_status pkv_index_destroy(pkv_index* index);
+/* Number of keys per (sequence, KV head) currently in the retrieval zone. */
+pkv_status pkv_index_len(const pkv_index* index, int64_t* n_out);
+/* Let `index` use `donor`'s retrieval workspace instead of its own (frees its own). Both indices must
+ * have the same config head counts and batch, and donor capacity >= index capacity. Work on the two
+ * indices must then be serialised (e.g. one stream for all layers). */
+pkv_status pkv_index_share_workspace(pkv_index* index, pkv_index* donor);
+
+/* (1) encode_keys — prefill (§4.1): encode tokens [0, n) of K (device bf16, layout above,
+ * tokens = retrieval-zone positions) and make them the index content (replaces previous content).
+ * Per key: y' = H (s (.) k) exactly (integer / fp64 Walsh-Hadamard butterflies), centroid id per subspace
+ * = sign pattern (Eq. 6), 3-bit magnitude by the midpoint rule on the Prop. 1 levels (AMB-5), sign bit,
+ * and w_b = ||k|| r_b / alpha_b (Eq. 7, 9) stored pre-divided by ||sign*L[idx]|| (AMB-6).
+ * Errors: INVALID_ARG (null/misaligned K, n < 0), CAPACITY (n > capacity). */
+pkv_status encode_keys(pkv_index* index, const void* K, int64_t sb, int64_t sh, int64_t st, int64_t n,
+                       cudaStream_t stream);
+
+/* (2) append_decode_keys — decode flush: encode t more keys (same layout, token 0 of K is
+ * the new key at retrieval position n) and append them at positions [n, n+t). CAPACITY if n+t > capacity
+ * (nothing appended). */
+pkv_status append_decode_keys(pkv_index* index, const void* K, int64_t sb, int64_t sh, int64_t st, int64_t t,
+                              cudaStream_t stream);
+
+/* Parameters of one retrieval. probes_T and n_cand come from pkv_schedule(n_global, top_k, ...) on the
+ * host (the GLOBAL retrieval length when sequence-sharded). Optional debug outputs (device pointers,
+ * NULL = not written) expose intermediate results for parity tests. */
+typedef struct {
+  int32_t probes_T;     /* T in [1, 256]                                                             */
+  int64_t n_cand;       /* C in [0, n] (global n when sharded)                                      */
+  int32_t top_k;        /* k >= 1                                                                     */
+  uint8_t* dbg_scores;  /* [batch][n_q][n_local] collision scores                              */
+  int32_t* dbg_cand;    /* [batch][n_q][n_cand] candidate ids (global), set semantics, -1 padded      */
+  float* dbg_est;       /* [batch][n_q][n_cand] RSQ-IP estimate aligned with dbg_cand                  */
+  float* dbg_q_rot;     /* [batch][n_q][D] rotated unit query q~ = R q/||q||               */
+} pkv_retrieve_params;
+
+/* (3) retrieve_topk — per decode step. q: device bf16 [batch][n_q][D] contiguous.
+ * Outputs (device): out_idx int32 [batch][n_q][top_k] retrieval-zone token ids (global ids when sharded),
+ * ordered by estimate descending, ties -> larger id, padded with -1 when n < top_k;
+ * out_est fp32 [batch][n_q][top_k] the RSQ-IP estimate of <k, q> (Eq. 10, includes ||q||, AMB-14),
+ * -inf where padded. Requires n >= 1 and n_cand >= min(top_k, n). */
+pkv_status retrieve_topk(pkv_index* index, const void* q, const pkv_retrieve_params* params, int32_t* out_idx,
+                         float* out_est, cudaStream_t stream);
+
+/* (4) sparse_attend — Eq. 2-3 over C(q) = hot rows U {retrieval rows idx[0..k), idx >= 0}:
+ * logits = <k_i, q> * scale in fp32 from the full-precision bf16 rows, softmax, o = sum p_i v_i.
+ * q: device bf16 [batch][n_q][D]. K, V: retrieval-zone rows in the strided layout above; they may be
+ * device pointers or pointers into cudaHostAllocMapped / cudaHostRegister'ed pinned host memory, read by
+ * the kernel through UVA — no copy is made. idx: device int32 [batch][n_q][k] (from
+ * retrieve_topk; -1 entries skipped; ids must be distinct per row). K_hot, V_hot: device bf16
+ * [batch][n_kv][n_hot][D] contiguous (sink + local + update buffer), may be NULL when
+ * n_hot == 0. out: device bf16 [batch][n_q][D]; lse: device fp32 [batch][n_q] = log sum exp(logits)
+ * (natural log), may be NULL. When sequence-sharded, idx holds global ids, K/V are this rank's rows
+ * (local row = id - shard_offset), hot rows are attended by the LAST rank only, and every rank receives
+ * the merged output. INVALID_ARG if k < 0, n_hot < 0, both sets empty, or misaligned pointers. */
+pkv_status sparse_attend(pkv_index* index, const void* q, const void* K, const void* V, int64_t sb, int64_t sh,
+                         int64_t st, const int32_t* idx, int32_t k, const void* K_hot, const void* V_hot,
+                         int32_t n_hot, float scale, void* out, float* lse, cudaStream_t stream);
+
+/* Diagnostics: copy metadata of positions [start, start+count) into caller device buffers in the
+ * canonical layout: ids uint8 [batch][n_kv][count][16] (subspace order), codes uint8
+ * [batch][n_kv][count][64] (coordinate c -> byte c>>1, low nibble for even c; nibble = sign<<3 | idx),
+ * w fp32 [batch][n_kv][count][16] = w_b / ||sign*L[idx]||_b (the stored weight, AMB-6). Any pointer may
+ * be NULL. */
+pkv_status pkv_index_export(const pkv_index* index, int64_t start, int64_t count, uint8_t* ids, uint8_t* codes,
+                            float* w, cudaStream_t stream);
+
+/* ---------------------------------------------------------------------------------------------------
+ * Sequence sharding across GPUs (not in the paper, which is single-GPU).
+ * Rank r owns retrieval positions [shard_offset, shard_offset + n_local) of every sequence/KV head in its
+ * own index. After pkv_comm_init, retrieve_topk and sparse_attend exchange three small messages per call
+ * over NCCL on the caller's stream: per-head score histograms, local top-k lists and partial softmax
+ * states, and return the same results as an unsharded index over the concatenated shards.
+ * ------------------------------------------------------------------------------------------------- */
+/* 128-byte NCCL unique id, to be broadcast from rank 0 to all ranks by the caller. */
+pkv_status pkv_nccl_unique_id(uint8_t out[128]);
+/* Attach a communicator to `index` (collective over `world` ranks; call on every rank). */
+pkv_status pkv_comm_init(pkv_index* index, const uint8_t id[128], int32_t rank, int32_t world,
+                         int64_t shard_offset);
+/* Attach `donor`'s communicator to `index` as well (e.g. one communicator for all layers of a model). The
+ * two indices must then be used from the same stream order on every rank. */
+pkv_status pkv_comm_share(pkv_index* index, pkv_index* donor, int64_t shard_offset);
+/* Single-process emulation for tests: treat `shards[0..P)` (indices on the SAME device, shard p owning
+ * positions [offsets[p], offsets[p]+n_p)) as one sharded index and run the sharded algorithm with the
+ * exchanges done by device copies. Inputs and outputs as retrieve_topk (out_idx/out_est written once). */
+pkv_status pkv_retrieve_topk_sharded_local(pkv_index* const* shards, const int64_t* offsets, int32_t P,
+                                           const void* q, const pkv_retrieve_params* params, int32_t* out_idx,
+                                           float* out_est, cudaStream_t stream);
+/* Same for sparse_attend: Ks[p], Vs[p] are shard p's rows (local row = id - offsets[p]); hot rows belong
+ * to shard P-1. */
+pkv_status pkv_sparse_attend_sharded_local(pkv_index* const* shards, const int64_t* offsets, int32_t P,
+                                           const void* q, const void* const* Ks, const void* const* Vs,
+                                           int64_t sb, int64_t sh, int64_t st, const int32_t* idx, int32_t k,
+                                           const void* K_hot, const void* V_hot, int32_t n_hot, float scale,
+                                           void* out, float* lse, cudaStream_t stream);
+
+/* Total number of kernels this library has launched in the process (host-side counter, for launch
+ * accounting in bench.py; graph replays are not counted). */
+pkv_status pkv_launch_count(uint64_t* total);
+/* Optional per-kernel timing for benchmarks: when enabled, every kernel launch is bracketed by two CUDA
+ * events on its stream (eager launches only; do not enable while capturing a graph). pkv_profile_read
+ * synchronises and returns the launch count and summed device time of one kernel kind; kinds are numbered
+ * 0..12 = encode, qprep, scan, threshold, compact, rerank, topk, topk_merge, attend, combine, head_hist,
+ * export, debug (pkv_kernel_name). Enabling or disabling resets the counters. */
+pkv_status pkv_profile_enable(int32_t on);
+pkv_status pkv_profile_read(int32_t kind, int64_t* launches, double* total_ms);
+const char* pkv_kernel_name(int32_t kind);
+/* Library build/version string. */
+const char* pkv_version(void);
+const char* pkv_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PARISKV_H */

@@ -1,0 +1,497 @@
+// C ABI entry points: validation, index lifetime, and the stream-ordered orchestration of the kernels.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "comm.h"
+#include "internal.h"
+
+namespace pkv {
+
+std::atomic<uint64_t> g_launches{0};
+static thread_local std::string g_err;
+
+pkv_status set_error(pkv_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+pkv_status cuda_status(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return PKV_OK;
+  return set_error(PKV_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+namespace {
+
+constexpr int SEL_STRIDE = 4 + 4 * MAX_CHUNKS;
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+#define PKV_CUDA(expr, what)                                    \
+  do {                                                          \
+    cudaError_t e_ = (expr);                                    \
+    if (e_ != cudaSuccess) return cuda_status(e_, what);        \
+  } while (0)
+
+pkv_status validate_config(const pkv_config* c) {
+  if (!c) return set_error(PKV_ERR_INVALID_ARG, "null config");
+  if (c->head_dim != PKV_HEAD_DIM || c->n_subspaces != PKV_SUBSPACES || c->subspace_dim != PKV_SUBSPACE_DIM)
+    return set_error(PKV_ERR_UNSUPPORTED, "only D=128, B=16, m=8 are supported");
+  if (c->rot_rounds != 1) return set_error(PKV_ERR_UNSUPPORTED, "only rot_rounds=1 is supported");
+  if (c->n_q_heads <= 0 || c->n_kv_heads <= 0 || c->n_q_heads % c->n_kv_heads)
+    return set_error(PKV_ERR_INVALID_ARG, "n_q_heads must be a positive multiple of n_kv_heads");
+  if (c->n_q_heads / c->n_kv_heads > GMAX) return set_error(PKV_ERR_UNSUPPORTED, "GQA group size must be <= 4");
+  if (c->n_tiers < 1 || c->n_tiers > PKV_MAX_TIERS) return set_error(PKV_ERR_INVALID_ARG, "n_tiers out of range");
+  for (int i = 0; i < c->n_tiers; ++i) {
+    if (c->tier_bonus[i] < 1) return set_error(PKV_ERR_INVALID_ARG, "tier bonuses must be >= 1");
+    if (i && c->tier_bonus[i] >= c->tier_bonus[i - 1])
+      return set_error(PKV_ERR_INVALID_ARG, "tier bonuses must be strictly decreasing");
+  }
+  if (c->tier_bonus[0] * PKV_SUBSPACES > HB - 1)
+    return set_error(PKV_ERR_UNSUPPORTED, "max collision score must be <= 127 (tier_bonus[0] <= 7)");
+  for (int i = 0; i < 8; ++i)
+    if (!(c->mag_levels[i] > 0.f) || (i && !(c->mag_levels[i] > c->mag_levels[i - 1])) || !(c->mag_levels[i] < 1.f))
+      return set_error(PKV_ERR_INVALID_ARG, "magnitude levels must be increasing in (0,1)");
+  return PKV_OK;
+}
+
+DevCfg make_devcfg(const pkv_config& c) {
+  DevCfg d;
+  std::memset(&d, 0, sizeof(d));
+  d.n_q = c.n_q_heads;
+  d.n_kv = c.n_kv_heads;
+  d.G = c.n_q_heads / c.n_kv_heads;
+  d.n_tiers = c.n_tiers;
+  for (int i = 0; i < PKV_MAX_TIERS; ++i) d.tier_bonus[i] = c.tier_bonus[i];
+  for (int i = 0; i < 8; ++i) d.levels[i] = c.mag_levels[i];
+  for (int i = 0; i < 7; ++i) d.mid_sq[i] = c.mag_mid_sq[i];
+  for (int j = 0; j < PKV_HEAD_DIM; ++j)
+    if (c.rot_sign[j]) d.sign_mask[j >> 5] |= 1u << (j & 31);
+  return d;
+}
+
+size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+pkv_status alloc_workspace(Workspace* ws, int batch, int n_q, int n_kv, int64_t cap) {
+  ws->batch = batch;
+  ws->n_q = n_q;
+  ws->n_kv = n_kv;
+  ws->cap = cap;
+  const size_t bq = (size_t)batch * n_q, bk = (size_t)batch * n_kv;
+  size_t sizes[14] = {
+      bk * NC * NB * 4,                                  // lut
+      bq * D * 16 * 4,                                   // rtab
+      bq * 4,                                            // qnorm
+      bq * D * 4,                                        // qrot
+      bk * (size_t)cap * 4,                              // scores
+      bk * MAX_CHUNKS * GMAX * HB * 4,                   // chunk_hist
+      (size_t)MAX_RANKS * bq * HB * 4,                   // head_hist
+      bq * SEL_STRIDE * 4,                               // sel
+      bq * (size_t)cap * 4,                              // cand
+      bq * (size_t)cap * 4,                              // est
+      (size_t)MAX_RANKS * bq * MAX_TOPK * 4,             // topk_est
+      (size_t)MAX_RANKS * bq * MAX_TOPK * 4,             // topk_idx
+      (size_t)MAX_RANKS * bq * MAX_SPLITS * PART * 4,    // part
+      0};
+  size_t total = 0;
+  for (size_t s : sizes) total += align_up(s);
+  void* base = nullptr;
+  cudaError_t e = cudaMalloc(&base, total);
+  if (e != cudaSuccess) return cuda_status(e, "workspace cudaMalloc");
+  char* p = static_cast<char*>(base);
+  auto take = [&](int i) {
+    char* r = p;
+    p += align_up(sizes[i]);
+    return r;
+  };
+  ws->lut = reinterpret_cast<uint32_t*>(take(0));
+  ws->rtab = reinterpret_cast<float*>(take(1));
+  ws->qnorm = reinterpret_cast<float*>(take(2));
+  ws->qrot = reinterpret_cast<float*>(take(3));
+  ws->scores = reinterpret_cast<uint32_t*>(take(4));
+  ws->chunk_hist = reinterpret_cast<uint32_t*>(take(5));
+  ws->head_hist = reinterpret_cast<uint32_t*>(take(6));
+  ws->sel = reinterpret_cast<int32_t*>(take(7));
+  ws->cand = reinterpret_cast<int32_t*>(take(8));
+  ws->est = reinterpret_cast<float*>(take(9));
+  ws->topk_est = reinterpret_cast<float*>(take(10));
+  ws->topk_idx = reinterpret_cast<int32_t*>(take(11));
+  ws->part = reinterpret_cast<float*>(take(12));
+  ws->base = base;
+  ws->bytes = total;
+  e = cudaMemset(base, 0, total);
+  if (e != cudaSuccess) return cuda_status(e, "workspace memset");
+  return PKV_OK;
+}
+
+void release_workspace(Workspace* ws) {
+  if (!ws) return;
+  if (--ws->refs == 0) {
+    if (ws->base) cudaFree(ws->base);
+    delete ws;
+  }
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+pkv_status check_kv_layout(const void* K, int64_t sb, int64_t sh, int64_t st, const char* who) {
+  if (!K) return set_error(PKV_ERR_INVALID_ARG, std::string(who) + ": null K/V pointer");
+  if (!aligned16(K)) return set_error(PKV_ERR_INVALID_ARG, std::string(who) + ": K/V must be 16-byte aligned");
+  if (sb < 0 || sh < 0 || st < 0 || (sb % 8) || (sh % 8) || (st % 8))
+    return set_error(PKV_ERR_INVALID_ARG, std::string(who) + ": strides must be non-negative multiples of 8");
+  return PKV_OK;
+}
+
+// -------------------------------------------------------------- retrieval phases (shared by all modes)
+pkv_status phase_scan(pkv_index* ix, const void* q, const pkv_retrieve_params* p, ScanPlan& plan,
+                      cudaStream_t s) {
+  const int64_t n = ix->n;
+  PKV_CUDA(launch_qprep(ix, q, p->probes_T, p->dbg_q_rot, s), "qprep");
+  plan = plan_scan(ix, n > 0 ? n : 1);
+  if (n > 0) {
+    PKV_CUDA(launch_scan(ix, n, plan, s), "scan");
+  } else {
+    PKV_CUDA(cudaMemsetAsync(ix->ws->chunk_hist, 0,
+                             (size_t)ix->batch * ix->cfg.n_kv_heads * MAX_CHUNKS * GMAX * HB * 4, s),
+             "hist clear");
+  }
+  if (p->dbg_scores && n > 0) PKV_CUDA(launch_dbg_scores(ix, n, p->dbg_scores, s), "dbg scores");
+  return PKV_OK;
+}
+
+pkv_status phase_select_rerank(pkv_index* ix, const pkv_retrieve_params* p, const ScanPlan& plan,
+                               const uint32_t* all_hist, int P, int rank, cudaStream_t s) {
+  const int64_t n = ix->n;
+  PKV_CUDA(launch_threshold(ix, plan, all_hist, P, rank, p->n_cand, s), "threshold");
+  if (n > 0) {
+    PKV_CUDA(launch_compact(ix, n, plan, ix->shard_offset, ix->cap, s), "compact");
+    const int64_t cmax = std::min<int64_t>(p->n_cand, n);
+    if (cmax > 0) PKV_CUDA(launch_rerank(ix, cmax, ix->shard_offset, s), "rerank");
+  }
+  return PKV_OK;
+}
+
+pkv_status check_retrieve(const pkv_index* ix, const void* q, const pkv_retrieve_params* p, int64_t n_global,
+                          const int32_t* out_idx, const float* out_est) {
+  if (!ix || !q || !p || !out_idx || !out_est) return set_error(PKV_ERR_INVALID_ARG, "retrieve_topk: null pointer");
+  if (!aligned16(q)) return set_error(PKV_ERR_INVALID_ARG, "retrieve_topk: q must be 16-byte aligned");
+  if (p->probes_T < 1 || p->probes_T > PKV_CENTROIDS)
+    return set_error(PKV_ERR_INVALID_ARG, "retrieve_topk: probes_T out of [1,256]");
+  if (p->top_k < 1 || p->top_k > MAX_TOPK) return set_error(PKV_ERR_INVALID_ARG, "retrieve_topk: top_k out of [1,1024]");
+  if (n_global < 1) return set_error(PKV_ERR_INVALID_ARG, "retrieve_topk: empty retrieval zone");
+  if (p->n_cand < std::min<int64_t>(p->top_k, n_global) || p->n_cand > n_global)
+    return set_error(PKV_ERR_INVALID_ARG, "retrieve_topk: n_cand must be in [min(top_k, n), n]");
+  return PKV_OK;
+}
+
+}  // namespace
+}  // namespace pkv
+
+using namespace pkv;
+
+extern "C" {
+
+const char* pkv_last_error(void) { return g_err.c_str(); }
+const char* pkv_version(void) { return "pariskv-b200 0.1 (sm_100a)"; }
+
+pkv_status pkv_launch_count(uint64_t* total) {
+  if (!total) return set_error(PKV_ERR_INVALID_ARG, "null");
+  *total = g_launches.load();
+  return PKV_OK;
+}
+
+pkv_status pkv_index_create(const pkv_config* cfg, int32_t batch, int64_t capacity, int32_t device, pkv_index** out) {
+  if (!out) return set_error(PKV_ERR_INVALID_ARG, "pkv_index_create: null out");
+  *out = nullptr;
+  pkv_status st = validate_config(cfg);
+  if (st != PKV_OK) return st;
+  if (batch < 1 || capacity < 1 || capacity > (int64_t)INT32_MAX - 1)
+    return set_error(PKV_ERR_INVALID_ARG, "pkv_index_create: batch >= 1 and 1 <= capacity < 2^31 required");
+  int ndev = 0;
+  PKV_CUDA(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+  if (device < 0 || device >= ndev) return set_error(PKV_ERR_INVALID_ARG, "pkv_index_create: bad device");
+  DeviceGuard g(device);
+  pkv_index* ix = new (std::nothrow) pkv_index();
+  if (!ix) return set_error(PKV_ERR_CUDA, "host allocation failed");
+  ix->cfg = *cfg;
+  ix->dcfg = make_devcfg(*cfg);
+  ix->device = device;
+  ix->batch = batch;
+  ix->cap = capacity;
+  cudaDeviceGetAttribute(&ix->num_sms, cudaDevAttrMultiProcessorCount, device);
+  cudaDeviceGetAttribute(&ix->smem_reserved, cudaDevAttrReservedSharedMemoryPerBlock, device);
+  const size_t units = (size_t)batch * cfg->n_kv_heads;
+  cudaError_t e = cudaMalloc(&ix->ids, units * capacity * NB);
+  if (e == cudaSuccess) e = cudaMalloc(&ix->rec, units * capacity * REC);
+  if (e != cudaSuccess) {
+    cudaFree(ix->ids);
+    delete ix;
+    return cuda_status(e, "index cudaMalloc");
+  }
+  ix->ws = new Workspace();
+  ix->ws->device = device;
+  st = alloc_workspace(ix->ws, batch, cfg->n_q_heads, cfg->n_kv_heads, capacity);
+  if (st == PKV_OK) {
+    e = init_scan_attrs();
+    if (e == cudaSuccess) e = init_rerank_attrs();
+    if (e != cudaSuccess) st = cuda_status(e, "cudaFuncSetAttribute");
+  }
+  if (st != PKV_OK) {
+    release_workspace(ix->ws);
+    cudaFree(ix->ids);
+    cudaFree(ix->rec);
+    delete ix;
+    return st;
+  }
+  *out = ix;
+  return PKV_OK;
+}
+
+pkv_status pkv_index_destroy(pkv_index* ix) {
+  if (!ix) return PKV_OK;
+  DeviceGuard g(ix->device);
+  comm_destroy(ix->comm);
+  release_workspace(ix->ws);
+  cudaFree(ix->ids);
+  cudaFree(ix->rec);
+  delete ix;
+  return PKV_OK;
+}
+
+pkv_status pkv_index_len(const pkv_index* ix, int64_t* n_out) {
+  if (!ix || !n_out) return set_error(PKV_ERR_INVALID_ARG, "pkv_index_len: null pointer");
+  *n_out = ix->n;
+  return PKV_OK;
+}
+
+pkv_status pkv_index_share_workspace(pkv_index* ix, pkv_index* donor) {
+  if (!ix || !donor) return set_error(PKV_ERR_INVALID_ARG, "share_workspace: null");
+  if (ix == donor || ix->ws == donor->ws) return PKV_OK;
+  if (ix->device != donor->device || ix->batch != donor->batch || ix->cfg.n_q_heads != donor->cfg.n_q_heads ||
+      ix->cfg.n_kv_heads != donor->cfg.n_kv_heads || donor->ws->cap < ix->cap)
+    return set_error(PKV_ERR_INVALID_ARG, "share_workspace: incompatible donor");
+  DeviceGuard g(ix->device);
+  release_workspace(ix->ws);
+  ix->ws = donor->ws;
+  ix->ws->refs++;
+  return PKV_OK;
+}
+
+pkv_status encode_keys(pkv_index* ix, const void* K, int64_t sb, int64_t sh, int64_t st, int64_t n,
+                       cudaStream_t stream) {
+  if (!ix) return set_error(PKV_ERR_INVALID_ARG, "encode_keys: null index");
+  if (n < 0) return set_error(PKV_ERR_INVALID_ARG, "encode_keys: n < 0");
+  if (n > ix->cap) return set_error(PKV_ERR_CAPACITY, "encode_keys: n exceeds capacity");
+  if (n > 0) {
+    pkv_status s = check_kv_layout(K, sb, sh, st, "encode_keys");
+    if (s != PKV_OK) return s;
+  }
+  DeviceGuard g(ix->device);
+  if (n > 0) PKV_CUDA(launch_encode(ix, K, sb, sh, st, 0, n, stream), "encode");
+  ix->n = n;
+  return PKV_OK;
+}
+
+pkv_status append_decode_keys(pkv_index* ix, const void* K, int64_t sb, int64_t sh, int64_t st, int64_t t,
+                              cudaStream_t stream) {
+  if (!ix) return set_error(PKV_ERR_INVALID_ARG, "append_decode_keys: null index");
+  if (t < 0) return set_error(PKV_ERR_INVALID_ARG, "append_decode_keys: t < 0");
+  if (ix->n + t > ix->cap) return set_error(PKV_ERR_CAPACITY, "append_decode_keys: capacity exceeded");
+  if (t > 0) {
+    pkv_status s = check_kv_layout(K, sb, sh, st, "append_decode_keys");
+    if (s != PKV_OK) return s;
+  }
+  DeviceGuard g(ix->device);
+  if (t > 0) PKV_CUDA(launch_encode(ix, K, sb, sh, st, ix->n, t, stream), "encode(append)");
+  ix->n += t;
+  return PKV_OK;
+}
+
+pkv_status pkv_index_export(const pkv_index* ix, int64_t start, int64_t count, uint8_t* ids, uint8_t* codes, float* w,
+                            cudaStream_t stream) {
+  if (!ix) return set_error(PKV_ERR_INVALID_ARG, "export: null index");
+  if (start < 0 || count < 0 || start + count > ix->n)
+    return set_error(PKV_ERR_INVALID_ARG, "export: range outside [0, n)");
+  DeviceGuard g(ix->device);
+  PKV_CUDA(launch_export(ix, start, count, ids, codes, w, stream), "export");
+  return PKV_OK;
+}
+
+pkv_status retrieve_topk(pkv_index* ix, const void* q, const pkv_retrieve_params* p, int32_t* out_idx, float* out_est,
+                         cudaStream_t stream) {
+  if (!ix) return set_error(PKV_ERR_INVALID_ARG, "retrieve_topk: null index");
+  const int64_t n_global = ix->comm ? comm_global_n(ix) : ix->n;
+  if (n_global < 0) return set_error(PKV_ERR_NCCL, "retrieve_topk: global length exchange failed");
+  pkv_status st = check_retrieve(ix, q, p, n_global, out_idx, out_est);
+  if (st != PKV_OK) return st;
+  DeviceGuard g(ix->device);
+  ScanPlan plan;
+  st = phase_scan(ix, q, p, plan, stream);
+  if (st != PKV_OK) return st;
+  Workspace* ws = ix->ws;
+  const size_t hist_slot = (size_t)ix->batch * ix->cfg.n_q_heads * HB;
+  const size_t topk_slot = (size_t)ix->batch * ix->cfg.n_q_heads * MAX_TOPK;
+  if (ix->comm) {
+    PKV_CUDA(launch_head_hist(ix, plan, ws->head_hist + ix->rank * hist_slot, stream), "head hist");
+    st = comm_allgather_u32(ix, ws->head_hist, hist_slot, stream);
+    if (st != PKV_OK) return st;
+    st = phase_select_rerank(ix, p, plan, ws->head_hist, ix->world, ix->rank, stream);
+    if (st != PKV_OK) return st;
+    PKV_CUDA(launch_topk(ix, p->n_cand, p->top_k, ws->topk_idx + ix->rank * topk_slot,
+                         ws->topk_est + ix->rank * topk_slot, MAX_TOPK, stream),
+             "topk");
+    st = comm_allgather_u32(ix, reinterpret_cast<uint32_t*>(ws->topk_idx), topk_slot, stream);
+    if (st == PKV_OK) st = comm_allgather_u32(ix, reinterpret_cast<uint32_t*>(ws->topk_est), topk_slot, stream);
+    if (st != PKV_OK) return st;
+    PKV_CUDA(launch_topk_merge(ix, ix->world, p->top_k, ws->topk_est, ws->topk_idx, out_idx, out_est, stream),
+             "topk merge");
+  } else {
+    st = phase_select_rerank(ix, p, plan, nullptr, 1, 0, stream);
+    if (st != PKV_OK) return st;
+    PKV_CUDA(launch_topk(ix, p->n_cand, p->top_k, out_idx, out_est, p->top_k, stream), "topk");
+  }
+  if (p->dbg_cand || p->dbg_est) PKV_CUDA(launch_dbg_cand(ix, p->n_cand, p->dbg_cand, p->dbg_est, stream), "dbg cand");
+  return PKV_OK;
+}
+
+pkv_status sparse_attend(pkv_index* ix, const void* q, const void* K, const void* V, int64_t sb, int64_t sh, int64_t st,
+                         const int32_t* idx, int32_t k, const void* K_hot, const void* V_hot, int32_t n_hot,
+                         float scale, void* out, float* lse, cudaStream_t stream) {
+  if (!ix || !q || !out) return set_error(PKV_ERR_INVALID_ARG, "sparse_attend: null pointer");
+  if (k < 0 || n_hot < 0 || k > MAX_TOPK) return set_error(PKV_ERR_INVALID_ARG, "sparse_attend: bad k / n_hot");
+  if (k > 0) {
+    if (!idx) return set_error(PKV_ERR_INVALID_ARG, "sparse_attend: null idx");
+    pkv_status s1 = check_kv_layout(K, sb, sh, st, "sparse_attend(K)");
+    if (s1 != PKV_OK) return s1;
+    s1 = check_kv_layout(V, sb, sh, st, "sparse_attend(V)");
+    if (s1 != PKV_OK) return s1;
+  }
+  if (n_hot > 0 && (!K_hot || !V_hot || !aligned16(K_hot) || !aligned16(V_hot)))
+    return set_error(PKV_ERR_INVALID_ARG, "sparse_attend: bad hot rows");
+  if (k == 0 && n_hot == 0) return set_error(PKV_ERR_INVALID_ARG, "sparse_attend: empty attention set");
+  if (!aligned16(q)) return set_error(PKV_ERR_INVALID_ARG, "sparse_attend: q must be 16-byte aligned");
+  DeviceGuard g(ix->device);
+  const int G = ix->dcfg.G;
+  const int splits = plan_attend_splits(ix, n_hot + G * k);
+  const bool last = !ix->comm || ix->rank == ix->world - 1;
+  AttendArgs a{q, K, V, sb, sh, st, idx, k, K_hot, V_hot, last ? n_hot : 0, scale,
+               ix->comm ? ix->shard_offset : 0, ix->comm ? ix->shard_offset + ix->n : INT64_MAX,
+               ix->comm ? ix->shard_offset : 0};
+  Workspace* ws = ix->ws;
+  const size_t part_slot = (size_t)ix->batch * ix->cfg.n_q_heads * MAX_SPLITS * PART;
+  const int slot = ix->comm ? ix->rank : 0;
+  PKV_CUDA(launch_attend_partial(ix, a, splits, ws->part + slot * part_slot, stream), "attend");
+  if (ix->comm) {
+    pkv_status s2 = comm_allgather_u32(ix, reinterpret_cast<uint32_t*>(ws->part), part_slot, stream);
+    if (s2 != PKV_OK) return s2;
+  }
+  PKV_CUDA(launch_attend_combine(ix, ws->part, splits, ix->comm ? ix->world : 1, out, lse, stream), "combine");
+  return PKV_OK;
+}
+
+// ---------------------------------------------------------------- single-process sharded emulation
+pkv_status pkv_retrieve_topk_sharded_local(pkv_index* const* shards, const int64_t* offsets, int32_t P, const void* q,
+                                           const pkv_retrieve_params* p, int32_t* out_idx, float* out_est,
+                                           cudaStream_t stream) {
+  if (!shards || !offsets || P < 1 || P > MAX_RANKS)
+    return set_error(PKV_ERR_INVALID_ARG, "sharded_local: need 1 <= P <= 8 shards");
+  int64_t n_global = 0;
+  for (int r = 0; r < P; ++r) {
+    if (!shards[r] || shards[r]->device != shards[0]->device || shards[r]->batch != shards[0]->batch ||
+        shards[r]->comm || (r && shards[r]->ws == shards[0]->ws))
+      return set_error(PKV_ERR_INVALID_ARG, "sharded_local: shards must be distinct, same device/batch, own workspace");
+    if (offsets[r] != n_global) return set_error(PKV_ERR_INVALID_ARG, "sharded_local: offsets must be contiguous");
+    n_global += shards[r]->n;
+  }
+  pkv_status st = check_retrieve(shards[0], q, p, n_global, out_idx, out_est);
+  if (st != PKV_OK) return st;
+  DeviceGuard g(shards[0]->device);
+  Workspace* w0 = shards[0]->ws;
+  const size_t hist_slot = (size_t)shards[0]->batch * shards[0]->cfg.n_q_heads * HB;
+  const size_t topk_slot = (size_t)shards[0]->batch * shards[0]->cfg.n_q_heads * MAX_TOPK;
+  ScanPlan plans[MAX_RANKS];
+  for (int r = 0; r < P; ++r) {
+    shards[r]->shard_offset = offsets[r];
+    pkv_retrieve_params pr = *p;
+    pr.dbg_scores = nullptr;
+    pr.dbg_cand = nullptr;
+    pr.dbg_est = nullptr;
+    if (r) pr.dbg_q_rot = nullptr;
+    st = phase_scan(shards[r], q, &pr, plans[r], stream);
+    if (st != PKV_OK) return st;
+    PKV_CUDA(launch_head_hist(shards[r], plans[r], w0->head_hist + r * hist_slot, stream), "head hist");
+  }
+  for (int r = 0; r < P; ++r) {
+    st = phase_select_rerank(shards[r], p, plans[r], w0->head_hist, P, r, stream);
+    if (st != PKV_OK) return st;
+    PKV_CUDA(launch_topk(shards[r], p->n_cand, p->top_k, w0->topk_idx + r * topk_slot, w0->topk_est + r * topk_slot,
+                         MAX_TOPK, stream),
+             "topk");
+  }
+  PKV_CUDA(launch_topk_merge(shards[0], P, p->top_k, w0->topk_est, w0->topk_idx, out_idx, out_est, stream), "merge");
+  for (int r = 0; r < P; ++r) shards[r]->shard_offset = 0;
+  return PKV_OK;
+}
+
+pkv_status pkv_sparse_attend_sharded_local(pkv_index* const* shards, const int64_t* offsets, int32_t P, const void* q,
+                                           const void* const* Ks, const void* const* Vs, int64_t sb, int64_t sh,
+                                           int64_t st, const int32_t* idx, int32_t k, const void* K_hot,
+                                           const void* V_hot, int32_t n_hot, float scale, void* out, float* lse,
+                                           cudaStream_t stream) {
+  if (!shards || !offsets || !Ks || !Vs || P < 1 || P > MAX_RANKS || !q || !out)
+    return set_error(PKV_ERR_INVALID_ARG, "attend_sharded_local: bad arguments");
+  if (k < 0 || n_hot < 0 || k > MAX_TOPK || (k == 0 && n_hot == 0))
+    return set_error(PKV_ERR_INVALID_ARG, "attend_sharded_local: bad k / n_hot");
+  for (int r = 1; r < P; ++r)
+    if (!shards[r] || shards[r]->ws == shards[0]->ws || shards[r]->device != shards[0]->device)
+      return set_error(PKV_ERR_INVALID_ARG, "attend_sharded_local: shards need their own workspace");
+  DeviceGuard g(shards[0]->device);
+  const int G = shards[0]->dcfg.G;
+  const int splits = plan_attend_splits(shards[0], n_hot + G * k);
+  Workspace* w0 = shards[0]->ws;
+  const size_t part_slot = (size_t)shards[0]->batch * shards[0]->cfg.n_q_heads * MAX_SPLITS * PART;
+  for (int r = 0; r < P; ++r) {
+    if (k > 0) {
+      pkv_status s1 = check_kv_layout(Ks[r], sb, sh, st, "attend_sharded_local(K)");
+      if (s1 == PKV_OK) s1 = check_kv_layout(Vs[r], sb, sh, st, "attend_sharded_local(V)");
+      if (s1 != PKV_OK) return s1;
+    }
+    AttendArgs a{q, Ks[r], Vs[r], sb, sh, st, idx, k, K_hot, V_hot, r == P - 1 ? n_hot : 0, scale, offsets[r],
+                 offsets[r] + shards[r]->n, offsets[r]};
+    PKV_CUDA(launch_attend_partial(shards[r], a, splits, w0->part + r * part_slot, stream), "attend");
+  }
+  PKV_CUDA(launch_attend_combine(shards[0], w0->part, splits, P, out, lse, stream), "combine");
+  return PKV_OK;
+}
+
+pkv_status pkv_nccl_unique_id(uint8_t out[128]) { return comm_unique_id(out); }
+
+pkv_status pkv_comm_init(pkv_index* ix, const uint8_t id[128], int32_t rank, int32_t world, int64_t shard_offset) {
+  if (!ix || !id || world < 1 || world > MAX_RANKS || rank < 0 || rank >= world || shard_offset < 0)
+    return set_error(PKV_ERR_INVALID_ARG, "pkv_comm_init: bad arguments (world must be in [1, 8])");
+  DeviceGuard g(ix->device);
+  return comm_init(ix, id, rank, world, shard_offset);
+}
+
+pkv_status pkv_comm_share(pkv_index* ix, pkv_index* donor, int64_t shard_offset) {
+  if (!ix || !donor || shard_offset < 0) return set_error(PKV_ERR_INVALID_ARG, "pkv_comm_share: bad arguments");
+  if (ix->device != donor->device) return set_error(PKV_ERR_INVALID_ARG, "pkv_comm_share: different devices");
+  return comm_share(ix, donor, shard_offset);
+}
+
+}  // extern "C"

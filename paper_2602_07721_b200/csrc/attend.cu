@@ -1,0 +1,212 @@
+// Gather + sparse attention (a7): Eq. 2-3 over hot rows U retrieved rows, with the full-precision
+// K/V rows read either from HBM or, for the million-token offload case, directly from pinned host memory
+// through UVA ("(iv) a UVA-based kernel") — no staging copy.
+//
+// attend_partial_kernel  grid (splits, n_kv, batch), 4 warps. Work items of one (sequence, KV head): the n_hot hot
+//                        rows (each scored against the G query heads of the group: read once, used G times) and
+//                        the G*k retrieved rows (each for its own query head). A warp keeps an online-softmax
+//                        state (m, l, o) per query head in the log2 domain; lane L owns dims 4L..4L+3; rows are
+//                        fetched 4 items at a time (8 x 8-byte loads in flight per lane) to cover UVA latency.
+//                        Emits one partial (m, l, o[128]) per (query head, split).
+// attend_combine_kernel  LSE merge of the partials (all splits, all ranks when sharded) -> bf16 out, natural lse.
+#include "common.cuh"
+
+namespace pkv {
+namespace {
+
+constexpr int AT_WARPS = 4;
+constexpr int AT_BATCH = 4;
+constexpr float LOG2E = 1.4426950408889634f;
+
+__device__ __forceinline__ float4 bf16x4(uint2 w) {
+  return make_float4(bf16_lo(w.x), bf16_hi(w.x), bf16_lo(w.y), bf16_hi(w.y));
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int x = 16; x > 0; x >>= 1) v += __shfl_xor_sync(0xffffffffu, v, x);
+  return v;
+}
+
+struct SoftState {
+  float m, l, o[4];
+};
+
+__device__ __forceinline__ void soft_update(SoftState& s, float x, const float4& v) {
+  const float mn = fmaxf(s.m, x);
+  const float c = exp2f(s.m - mn);
+  const float p = exp2f(x - mn);
+  s.l = s.l * c + p;
+  s.o[0] = s.o[0] * c + p * v.x;
+  s.o[1] = s.o[1] * c + p * v.y;
+  s.o[2] = s.o[2] * c + p * v.z;
+  s.o[3] = s.o[3] * c + p * v.w;
+  s.m = mn;
+}
+
+__global__ void __launch_bounds__(AT_WARPS * 32) attend_partial_kernel(AttendArgs a, int n_q, int n_kv, int G,
+                                                                       int items_per_split, float* __restrict__ part) {
+  __shared__ float sm_m[AT_WARPS][GMAX], sm_l[AT_WARPS][GMAX];
+  __shared__ float sm_o[AT_WARPS][GMAX][D];
+  const int split = blockIdx.x, g = blockIdx.y, b = blockIdx.z;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const float qscale = a.scale * LOG2E;
+  float4 qv[GMAX];
+#pragma unroll
+  for (int hh = 0; hh < GMAX; ++hh) {
+    if (hh < G) {
+      const uint16_t* qp = static_cast<const uint16_t*>(a.q) + ((int64_t)b * n_q + g * G + hh) * D + 4 * lane;
+      const float4 f = bf16x4(ldg_v2(qp));
+      qv[hh] = make_float4(f.x * qscale, f.y * qscale, f.z * qscale, f.w * qscale);
+    } else {
+      qv[hh] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+  SoftState st[GMAX];
+#pragma unroll
+  for (int hh = 0; hh < GMAX; ++hh) {
+    st[hh].m = -INFINITY;
+    st[hh].l = 0.f;
+    st[hh].o[0] = st[hh].o[1] = st[hh].o[2] = st[hh].o[3] = 0.f;
+  }
+  const int n_items = a.n_hot + G * a.k;
+  const int i0 = split * items_per_split;
+  const int i1 = min(n_items, i0 + items_per_split);
+  const uint16_t* Kb = static_cast<const uint16_t*>(a.K);
+  const uint16_t* Vb = static_cast<const uint16_t*>(a.V);
+  const uint16_t* Kh = static_cast<const uint16_t*>(a.K_hot) + ((int64_t)b * n_kv + g) * a.n_hot * D;
+  const uint16_t* Vh = static_cast<const uint16_t*>(a.V_hot) + ((int64_t)b * n_kv + g) * a.n_hot * D;
+  for (int base = i0 + warp * AT_BATCH; base < i1; base += AT_WARPS * AT_BATCH) {
+    uint2 kr[AT_BATCH], vr[AT_BATCH];
+    int head[AT_BATCH];  // -1: hot row (all heads), -2: skip, else query head within the group
+#pragma unroll
+    for (int u = 0; u < AT_BATCH; ++u) {
+      const int it = base + u;
+      head[u] = -2;
+      kr[u] = make_uint2(0, 0);
+      vr[u] = make_uint2(0, 0);
+      if (it < i1) {
+        if (it < a.n_hot) {
+          head[u] = -1;
+          kr[u] = ldg_v2(Kh + (int64_t)it * D + 4 * lane);
+          vr[u] = ldg_v2(Vh + (int64_t)it * D + 4 * lane);
+        } else {
+          const int r = it - a.n_hot;
+          const int hh = r / a.k, j = r % a.k;
+          const int id = a.idx[((int64_t)b * n_q + g * G + hh) * a.k + j];
+          if (id >= 0 && id >= a.own_lo && id < a.own_hi) {
+            head[u] = hh;
+            const int64_t row = (int64_t)id - a.id_offset;
+            const int64_t off = (int64_t)b * a.sb + (int64_t)g * a.sh + row * a.st + 4 * lane;
+            kr[u] = ldg_v2(Kb + off);
+            vr[u] = ldg_v2(Vb + off);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < AT_BATCH; ++u) {
+      if (head[u] == -2) continue;
+      const float4 kf = bf16x4(kr[u]);
+      const float4 vf = bf16x4(vr[u]);
+#pragma unroll
+      for (int hh = 0; hh < GMAX; ++hh) {
+        if (hh >= G) break;
+        if (head[u] != -1 && head[u] != hh) continue;
+        float d = kf.x * qv[hh].x + kf.y * qv[hh].y + kf.z * qv[hh].z + kf.w * qv[hh].w;
+        d = warp_sum(d);
+        soft_update(st[hh], d, vf);
+      }
+    }
+  }
+  // merge the 4 warps' states
+#pragma unroll
+  for (int hh = 0; hh < GMAX; ++hh) {
+    if (lane == 0) {
+      sm_m[warp][hh] = st[hh].m;
+      sm_l[warp][hh] = st[hh].l;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) sm_o[warp][hh][4 * lane + i] = st[hh].o[i];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < G * D; e += AT_WARPS * 32) {
+    const int hh = e / D, d = e % D;
+    float M = -INFINITY;
+    for (int w = 0; w < AT_WARPS; ++w) M = fmaxf(M, sm_m[w][hh]);
+    float L = 0.f, O = 0.f;
+    if (M != -INFINITY) {
+      for (int w = 0; w < AT_WARPS; ++w) {
+        const float c = exp2f(sm_m[w][hh] - M);
+        L += sm_l[w][hh] * c;
+        O += sm_o[w][hh][d] * c;
+      }
+    }
+    float* p = part + (((int64_t)b * n_q + g * G + hh) * MAX_SPLITS + split) * PART;
+    if (d == 0) {
+      p[0] = M;
+      p[1] = L;
+    }
+    p[2 + d] = O;
+  }
+}
+
+__global__ void __launch_bounds__(D) attend_combine_kernel(const float* __restrict__ parts, int nsplits, int P,
+                                                            int64_t rank_stride, int n_q, void* out, float* lse) {
+  const int h = blockIdx.x, b = blockIdx.y, d = threadIdx.x;
+  const int64_t bhq = (int64_t)b * n_q + h;
+  float M = -INFINITY;
+  for (int r = 0; r < P; ++r)
+    for (int s = 0; s < nsplits; ++s) M = fmaxf(M, parts[r * rank_stride + (bhq * MAX_SPLITS + s) * PART]);
+  float L = 0.f, O = 0.f;
+  if (M != -INFINITY) {
+    for (int r = 0; r < P; ++r) {
+      for (int s = 0; s < nsplits; ++s) {
+        const float* p = parts + r * rank_stride + (bhq * MAX_SPLITS + s) * PART;
+        const float m = p[0];
+        if (m == -INFINITY) continue;
+        const float c = exp2f(m - M);
+        L += p[1] * c;
+        O += p[2 + d] * c;
+      }
+    }
+  }
+  const float o = L > 0.f ? O / L : 0.f;
+  static_cast<__nv_bfloat16*>(out)[bhq * D + d] = __float2bfloat16_rn(o);
+  if (lse && d == 0) lse[bhq] = L > 0.f ? (M + log2f(L)) * 0.6931471805599453f : -INFINITY;
+}
+
+}  // namespace
+
+int plan_attend_splits(const pkv_index* ix, int total_items) {
+  const int units = ix->batch * ix->cfg.n_kv_heads;
+  int splits = (2 * ix->num_sms + units - 1) / units;
+  const int max_by_items = (total_items + 15) / 16;
+  if (splits > max_by_items) splits = max_by_items;
+  if (splits > MAX_SPLITS) splits = MAX_SPLITS;
+  if (splits < 1) splits = 1;
+  return splits;
+}
+
+cudaError_t launch_attend_partial(const pkv_index* ix, const AttendArgs& a, int splits, float* part_out,
+                                  cudaStream_t stream) {
+  const int G = ix->dcfg.G;
+  const int n_items = a.n_hot + G * a.k;
+  const int per = (n_items + splits - 1) / splits;
+  dim3 grid(splits, ix->cfg.n_kv_heads, ix->batch);
+  ProfScope p_(K_ATTEND, stream);
+  attend_partial_kernel<<<grid, AT_WARPS * 32, 0, stream>>>(a, ix->cfg.n_q_heads, ix->cfg.n_kv_heads, G,
+                                                            per > 0 ? per : 1, part_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_attend_combine(const pkv_index* ix, const float* parts, int nsplits, int P, void* out, float* lse,
+                                  cudaStream_t stream) {
+  dim3 grid(ix->cfg.n_q_heads, ix->batch);
+  const int64_t rank_stride = (int64_t)ix->batch * ix->cfg.n_q_heads * MAX_SPLITS * PART;
+  ProfScope p_(K_COMBINE, stream);
+  attend_combine_kernel<<<grid, D, 0, stream>>>(parts, nsplits, P, rank_stride, ix->cfg.n_q_heads, out, lse);
+  return cudaGetLastError();
+}
+
+}  // namespace pkv

@@ -1,0 +1,214 @@
+// Key encoder: prefill summarisation and decode-flush append (PAPER §4.1).
+//
+// One half-warp per key, lane b = subspace b (coordinates 8b..8b+7). Per key:
+//   y' = H (s (.) k)  — the SRHT rotation as radix-2 Walsh-Hadamard butterflies, computed EXACTLY:
+//       fast path: block-floating-point int32 butterflies (exact when every nonzero element of the key is
+//       within 16 binades of the largest; 255*2^16*128 < 2^31), else fp64 butterflies in the oracle's order
+//       (bit-identical to the oracle in every case).
+//   S_b = fp64 left-to-right sum of y_j^2; centroid id = sign pattern (Eq. 6); 3-bit magnitude by the
+//   midpoint rule y_j^2 >= M_t S_b on the Prop. 1 levels (AMB-5) — the fp64 op sequence of the oracle.
+//   w'_b = w_b / ||sign*L[idx]|| = S_b / (sqrt(128) <sign*L[idx], y_b>)  (Eq. 7, 9 with AMB-6; alpha clamp 1e-3)
+// Bytes per key: 256 in (bf16 K), 144 out (16 ids + 64 nibbles + 64 w'). HBM-bound.
+#include "common.cuh"
+
+namespace pkv {
+namespace {
+
+constexpr int KEYS_PER_BLOCK = 16;  // 256 threads
+
+template <typename T>
+__device__ __forceinline__ T shfl_x(T v, int m) {
+  return __shfl_xor_sync(0xffffffffu, v, m, 16);
+}
+
+// Walsh-Hadamard butterflies over the 128 coordinates held 8-per-lane by a half-warp.
+// Stage order h = 1, 2, 4 (in-lane), 8, 16, 32, 64 (across lanes), pair (i, i+h) -> (a+b, a-b).
+template <typename T>
+__device__ __forceinline__ void fwht128(T v[8], int lane16) {
+#pragma unroll
+  for (int h = 1; h < 8; h <<= 1) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if ((i & h) == 0) {
+        T a = v[i], b = v[i + h];
+        v[i] = a + b;
+        v[i + h] = a - b;
+      }
+    }
+  }
+#pragma unroll
+  for (int x = 1; x < 16; x <<= 1) {
+    const bool upper = (lane16 & x) != 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      T o = shfl_x(v[i], x);
+      v[i] = upper ? (o - v[i]) : (v[i] + o);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) encode_kernel(const uint16_t* __restrict__ K, int64_t sb, int64_t sh,
+                                                     int64_t st, int64_t t0, int64_t count, int n_kv,
+                                                     int64_t cap, int64_t total, DevCfg cfg,
+                                                     uint8_t* __restrict__ ids, uint8_t* __restrict__ rec) {
+  const int lane16 = threadIdx.x & 15;
+  int64_t kk = (int64_t)blockIdx.x * KEYS_PER_BLOCK + (threadIdx.x >> 4);
+  const bool live = kk < total;
+  if (!live) kk = total - 1;  // keep the half-warp shuffles full; results discarded
+  const int64_t tt = kk % count;
+  const int64_t bh = kk / count;
+  const int64_t b = bh / n_kv, h = bh % n_kv;
+  const int64_t t = t0 + tt;
+
+  const uint4 raw = ldg_nc_v4(K + b * sb + h * sh + tt * st + 8 * lane16);
+  const uint32_t w4[4] = {raw.x, raw.y, raw.z, raw.w};
+  uint32_t e[8], mant[8], sgn[8];
+  int emax = 0;
+  bool sub = false;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t bits = (i & 1) ? (w4[i >> 1] >> 16) : (w4[i >> 1] & 0xffffu);
+    e[i] = (bits >> 7) & 0xffu;
+    mant[i] = bits & 0x7fu;
+    sgn[i] = ((bits >> 15) & 1u) ^ (uint32_t)sign_bit(cfg, 8 * lane16 + i);
+    emax = max(emax, (int)e[i]);
+    sub |= (e[i] == 0u && mant[i] != 0u) || e[i] == 0xffu;
+  }
+#pragma unroll
+  for (int x = 1; x < 16; x <<= 1) emax = max(emax, shfl_x(emax, x));
+  bool ok = !sub;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) ok &= (e[i] == 0u) || ((int)e[i] >= emax - 16);
+  const bool warp_ok = __all_sync(0xffffffffu, ok);
+
+  double y[8];
+  if (warp_ok) {
+    int v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int nabs = (e[i] == 0u) ? 0 : (int)((128u | mant[i]) << (e[i] - (uint32_t)emax + 16u));
+      v[i] = sgn[i] ? -nabs : nabs;
+    }
+    fwht128<int>(v, lane16);
+    const double scale = ldexp(1.0, emax - 150);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) y[i] = (double)v[i] * scale;  // exact: |v| < 2^31, power-of-two scale
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t bits = (i & 1) ? (w4[i >> 1] >> 16) : (w4[i >> 1] & 0xffffu);
+      const double x = (double)__uint_as_float(bits << 16);
+      y[i] = sign_bit(cfg, 8 * lane16 + i) ? -x : x;
+    }
+    fwht128<double>(y, lane16);
+  }
+
+  // ---- per-subspace decisions, fp64, fixed op order (no FMA contraction) ----
+  double sq[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) sq[i] = __dmul_rn(y[i], y[i]);
+  double S = sq[0];
+#pragma unroll
+  for (int i = 1; i < 8; ++i) S = __dadd_rn(S, sq[i]);
+  double th[7];
+#pragma unroll
+  for (int i = 0; i < 7; ++i) th[i] = __dmul_rn(cfg.mid_sq[i], S);
+
+  uint32_t id = 0, code = 0;
+  float dot = 0.f, vn2 = 0.f;
+  const bool degenerate = (S == 0.0);
+  // y scaled to a float-safe range for the weight arithmetic (ratios only)
+  int ex = 0;
+  double ymax = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) ymax = fmax(ymax, fabs(y[i]));
+#pragma unroll
+  for (int x = 1; x < 16; x <<= 1) ymax = fmax(ymax, shfl_x(ymax, x));
+  frexp(ymax, &ex);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const bool pos = y[i] >= 0.0;
+    const bool b2 = sq[i] >= th[3];
+    const double t1 = b2 ? th[5] : th[1];
+    const bool b1 = sq[i] >= t1;
+    const double t0v = b2 ? (b1 ? th[6] : th[4]) : (b1 ? th[2] : th[0]);
+    const bool b0 = sq[i] >= t0v;
+    uint32_t idx = 4u * b2 + 2u * b1 + (uint32_t)b0;
+    uint32_t sbit = pos ? 1u : 0u;
+    if (degenerate) {  // AMB-7: encode(e_1)
+      idx = (i == 0) ? 7u : 0u;
+      sbit = 1u;
+    }
+    id |= (pos ? 1u : 0u) << i;
+    code |= ((sbit << 3) | idx) << (4 * i);
+    const float L = cfg.levels[idx];
+    const float yf = (float)ldexp(y[i], -ex);
+    dot = fmaf(sbit ? L : -L, yf, dot);
+    vn2 = fmaf(L, L, vn2);
+  }
+  const float Sf = (float)ldexp(S, -2 * ex);
+  float wprime = 0.f;
+  if (!degenerate) {
+    // alpha = dot / (||v~|| sqrt(S)); clamp at 1e-3 (AMB-6)
+    const bool clamped = (dot <= 0.f) || (dot * dot < 1e-6f * vn2 * Sf);
+    const float w_rel = clamped ? sqrtf(Sf * (1.0f / 128.0f)) / (1e-3f * sqrtf(vn2)) : Sf / (11.313708498984761f * dot);
+    wprime = (float)ldexp((double)w_rel, ex);
+  }
+
+  // ---- stores ----
+  uint32_t idw = 0;
+  const int q = lane16 & 3;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t o = __shfl_sync(0xffffffffu, id, (int)((4 * q + j + t) & 15), 16);
+    idw |= (o & 0xffu) << (8 * j);
+  }
+  if (live) {
+    const int64_t row = (b * n_kv + h) * cap + t;
+    if (lane16 < 4) reinterpret_cast<uint32_t*>(ids + row * NB)[lane16] = idw;
+    uint8_t* r = rec + row * REC;
+    reinterpret_cast<uint32_t*>(r)[lane16] = code;
+    reinterpret_cast<float*>(r + 64)[lane16] = wprime;
+  }
+}
+
+__global__ void export_kernel(const uint8_t* __restrict__ ids_in, const uint8_t* __restrict__ rec_in, int64_t start,
+                              int64_t count, int n_kv, int64_t cap, int64_t total, uint8_t* ids, uint8_t* codes,
+                              float* w) {
+  const int64_t kk = (int64_t)blockIdx.x * 16 + (threadIdx.x >> 4);
+  const int s = threadIdx.x & 15;
+  if (kk >= total) return;
+  const int64_t i = kk % count, bh = kk / count;
+  const int64_t t = start + i;
+  const int64_t row = bh * cap + t;
+  if (ids) ids[kk * NB + s] = ids_in[row * NB + ((s - t) & 15)];
+  if (codes) reinterpret_cast<uint32_t*>(codes + kk * 64)[s] = reinterpret_cast<const uint32_t*>(rec_in + row * REC)[s];
+  if (w) w[kk * NB + s] = reinterpret_cast<const float*>(rec_in + row * REC + 64)[s];
+}
+
+}  // namespace
+
+cudaError_t launch_encode(const pkv_index* ix, const void* K, int64_t sb, int64_t sh, int64_t st, int64_t t0,
+                          int64_t count, cudaStream_t stream) {
+  const int64_t total = (int64_t)ix->batch * ix->cfg.n_kv_heads * count;
+  if (total == 0) return cudaSuccess;
+  const int64_t blocks = (total + KEYS_PER_BLOCK - 1) / KEYS_PER_BLOCK;
+  ProfScope p_(K_ENCODE, stream);
+  encode_kernel<<<(unsigned)blocks, 256, 0, stream>>>(static_cast<const uint16_t*>(K), sb, sh, st, t0, count,
+                                                      ix->cfg.n_kv_heads, ix->cap, total, ix->dcfg, ix->ids,
+                                                      ix->rec);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_export(const pkv_index* ix, int64_t start, int64_t count, uint8_t* ids, uint8_t* codes,
+                          float* w, cudaStream_t stream) {
+  const int64_t total = (int64_t)ix->batch * ix->cfg.n_kv_heads * count;
+  if (total == 0) return cudaSuccess;
+  ProfScope p_(K_EXPORT, stream);
+  export_kernel<<<(unsigned)((total + 15) / 16), 256, 0, stream>>>(ix->ids, ix->rec, start, count,
+                                                                   ix->cfg.n_kv_heads, ix->cap, total, ids,
+                                                                   codes, w);
+  return cudaGetLastError();
+}
+
+}  // namespace pkv

@@ -1,0 +1,158 @@
+// Internal declarations shared by the host side (api.cpp, comm.cpp, levels.cpp) and the kernel
+// launchers (*.cu). Not part of the ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <string>
+
+#include "../../include/pariskv.h"
+
+namespace pkv {
+
+constexpr int D = PKV_HEAD_DIM;        // 128
+constexpr int NB = PKV_SUBSPACES;      // 16 subspaces
+constexpr int M = PKV_SUBSPACE_DIM;    // 8
+constexpr int NC = PKV_CENTROIDS;      // 256 analytic centroids per subspace (Eq. 5)
+constexpr int HB = 128;                // histogram bins (max collision score <= 127)
+constexpr int GMAX = 4;                // query heads per KV head packed in one u32 (bytes)
+constexpr int REC = 128;               // bytes per rerank record: 64 B nibbles + 16 x fp32 w'
+constexpr int MAX_TOPK = 1024;
+constexpr int MAX_CHUNKS = 256;        // scan chunks per (sequence, KV head)
+constexpr int MAX_SPLITS = 64;         // attention split-k partials per (sequence, q head)
+constexpr int PART = D + 2;            // floats per attention partial: m, l, o[128]
+
+// Device-side copy of the offline constants, passed to kernels by value.
+struct DevCfg {
+  int n_q, n_kv, G;
+  int n_tiers;
+  int tier_bonus[PKV_MAX_TIERS];
+  float levels[8];
+  double mid_sq[7];
+  unsigned int sign_mask[4];  // bit d of word d/32 = rot_sign[d]
+};
+
+struct Workspace {
+  int device = -1;
+  int batch = 0, n_q = 0, n_kv = 0;
+  int64_t cap = 0;
+  uint32_t* lut = nullptr;        // [batch][n_kv][256 c][16 s] packed bonuses (byte j = query head g*G+j)
+  float* rtab = nullptr;          // [batch][n_q][128 coord][16 nibble] rerank tables sign*L[idx]*q~
+  float* qnorm = nullptr;         // [batch][n_q]
+  float* qrot = nullptr;          // [batch][n_q][128]
+  uint32_t* scores = nullptr;     // [batch][n_kv][cap] packed collision scores
+  uint32_t* chunk_hist = nullptr; // [batch][n_kv][MAX_CHUNKS][GMAX][HB]
+  uint32_t* head_hist = nullptr;  // [MAX_RANKS][batch][n_q][HB] (per-rank totals; sharded exchange H)
+  int32_t* sel = nullptr;         // [batch][n_q][4 + 4*MAX_CHUNKS] threshold + per-chunk offsets
+  int32_t* cand = nullptr;        // [batch][n_q][cap]
+  float* est = nullptr;           // [batch][n_q][cap]
+  float* topk_est = nullptr;      // [MAX_RANKS][batch][n_q][MAX_TOPK] (sharded exchange T)
+  int32_t* topk_idx = nullptr;    // [MAX_RANKS][batch][n_q][MAX_TOPK]
+  float* part = nullptr;          // [MAX_RANKS][batch][n_q][MAX_SPLITS][PART] (exchange A)
+  void* base = nullptr;
+  size_t bytes = 0;
+  int refs = 1;
+};
+
+constexpr int MAX_RANKS = 8;
+
+struct Comm;  // comm.cpp
+
+}  // namespace pkv
+
+struct pkv_index {
+  pkv_config cfg;
+  pkv::DevCfg dcfg;
+  int device = 0;
+  int batch = 0;
+  int64_t cap = 0;
+  int64_t n = 0;
+  uint8_t* ids = nullptr;   // [batch][n_kv][cap][16]; row of key t rotated left by (t mod 16) bytes
+  uint8_t* rec = nullptr;   // [batch][n_kv][cap][128]
+  pkv::Workspace* ws = nullptr;
+  pkv::Comm* comm = nullptr;
+  int rank = 0, world = 1;
+  int64_t shard_offset = 0;
+  int num_sms = 148;
+  int smem_reserved = 1024;
+};
+
+namespace pkv {
+
+// Kernel kinds for launch accounting / optional event timing (profile.cpp)
+enum KernelKind { K_ENCODE, K_QPREP, K_SCAN, K_THRESHOLD, K_COMPACT, K_RERANK, K_TOPK, K_MERGE, K_ATTEND,
+                  K_COMBINE, K_HEADHIST, K_EXPORT, K_DEBUG, K_NUM_KINDS };
+class ProfScope {  // bracket one kernel launch: counts it, and records events when profiling is on
+ public:
+  ProfScope(int kind, cudaStream_t s);
+  ~ProfScope();
+
+ private:
+  int kind_;
+  cudaStream_t s_;
+  cudaEvent_t a_ = nullptr;
+};
+
+// Error plumbing (api.cpp)
+pkv_status set_error(pkv_status s, const std::string& msg);
+pkv_status cuda_status(cudaError_t e, const char* what);
+extern std::atomic<uint64_t> g_launches;
+
+// Host-side constants (levels.cpp)
+void prop1_levels(int m, double out_levels[8]);
+
+// Launchers (*.cu). All enqueue on `stream` and return the launch error.
+cudaError_t launch_encode(const pkv_index* ix, const void* K, int64_t sb, int64_t sh, int64_t st, int64_t t0,
+                          int64_t count, cudaStream_t stream);
+cudaError_t launch_export(const pkv_index* ix, int64_t start, int64_t count, uint8_t* ids, uint8_t* codes,
+                          float* w, cudaStream_t stream);
+cudaError_t launch_qprep(const pkv_index* ix, const void* q, int T, float* dbg_q_rot, cudaStream_t stream);
+
+struct ScanPlan {
+  int nchunks;
+  int64_t chunk;  // keys per chunk (multiple of 32)
+};
+ScanPlan plan_scan(const pkv_index* ix, int64_t n);
+cudaError_t init_scan_attrs();
+cudaError_t init_rerank_attrs();
+cudaError_t launch_scan(const pkv_index* ix, int64_t n, const ScanPlan& plan, cudaStream_t stream);
+// Per-head totals of the chunk histograms -> head_hist[slot].
+cudaError_t launch_head_hist(const pkv_index* ix, const ScanPlan& plan, uint32_t* head_hist_out,
+                             cudaStream_t stream);
+// Threshold + per-chunk offsets. all_hist: [P][batch][n_q][HB] gathered per-rank totals (P >= 1).
+cudaError_t launch_threshold(const pkv_index* ix, const ScanPlan& plan, const uint32_t* all_hist, int P,
+                             int rank, int64_t C, cudaStream_t stream);
+cudaError_t launch_compact(const pkv_index* ix, int64_t n, const ScanPlan& plan, int64_t id_offset,
+                           int64_t cand_stride, cudaStream_t stream);
+cudaError_t launch_dbg_scores(const pkv_index* ix, int64_t n, uint8_t* out, cudaStream_t stream);
+cudaError_t launch_rerank(const pkv_index* ix, int64_t C_cap, int64_t id_offset, cudaStream_t stream);
+cudaError_t launch_topk(const pkv_index* ix, int64_t C_cap, int k, int32_t* out_idx, float* out_est,
+                        int out_stride, cudaStream_t stream);
+cudaError_t launch_topk_merge(const pkv_index* ix, int P, int k, const float* all_est, const int32_t* all_idx,
+                              int32_t* out_idx, float* out_est, cudaStream_t stream);
+cudaError_t launch_dbg_cand(const pkv_index* ix, int64_t C, int32_t* dbg_cand, float* dbg_est,
+                            cudaStream_t stream);
+
+struct AttendArgs {
+  const void* q;
+  const void* K;
+  const void* V;
+  int64_t sb, sh, st;
+  const int32_t* idx;
+  int k;
+  const void* K_hot;
+  const void* V_hot;
+  int n_hot;
+  float scale;
+  int64_t own_lo, own_hi;  // global ids owned by this shard
+  int64_t id_offset;       // local row = id - id_offset
+};
+int plan_attend_splits(const pkv_index* ix, int total_rows);
+cudaError_t launch_attend_partial(const pkv_index* ix, const AttendArgs& a, int splits, float* part_out,
+                                  cudaStream_t stream);
+cudaError_t launch_attend_combine(const pkv_index* ix, const float* parts, int nsplits, int P, void* out,
+                                  float* lse, cudaStream_t stream);
+
+}  // namespace pkv

@@ -1,0 +1,98 @@
+// Optional per-kernel CUDA-event timing (eager mode only; bench.py uses it for the live roofline numbers).
+// When enabled, every kernel launch is bracketed by two events recorded on the launch stream.
+#include <cuda_runtime.h>
+
+#include <mutex>
+#include <vector>
+
+#include "internal.h"
+
+namespace pkv {
+namespace {
+
+struct Rec {
+  int kind;
+  cudaEvent_t a, b;
+};
+std::mutex g_mu;
+bool g_on = false;
+std::vector<Rec> g_recs;
+std::vector<cudaEvent_t> g_pool;
+int64_t g_count[K_NUM_KINDS] = {};
+double g_ms[K_NUM_KINDS] = {};
+
+cudaEvent_t get_event() {
+  if (!g_pool.empty()) {
+    cudaEvent_t e = g_pool.back();
+    g_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+void drain() {  // caller holds g_mu
+  for (auto& r : g_recs) {
+    float ms = 0.f;
+    cudaEventSynchronize(r.b);
+    if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) {
+      g_count[r.kind]++;
+      g_ms[r.kind] += ms;
+    }
+    g_pool.push_back(r.a);
+    g_pool.push_back(r.b);
+  }
+  g_recs.clear();
+}
+
+const char* kNames[K_NUM_KINDS] = {"encode", "qprep", "scan", "threshold", "compact", "rerank", "topk",
+                                   "topk_merge", "attend", "combine", "head_hist", "export", "debug"};
+
+}  // namespace
+
+ProfScope::ProfScope(int kind, cudaStream_t s) : kind_(kind), s_(s) {
+  if (g_on) {
+    std::lock_guard<std::mutex> l(g_mu);
+    a_ = get_event();
+    cudaEventRecord(a_, s_);
+  }
+}
+
+ProfScope::~ProfScope() {
+  g_launches++;
+  if (a_) {
+    std::lock_guard<std::mutex> l(g_mu);
+    cudaEvent_t b = get_event();
+    cudaEventRecord(b, s_);
+    g_recs.push_back(Rec{kind_, a_, b});
+    if (g_recs.size() > 4096) drain();
+  }
+}
+
+}  // namespace pkv
+
+extern "C" pkv_status pkv_profile_enable(int32_t on) {
+  std::lock_guard<std::mutex> l(pkv::g_mu);
+  pkv::drain();
+  for (int i = 0; i < pkv::K_NUM_KINDS; ++i) {
+    pkv::g_count[i] = 0;
+    pkv::g_ms[i] = 0.0;
+  }
+  pkv::g_on = on != 0;
+  return PKV_OK;
+}
+
+extern "C" pkv_status pkv_profile_read(int32_t kind, int64_t* launches, double* total_ms) {
+  if (kind < 0 || kind >= pkv::K_NUM_KINDS || !launches || !total_ms)
+    return pkv::set_error(PKV_ERR_INVALID_ARG, "pkv_profile_read: bad kind");
+  std::lock_guard<std::mutex> l(pkv::g_mu);
+  pkv::drain();
+  *launches = pkv::g_count[kind];
+  *total_ms = pkv::g_ms[kind];
+  return PKV_OK;
+}
+
+extern "C" const char* pkv_kernel_name(int32_t kind) {
+  return (kind >= 0 && kind < pkv::K_NUM_KINDS) ? pkv::kNames[kind] : "";
+}

@@ -1,0 +1,297 @@
+"""Thin ctypes binding of libpariskv.so (include/pariskv.h). Argument marshalling only: every step of the
+hot path runs in the library's CUDA kernels; torch supplies device memory and streams. There is no CPU
+fallback — importing this module fails loudly when the shared library is missing."""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpariskv.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"libpariskv.so not built ({LIB_PATH}); run `python -m paper_2602_07721_b200.build`")
+_lib = ctypes.CDLL(LIB_PATH)
+
+PKV_OK, PKV_ERR_INVALID_ARG, PKV_ERR_CAPACITY, PKV_ERR_CUDA, PKV_ERR_UNSUPPORTED, PKV_ERR_NCCL = 0, -1, -2, -3, -4, -5
+D = 128
+
+
+class PkvError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"pariskv status {status}: {msg}")
+        self.status = status
+
+
+class Config(ctypes.Structure):
+    _fields_ = [("head_dim", ctypes.c_int32), ("n_subspaces", ctypes.c_int32), ("subspace_dim", ctypes.c_int32),
+                ("n_q_heads", ctypes.c_int32), ("n_kv_heads", ctypes.c_int32), ("n_tiers", ctypes.c_int32),
+                ("tier_bonus", ctypes.c_int32 * 8), ("mag_levels", ctypes.c_float * 8),
+                ("mag_mid_sq", ctypes.c_double * 7), ("rot_sign", ctypes.c_uint8 * 128),
+                ("rot_rounds", ctypes.c_int32)]
+
+
+class RetrieveParams(ctypes.Structure):
+    _fields_ = [("probes_T", ctypes.c_int32), ("n_cand", ctypes.c_int64), ("top_k", ctypes.c_int32),
+                ("dbg_scores", ctypes.c_void_p), ("dbg_cand", ctypes.c_void_p), ("dbg_est", ctypes.c_void_p),
+                ("dbg_q_rot", ctypes.c_void_p)]
+
+
+_vp, _i32, _i64, _f32 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_float
+_sigs = {
+    "pkv_config_init": [ctypes.POINTER(Config), _i32, _i32, _vp],
+    "pkv_schedule": [_i64, _i32, ctypes.POINTER(_i32), ctypes.POINTER(_i64)],
+    "pkv_index_create": [ctypes.POINTER(Config), _i32, _i64, _i32, ctypes.POINTER(_vp)],
+    "pkv_index_destroy": [_vp],
+    "pkv_index_len": [_vp, ctypes.POINTER(_i64)],
+    "pkv_index_share_workspace": [_vp, _vp],
+    "encode_keys": [_vp, _vp, _i64, _i64, _i64, _i64, _vp],
+    "append_decode_keys": [_vp, _vp, _i64, _i64, _i64, _i64, _vp],
+    "retrieve_topk": [_vp, _vp, ctypes.POINTER(RetrieveParams), _vp, _vp, _vp],
+    "sparse_attend": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _i32, _vp, _vp, _i32, _f32, _vp, _vp, _vp],
+    "pkv_index_export": [_vp, _i64, _i64, _vp, _vp, _vp, _vp],
+    "pkv_nccl_unique_id": [_vp],
+    "pkv_comm_init": [_vp, _vp, _i32, _i32, _i64],
+    "pkv_comm_share": [_vp, _vp, _i64],
+    "pkv_retrieve_topk_sharded_local": [_vp, _vp, _i32, _vp, ctypes.POINTER(RetrieveParams), _vp, _vp, _vp],
+    "pkv_sparse_attend_sharded_local": [_vp, _vp, _i32, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _i32, _vp, _vp, _i32,
+                                        _f32, _vp, _vp, _vp],
+    "pkv_launch_count": [ctypes.POINTER(ctypes.c_uint64)],
+    "pkv_profile_enable": [_i32],
+    "pkv_profile_read": [_i32, ctypes.POINTER(_i64), ctypes.POINTER(ctypes.c_double)],
+}
+for _name, _args in _sigs.items():
+    _fn = getattr(_lib, _name)
+    _fn.argtypes = _args
+    _fn.restype = ctypes.c_int
+_lib.pkv_last_error.restype = ctypes.c_char_p
+_lib.pkv_version.restype = ctypes.c_char_p
+_lib.pkv_kernel_name.restype = ctypes.c_char_p
+_lib.pkv_kernel_name.argtypes = [_i32]
+
+EXPORTED = tuple(_sigs) + ("pkv_last_error", "pkv_version", "pkv_kernel_name")
+KERNEL_KINDS = ("encode", "qprep", "scan", "threshold", "compact", "rerank", "topk", "topk_merge", "attend",
+                "combine", "head_hist", "export", "debug")
+
+
+def _check(status: int):
+    if status != PKV_OK:
+        raise PkvError(status, _lib.pkv_last_error().decode())
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def version() -> str:
+    return _lib.pkv_version().decode()
+
+
+def launch_count() -> int:
+    v = ctypes.c_uint64(0)
+    _check(_lib.pkv_launch_count(ctypes.byref(v)))
+    return int(v.value)
+
+
+def profile_enable(on: bool):
+    _check(_lib.pkv_profile_enable(1 if on else 0))
+
+
+def profile_read() -> dict:
+    """{kernel kind: (launches, total device ms)} since the last profile_enable."""
+    out = {}
+    for i, name in enumerate(KERNEL_KINDS):
+        n, ms = _i64(0), ctypes.c_double(0)
+        _check(_lib.pkv_profile_read(i, ctypes.byref(n), ctypes.byref(ms)))
+        if n.value:
+            out[name] = (int(n.value), float(ms.value))
+    return out
+
+
+def config_init(n_q_heads: int, n_kv_heads: int, rot_sign_bits) -> Config:
+    cfg = Config()
+    signs = np.ascontiguousarray(np.asarray(rot_sign_bits, dtype=np.uint8))
+    assert signs.shape == (D,)
+    _check(_lib.pkv_config_init(ctypes.byref(cfg), n_q_heads, n_kv_heads, signs.ctypes.data_as(ctypes.c_void_p)))
+    return cfg
+
+
+def schedule(n: int, top_k: int):
+    T, C = _i32(0), _i64(0)
+    _check(_lib.pkv_schedule(n, top_k, ctypes.byref(T), ctypes.byref(C)))
+    return int(T.value), int(C.value)
+
+
+class Index:
+    """Owns a pkv_index (GPU-resident key summaries of the retrieval zone)."""
+
+    def __init__(self, cfg: Config, batch: int, capacity: int, device: int = 0):
+        self.cfg = cfg
+        self.batch = batch
+        self.capacity = capacity
+        self.device = device
+        self.n_q = cfg.n_q_heads
+        self.n_kv = cfg.n_kv_heads
+        h = _vp()
+        _check(_lib.pkv_index_create(ctypes.byref(cfg), batch, capacity, device, ctypes.byref(h)))
+        self.handle = h
+
+    def close(self):
+        if getattr(self, "handle", None) is not None and self.handle.value:
+            _lib.pkv_index_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __len__(self):
+        n = _i64(0)
+        _check(_lib.pkv_index_len(self.handle, ctypes.byref(n)))
+        return int(n.value)
+
+    def share_workspace(self, donor: "Index"):
+        _check(_lib.pkv_index_share_workspace(self.handle, donor.handle))
+
+    def export(self, start: int = 0, count: int | None = None, stream=None):
+        """Canonical metadata of positions [start, start+count): (ids u8 [b,kv,c,16], codes u8 [b,kv,c,64],
+        w f32 [b,kv,c,16])."""
+        count = len(self) - start if count is None else count
+        dev = torch.device("cuda", self.device)
+        ids = torch.empty(self.batch, self.n_kv, count, 16, dtype=torch.uint8, device=dev)
+        codes = torch.empty(self.batch, self.n_kv, count, 64, dtype=torch.uint8, device=dev)
+        w = torch.empty(self.batch, self.n_kv, count, 16, dtype=torch.float32, device=dev)
+        _check(_lib.pkv_index_export(self.handle, start, count, _ptr(ids), _ptr(codes), _ptr(w), _stream(stream)))
+        return ids, codes, w
+
+
+def _kv_strides(K: torch.Tensor):
+    assert K.dtype == torch.bfloat16 and K.dim() == 4 and K.shape[-1] == D and K.stride(-1) == 1
+    return K.stride(0), K.stride(1), K.stride(2)
+
+
+def encode_keys(index: Index, K: torch.Tensor, n: int | None = None, stream=None):
+    """(1) prefill: K bf16 [batch, n_kv, tokens, 128] (any strides with unit last stride)."""
+    n = K.shape[2] if n is None else n
+    sb, sh, st = _kv_strides(K)
+    _check(_lib.encode_keys(index.handle, _ptr(K), sb, sh, st, n, _stream(stream)))
+
+
+def append_decode_keys(index: Index, K: torch.Tensor, t: int | None = None, stream=None):
+    """(2) decode flush: append the t keys of K bf16 [batch, n_kv, t, 128]."""
+    t = K.shape[2] if t is None else t
+    sb, sh, st = _kv_strides(K)
+    _check(_lib.append_decode_keys(index.handle, _ptr(K), sb, sh, st, t, _stream(stream)))
+
+
+def retrieve_topk(index: Index, q: torch.Tensor, top_k: int, probes_T: int | None = None, n_cand: int | None = None,
+                  n_global: int | None = None, out_idx=None, out_est=None, debug: bool = False, stream=None):
+    """(3) q bf16 [batch, n_q, 128] -> (idx int32 [batch, n_q, k], est f32 [batch, n_q, k], dbg dict|None).
+    probes_T / n_cand default to the library schedule on the (global) retrieval length."""
+    assert q.dtype == torch.bfloat16 and q.is_contiguous() and q.shape[-1] == D
+    n = len(index) if n_global is None else n_global
+    T0, C0 = schedule(n, top_k)
+    T = T0 if probes_T is None else probes_T
+    C = C0 if n_cand is None else n_cand
+    dev = q.device
+    if out_idx is None:
+        out_idx = torch.empty(index.batch, index.n_q, top_k, dtype=torch.int32, device=dev)
+    if out_est is None:
+        out_est = torch.empty(index.batch, index.n_q, top_k, dtype=torch.float32, device=dev)
+    p = RetrieveParams(T, C, top_k, None, None, None, None)
+    dbg = None
+    if debug:
+        nl = len(index)
+        dbg = dict(scores=torch.empty(index.batch, index.n_q, nl, dtype=torch.uint8, device=dev),
+                   cand=torch.empty(index.batch, index.n_q, C, dtype=torch.int32, device=dev),
+                   est=torch.empty(index.batch, index.n_q, C, dtype=torch.float32, device=dev),
+                   q_rot=torch.empty(index.batch, index.n_q, D, dtype=torch.float32, device=dev), T=T, C=C)
+        p.dbg_scores, p.dbg_cand = dbg["scores"].data_ptr(), dbg["cand"].data_ptr()
+        p.dbg_est, p.dbg_q_rot = dbg["est"].data_ptr(), dbg["q_rot"].data_ptr()
+    _check(_lib.retrieve_topk(index.handle, _ptr(q), ctypes.byref(p), _ptr(out_idx), _ptr(out_est), _stream(stream)))
+    return out_idx, out_est, dbg
+
+
+def sparse_attend(index: Index, q: torch.Tensor, K: torch.Tensor | None, V: torch.Tensor | None, idx, K_hot=None,
+                  V_hot=None, scale: float | None = None, out=None, lse=None, strides=None, K_ptr=None, V_ptr=None,
+                  stream=None):
+    """(4) attention over hot rows U retrieved rows. K/V: bf16 [batch, n_kv, tokens, 128] device tensors, or pass
+    raw UVA pointers K_ptr/V_ptr (int) with `strides` (sb, sh, st) for pinned host memory."""
+    k = 0 if idx is None else idx.shape[-1]
+    n_hot = 0 if K_hot is None else K_hot.shape[2]
+    scale = 1.0 / np.sqrt(D) if scale is None else scale
+    if K_ptr is None:
+        if K is not None:
+            sb, sh, st = _kv_strides(K)
+            assert V.stride() == K.stride()
+            K_ptr, V_ptr = K.data_ptr(), V.data_ptr()
+        else:
+            sb = sh = st = 0
+            K_ptr = V_ptr = None
+    else:
+        sb, sh, st = strides
+    if out is None:
+        out = torch.empty(index.batch, index.n_q, D, dtype=torch.bfloat16, device=q.device)
+    if lse is None:
+        lse = torch.empty(index.batch, index.n_q, dtype=torch.float32, device=q.device)
+    if K_hot is not None:
+        assert K_hot.is_contiguous() and V_hot.is_contiguous()
+    _check(_lib.sparse_attend(index.handle, _ptr(q), _vp(K_ptr), _vp(V_ptr), sb, sh, st, _ptr(idx), k,
+                              _ptr(K_hot), _ptr(V_hot), n_hot, scale, _ptr(out), _ptr(lse), _stream(stream)))
+    return out, lse
+
+
+def nccl_unique_id() -> bytes:
+    buf = (ctypes.c_uint8 * 128)()
+    _check(_lib.pkv_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def comm_init(index: Index, uid: bytes, rank: int, world: int, shard_offset: int):
+    buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
+    _check(_lib.pkv_comm_init(index.handle, buf, rank, world, shard_offset))
+
+
+def comm_share(index: Index, donor: Index, shard_offset: int):
+    _check(_lib.pkv_comm_share(index.handle, donor.handle, shard_offset))
+
+
+def retrieve_topk_sharded_local(shards, offsets, q, top_k, n_global, stream=None):
+    P = len(shards)
+    T, C = schedule(n_global, top_k)
+    hs = (_vp * P)(*[s.handle.value for s in shards])
+    offs = (_i64 * P)(*offsets)
+    out_idx = torch.empty(shards[0].batch, shards[0].n_q, top_k, dtype=torch.int32, device=q.device)
+    out_est = torch.empty(shards[0].batch, shards[0].n_q, top_k, dtype=torch.float32, device=q.device)
+    p = RetrieveParams(T, C, top_k, None, None, None, None)
+    _check(_lib.pkv_retrieve_topk_sharded_local(hs, offs, P, _ptr(q), ctypes.byref(p), _ptr(out_idx), _ptr(out_est),
+                                                _stream(stream)))
+    return out_idx, out_est
+
+
+def sparse_attend_sharded_local(shards, offsets, q, Ks, Vs, idx, K_hot=None, V_hot=None, scale=None, stream=None):
+    P = len(shards)
+    k = idx.shape[-1]
+    n_hot = 0 if K_hot is None else K_hot.shape[2]
+    scale = 1.0 / np.sqrt(D) if scale is None else scale
+    sb, sh, st = _kv_strides(Ks[0])
+    hs = (_vp * P)(*[s.handle.value for s in shards])
+    offs = (_i64 * P)(*offsets)
+    kp = (_vp * P)(*[t.data_ptr() for t in Ks])
+    vp = (_vp * P)(*[t.data_ptr() for t in Vs])
+    out = torch.empty(shards[0].batch, shards[0].n_q, D, dtype=torch.bfloat16, device=q.device)
+    lse = torch.empty(shards[0].batch, shards[0].n_q, dtype=torch.float32, device=q.device)
+    _check(_lib.pkv_sparse_attend_sharded_local(hs, offs, P, _ptr(q), kp, vp, sb, sh, st, _ptr(idx), k, _ptr(K_hot),
+                                                _ptr(V_hot), n_hot, scale, _ptr(out), _ptr(lse), _stream(stream)))
+    return out, lse

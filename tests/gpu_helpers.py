@@ -1,0 +1,69 @@
+"""Shared helpers for the -m gpu parity tests: run the oracle on the same seeded inputs the CUDA path gets,
+and the comparison rules of DESIGN.md §Parity (bit-exact codes/scores/candidates; AMB-15/16/17 tolerances)."""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+import synth
+from oracle import coarse, levels, quantizer, rerank
+
+SB = synth.rotation_sign_bits()
+L32 = levels.levels_f32(8)
+MSQ = levels.mid_sq(L32)
+EST_REL = 1e-3          # north star: reranked scores within 1e-3 relative (AMB-15 scaled form)
+ATT_ABS = 2e-3          # north star: attention output within 2e-3 absolute in bf16 (AMB-17)
+
+
+def oracle_meta(K_f64: np.ndarray, exact_codes=False) -> dict:
+    return quantizer.encode_keys(K_f64, SB, L32, MSQ, exact_codes=exact_codes)
+
+
+def est_tol(est_oracle, knorm, qnorm):
+    """AMB-15: |d| <= 1e-3 * max(|est|, 1e-2 ||k|| ||q||)."""
+    return EST_REL * np.maximum(np.abs(est_oracle), 1e-2 * knorm * qnorm)
+
+
+def check_encode(ids_gpu, codes_gpu, w_gpu, meta):
+    """Bit-exact ids and codes; stored weight w' = w / ||sign*L[idx]|| within 1e-5 relative."""
+    assert np.array_equal(ids_gpu, meta["ids"]), "centroid ids differ"
+    assert np.array_equal(codes_gpu, meta["codes"]), "4-bit codes differ"
+    want = meta["w"] / meta["vnorm"]
+    err = np.abs(w_gpu.astype(np.float64) - want)
+    assert np.all(err <= 1e-5 * np.abs(want) + 1e-30), f"w' max rel err {np.max(err / (np.abs(want) + 1e-30))}"
+
+
+def check_topk(idx_gpu, est_gpu, cand, est_or, knorm_by_id, qnorm, k):
+    """AMB-16: GPU top-k set == oracle set except ids whose oracle estimate is within tolerance of the
+    oracle's k-th estimate; GPU estimates of its picks match the oracle within AMB-15; order descending."""
+    idx_o, val_o = rerank.topk(est_or, cand, k)
+    valid_o = idx_o >= 0
+    assert np.array_equal(idx_gpu >= 0, valid_o), "padding differs"
+    by_id = dict(zip(cand.tolist(), est_or.tolist()))
+    g = [int(i) for i in idx_gpu if i >= 0]
+    assert len(set(g)) == len(g)
+    o = [int(i) for i in idx_o if i >= 0]
+    if not o:
+        return
+    kth = val_o[valid_o][-1]
+    for i in set(g) ^ set(o):
+        tol = 2 * est_tol(kth, knorm_by_id[i], qnorm)
+        assert abs(by_id[i] - kth) <= tol, f"top-k differs beyond ties: id {i} est {by_id[i]} kth {kth}"
+    ge = np.array([by_id[i] for i in g])
+    eg = est_gpu[: len(g)].astype(np.float64)
+    tol = est_tol(ge, np.array([knorm_by_id[i] for i in g]), qnorm)
+    assert np.all(np.abs(eg - ge) <= tol)
+    assert np.all(np.diff(eg) <= 0)
+
+
+def bf16_f64(t: torch.Tensor) -> np.ndarray:
+    return synth.to_f64(t)
+
+
+def oracle_retrieval(meta, q_f64, T, C, k):
+    bonus = coarse.query_bonus_tables(q_f64, SB, T)
+    score = coarse.collision_scores(meta["ids"], bonus)
+    cand = coarse.bucket_topk(score, C)
+    qt, qn = rerank.rotated_unit_query(q_f64, SB)
+    est = rerank.estimate(meta, cand, qt, qn)
+    return dict(score=score, cand=cand, est=est, qt=qt, qnorm=qn)

@@ -1,0 +1,299 @@
+"""-m gpu parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded inputs.
+
+Bars: centroid ids, 4-bit codes, collision scores and candidate sets bit-exact;
+weights 1e-5 relative; RSQ-IP estimates within the AMB-15 form of 1e-3 relative; top-k equal up to
+estimate ties (AMB-16); attention within 2e-3 absolute + one bf16 rounding, on the GPU's own index set."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import attention, coarse, pipeline, sharded
+from tests.gpu_helpers import (ATT_ABS, SB, bf16_f64, check_encode, check_topk, oracle_meta, oracle_retrieval)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pkv():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2602_07721_b200 import build
+    build.build()
+    from paper_2602_07721_b200 import pariskv
+    return pariskv
+
+
+def make_problem(seed, batch, n_q, n_kv, n, plant=True, device="cuda"):
+    stats = synth.head_stats(seed, n_kv, device=device)
+    K = synth.llm_keys(seed, batch, n_kv, n, device=device, stats=stats)
+    q = synth.llm_queries(seed, batch, n_q, n_kv, device=device, stats=stats)
+    if plant and n >= 4 * 25 * (n_q // n_kv):
+        synth.plant(K, q, seed)
+    V = synth.values(seed, batch, n_kv, n, device=device)
+    return K, q, V
+
+
+def run_and_check(pkv, K, q, V, k, T=None, C=None, n_hot=0, check_all_heads=True, cfg=None):
+    batch, n_kv, n, _ = K.shape
+    n_q = q.shape[1]
+    G = n_q // n_kv
+    cfg = cfg or pkv.config_init(n_q, n_kv, SB)
+    ix = pkv.Index(cfg, batch, max(n, 1))
+    pkv.encode_keys(ix, K)
+    idx, est, dbg = pkv.retrieve_topk(ix, q, k, probes_T=T, n_cand=C, debug=True)
+    Kh = Vh = None
+    if n_hot:
+        Kh = synth.isotropic(91, (batch, n_kv, n_hot, 128), device="cuda")
+        Vh = synth.isotropic(92, (batch, n_kv, n_hot, 128), device="cuda")
+    out, lse = pkv.sparse_attend(ix, q, K, V, idx, Kh, Vh)
+    ids_g, codes_g, w_g = [t.cpu().numpy() for t in ix.export()]
+    torch.cuda.synchronize()
+    Tn, Cn = dbg["T"], dbg["C"]
+    for b in range(batch):
+        for g in range(n_kv):
+            Kf = bf16_f64(K[b, g])
+            meta = oracle_meta(Kf)
+            check_encode(ids_g[b, g], codes_g[b, g], w_g[b, g], meta)
+            for hh in range(G):
+                h = g * G + hh
+                if not check_all_heads and hh > 0:
+                    continue
+                qf = bf16_f64(q[b, h])
+                r = oracle_retrieval(meta, qf, Tn, Cn, k)
+                assert np.array_equal(dbg["scores"][b, h].cpu().numpy().astype(np.int64), r["score"]), "scores"
+                cg = dbg["cand"][b, h].cpu().numpy()
+                assert np.array_equal(np.sort(cg[cg >= 0]), r["cand"]), "candidate set"
+                assert np.allclose(dbg["q_rot"][b, h].cpu().numpy(), r["qt"], atol=2e-6)
+                # estimates, aligned by id
+                eg = dict(zip(cg.tolist(), dbg["est"][b, h].cpu().numpy().tolist()))
+                eo = r["est"]
+                kn = meta["knorm"][r["cand"]]
+                tol = 1e-3 * np.maximum(np.abs(eo), 1e-2 * kn * r["qnorm"])
+                egv = np.array([eg[int(i)] for i in r["cand"]])
+                assert np.all(np.abs(egv - eo) <= tol), f"est max err {np.max(np.abs(egv - eo) / tol)} x tol"
+                check_topk(idx[b, h].cpu().numpy(), est[b, h].cpu().numpy(), r["cand"], eo,
+                           dict(zip(range(n), meta["knorm"].tolist())), r["qnorm"], k)
+                # attention on the GPU's own index set (AMB-17)
+                ig = idx[b, h].cpu().numpy()
+                o, l = pipeline.attend(qf, Kf, bf16_f64(V[b, g]), ig,
+                                       None if Kh is None else bf16_f64(Kh[b, g]),
+                                       None if Vh is None else bf16_f64(Vh[b, g]))
+                og = out[b, h].float().cpu().numpy()
+                assert np.all(np.abs(og - o) <= ATT_ABS + 2.0 ** -8 * np.abs(o)), f"attn err {np.max(np.abs(og - o))}"
+                assert abs(float(lse[b, h]) - l) <= 1e-3 * max(1.0, abs(l))
+    return ix, idx, est, dbg
+
+
+def test_config1_single_head_4096(pkv):
+    """BASELINE config 1: 1 head, d=128, N=4096, 1 query, top-k=64, paper defaults."""
+    K, q, V = make_problem(1, 1, 1, 1, 4096, plant=False)
+    synth.plant(K, q, 1, n_plant=25)
+    run_and_check(pkv, K, q, V, k=64)
+
+
+def test_gqa_batch_ragged(pkv):
+    K, q, V = make_problem(2, 2, 8, 2, 5003)
+    run_and_check(pkv, K, q, V, k=100, n_hot=37)
+
+
+def test_llama_shape_small_n(pkv):
+    K, q, V = make_problem(3, 1, 32, 8, 3001)
+    run_and_check(pkv, K, q, V, k=100, n_hot=272, check_all_heads=False)
+
+
+@pytest.mark.parametrize("n", [1, 7, 33, 50, 99, 100, 129, 2049])
+def test_tiny_and_ragged_lengths(pkv, n):
+    K, q, V = make_problem(4 + n, 1, 4, 2, n, plant=False)
+    run_and_check(pkv, K, q, V, k=64)
+
+
+def test_group_size_two_and_one(pkv):
+    K, q, V = make_problem(5, 1, 4, 2, 3000, plant=False)
+    run_and_check(pkv, K, q, V, k=32)
+    K, q, V = make_problem(6, 1, 3, 3, 3000, plant=False)
+    run_and_check(pkv, K, q, V, k=32)
+
+
+@pytest.mark.parametrize("T,C", [(1, 100), (256, 900), (26, 3000), (7, 64)])
+def test_probe_and_candidate_extremes(pkv, T, C):
+    K, q, V = make_problem(7, 1, 4, 1, 3000, plant=False)
+    run_and_check(pkv, K, q, V, k=64, T=T, C=C)
+
+
+def test_single_tier_many_ties(pkv):
+    K, q, V = make_problem(8, 1, 4, 1, 6000, plant=False)
+    cfg = pkv.config_init(4, 1, SB)
+    cfg.n_tiers = 1
+    cfg.tier_bonus[0] = 1
+    for i in range(1, 8):
+        cfg.tier_bonus[i] = 0
+    ix = pkv.Index(cfg, 1, 6000)
+    pkv.encode_keys(ix, K)
+    T, C = 26, 500
+    idx, est, dbg = pkv.retrieve_topk(ix, q, 64, probes_T=T, n_cand=C, debug=True)
+    meta = oracle_meta(bf16_f64(K[0, 0]))
+    for h in range(4):
+        qf = bf16_f64(q[0, h])
+        bonus = coarse.query_bonus_tables(qf, SB, T, tier_bonus=(1,))
+        sc = coarse.collision_scores(meta["ids"], bonus)
+        assert sc.max() <= 16
+        assert np.array_equal(dbg["scores"][0, h].cpu().numpy().astype(np.int64), sc)
+        cg = dbg["cand"][0, h].cpu().numpy()
+        assert np.array_equal(np.sort(cg), coarse.bucket_topk(sc, C))
+
+
+def test_degenerate_and_wide_range_keys(pkv):
+    """Zero keys, zero subspaces (AMB-7) and keys spanning > 16 binades (fp64 butterfly fallback)."""
+    K, q, V = make_problem(9, 1, 4, 1, 2048, plant=False)
+    K[0, 0, 5] = 0
+    K[0, 0, 6, 16:24] = 0
+    K[0, 0, 7, :64] = 0
+    K[0, 0, 10:40, 3] = 1e-9
+    K[0, 0, 40:60, 100] = 3e-30
+    K[0, 0, 60:70, :] = torch.randn(10, 128, device="cuda").to(torch.bfloat16) * 1e-20
+    K[0, 0, 70] = -0.0
+    run_and_check(pkv, K, q, V, k=64)
+
+
+def test_append_equals_prefill(pkv):
+    K, q, V = make_problem(10, 1, 8, 2, 4000)
+    cfg = pkv.config_init(8, 2, SB)
+    a = pkv.Index(cfg, 1, 4000)
+    pkv.encode_keys(a, K)
+    b = pkv.Index(cfg, 1, 4000)
+    pkv.encode_keys(b, K[:, :, :1000])
+    for t0 in range(1000, 4000, 512):
+        pkv.append_decode_keys(b, K[:, :, t0:t0 + 512])
+    assert len(b) == 4000
+    for x, y in zip(a.export(), b.export()):
+        assert torch.equal(x, y)
+    ia, ea, _ = pkv.retrieve_topk(a, q, 100)
+    ib, eb, _ = pkv.retrieve_topk(b, q, 100)
+    assert torch.equal(ia, ib) and torch.equal(ea, eb)
+    with pytest.raises(pkv.PkvError) as e:
+        pkv.append_decode_keys(b, K[:, :, :1])
+    assert e.value.status == pkv.PKV_ERR_CAPACITY
+    assert len(b) == 4000
+
+
+def test_strided_kv_layout(pkv):
+    """K as a [batch, tokens, n_kv, D] tensor viewed as [batch, n_kv, tokens, D] (non-contiguous strides)."""
+    K, q, V = make_problem(11, 1, 8, 2, 3000)
+    Kt = K.transpose(1, 2).contiguous().transpose(1, 2)
+    Vt = V.transpose(1, 2).contiguous().transpose(1, 2)
+    assert not Kt.is_contiguous()
+    cfg = pkv.config_init(8, 2, SB)
+    a = pkv.Index(cfg, 1, 3000)
+    pkv.encode_keys(a, K)
+    b = pkv.Index(cfg, 1, 3000)
+    pkv.encode_keys(b, Kt)
+    for x, y in zip(a.export(), b.export()):
+        assert torch.equal(x, y)
+    idx, _, _ = pkv.retrieve_topk(a, q, 100)
+    o1, l1 = pkv.sparse_attend(a, q, K, V, idx)
+    o2, l2 = pkv.sparse_attend(b, q, Kt, Vt, idx)
+    assert torch.equal(o1, o2) and torch.equal(l1, l2)
+
+
+def test_attention_hot_only_and_invalid_args(pkv):
+    K, q, V = make_problem(12, 1, 8, 2, 500, plant=False)
+    cfg = pkv.config_init(8, 2, SB)
+    ix = pkv.Index(cfg, 1, 500)
+    pkv.encode_keys(ix, K)
+    Kh, Vh = K[:, :, :300].contiguous(), V[:, :, :300].contiguous()
+    out, lse = pkv.sparse_attend(ix, q, None, None, None, Kh, Vh)
+    for h in range(8):
+        o, l = attention.full_attention(bf16_f64(q[0, h]), bf16_f64(Kh[0, h // 4]), bf16_f64(Vh[0, h // 4]),
+                                        1 / np.sqrt(128))
+        assert np.all(np.abs(out[0, h].float().cpu().numpy() - o) <= ATT_ABS + 2.0 ** -8 * np.abs(o))
+    with pytest.raises(pkv.PkvError):
+        pkv.sparse_attend(ix, q, None, None, None, None, None)
+    with pytest.raises(pkv.PkvError):
+        pkv.retrieve_topk(ix, q, 100, n_cand=10)          # C < min(k, n)
+    with pytest.raises(pkv.PkvError):
+        pkv.retrieve_topk(ix, q, 100, probes_T=0)
+    empty = pkv.Index(cfg, 1, 16)
+    with pytest.raises(pkv.PkvError):
+        pkv.retrieve_topk(empty, q, 10)
+
+
+def test_uva_pinned_host_kv(pkv):
+    """a7 with K/V in pinned host memory read through UVA equals the HBM result."""
+    K, q, V = make_problem(13, 1, 8, 2, 4096)
+    cfg = pkv.config_init(8, 2, SB)
+    ix = pkv.Index(cfg, 1, 4096)
+    pkv.encode_keys(ix, K)
+    idx, _, _ = pkv.retrieve_topk(ix, q, 100)
+    Kh = K.cpu().pin_memory()
+    Vh = V.cpu().pin_memory()
+    o1, l1 = pkv.sparse_attend(ix, q, K, V, idx)
+    o2, l2 = pkv.sparse_attend(ix, q, None, None, idx, K_ptr=Kh.data_ptr(), V_ptr=Vh.data_ptr(),
+                               strides=(Kh.stride(0), Kh.stride(1), Kh.stride(2)))
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2) and torch.equal(l1, l2)
+
+
+@pytest.mark.parametrize("P", [2, 3, 4])
+def test_sequence_sharded_local_equals_unsharded(pkv, P):
+    """§Multi-GPU decomposition on one device: P shards with the exchange buffers filled by device
+    copies produce the unsharded result exactly (same kernels as the NCCL path)."""
+    n = 6000
+    K, q, V = make_problem(14, 1, 8, 2, n)
+    cfg = pkv.config_init(8, 2, SB)
+    full = pkv.Index(cfg, 1, n)
+    pkv.encode_keys(full, K)
+    i0, e0, _ = pkv.retrieve_topk(full, q, 100)
+    Kh = synth.isotropic(93, (1, 2, 50, 128), device="cuda")
+    Vh = synth.isotropic(94, (1, 2, 50, 128), device="cuda")
+    o0, l0 = pkv.sparse_attend(full, q, K, V, i0, Kh, Vh)
+    bounds = sharded.shard_ranges(n, P)
+    shards, Ks, Vs = [], [], []
+    for a, b in bounds:
+        s = pkv.Index(cfg, 1, b - a)
+        Ks.append(K[:, :, a:b].contiguous())
+        Vs.append(V[:, :, a:b].contiguous())
+        pkv.encode_keys(s, Ks[-1])
+        shards.append(s)
+    offs = [a for a, _ in bounds]
+    i1, e1 = pkv.retrieve_topk_sharded_local(shards, offs, q, 100, n)
+    assert torch.equal(i0, i1) and torch.equal(e0, e1)
+    o1, l1 = pkv.sparse_attend_sharded_local(shards, offs, q, Ks, Vs, i1, Kh, Vh)
+    assert torch.allclose(o0.float(), o1.float(), atol=2e-3, rtol=1e-2)
+    assert torch.allclose(l0, l1, atol=1e-4, rtol=1e-5)
+
+
+@pytest.mark.slow
+def test_full_size_128k_sampled_head(pkv):
+    """BASELINE config 2 shape (32 q / 8 KV heads, n = 130,800) in the launch configuration bench.py times:
+    one KV head (4 query heads) checked in full against the oracle, plus sampled keys of every head."""
+    n = 130800
+    K, q, V = make_problem(15, 1, 32, 8, n, device="cuda")
+    cfg = pkv.config_init(32, 8, SB)
+    ix = pkv.Index(cfg, 1, n)
+    pkv.encode_keys(ix, K)
+    idx, est, dbg = pkv.retrieve_topk(ix, q, 100, debug=True)
+    out, lse = pkv.sparse_attend(ix, q, K, V, idx)
+    ids_g, codes_g, w_g = [t.cpu().numpy() for t in ix.export()]
+    rng = np.random.default_rng(0)
+    for g in range(8):
+        pos = rng.choice(n, 512, replace=False)
+        meta = oracle_meta(bf16_f64(K[0, g, torch.as_tensor(pos, device="cuda")]))
+        check_encode(ids_g[0, g, pos], codes_g[0, g, pos], w_g[0, g, pos], meta)
+    g = 5
+    Kf = bf16_f64(K[0, g])
+    meta = oracle_meta(Kf)
+    for hh in range(4):
+        h = 4 * g + hh
+        qf = bf16_f64(q[0, h])
+        r = oracle_retrieval(meta, qf, dbg["T"], dbg["C"], 100)
+        assert np.array_equal(dbg["scores"][0, h].cpu().numpy().astype(np.int64), r["score"])
+        cg = dbg["cand"][0, h].cpu().numpy()
+        assert np.array_equal(np.sort(cg), r["cand"])
+        check_topk(idx[0, h].cpu().numpy(), est[0, h].cpu().numpy(), r["cand"], r["est"],
+                   dict(zip(range(n), meta["knorm"].tolist())), r["qnorm"], 100)
+        o, l = pipeline.attend(qf, Kf, bf16_f64(V[0, g]), idx[0, h].cpu().numpy())
+        og = out[0, h].float().cpu().numpy()
+        assert np.all(np.abs(og - o) <= ATT_ABS + 2.0 ** -8 * np.abs(o))
