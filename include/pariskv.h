@@ -198,7 +198,7 @@ pkv_status pkv_launch_count(uint64_t* total);
 /* Optional per-kernel timing for benchmarks: when enabled, every kernel launch is bracketed by two CUDA
  * events on its stream (eager launches only; do not enable while capturing a graph). pkv_profile_read
  * synchronises and returns the launch count and summed device time of one kernel kind; kinds are numbered
- * 0..12 = encode, qprep, scan, threshold, compact, rerank, topk, topk_merge, attend, combine, head_hist,
+ * 0..12 = encode, qprep, scan, select, (unused), rerank, topk, topk_merge, attend, combine, head_hist,
  * export, debug (pkv_kernel_name). Enabling or disabling resets the counters. */
 pkv_status pkv_profile_enable(int32_t on);
 pkv_status pkv_profile_read(int32_t kind, int64_t* launches, double* total_ms);

@@ -107,7 +107,7 @@ pkv_status alloc_workspace(Workspace* ws, int batch, int n_q, int n_kv, int64_t 
       (size_t)MAX_RANKS * bq * MAX_TOPK * 4,             // topk_est
       (size_t)MAX_RANKS * bq * MAX_TOPK * 4,             // topk_idx
       (size_t)MAX_RANKS * bq * MAX_SPLITS * PART * 4,    // part
-      0};
+      bk * 4};                                           // ticket
   size_t total = 0;
   for (size_t s : sizes) total += align_up(s);
   void* base = nullptr;
@@ -132,6 +132,7 @@ pkv_status alloc_workspace(Workspace* ws, int batch, int n_q, int n_kv, int64_t 
   ws->topk_est = reinterpret_cast<float*>(take(10));
   ws->topk_idx = reinterpret_cast<int32_t*>(take(11));
   ws->part = reinterpret_cast<float*>(take(12));
+  ws->ticket = reinterpret_cast<unsigned int*>(take(13));
   ws->base = base;
   ws->bytes = total;
   e = cudaMemset(base, 0, total);
@@ -177,9 +178,8 @@ pkv_status phase_scan(pkv_index* ix, const void* q, const pkv_retrieve_params* p
 pkv_status phase_select_rerank(pkv_index* ix, const pkv_retrieve_params* p, const ScanPlan& plan,
                                const uint32_t* all_hist, int P, int rank, cudaStream_t s) {
   const int64_t n = ix->n;
-  PKV_CUDA(launch_threshold(ix, plan, all_hist, P, rank, p->n_cand, s), "threshold");
+  PKV_CUDA(launch_select(ix, n > 0 ? n : 0, plan, all_hist, P, rank, p->n_cand, ix->shard_offset, s), "select");
   if (n > 0) {
-    PKV_CUDA(launch_compact(ix, n, plan, ix->shard_offset, ix->cap, s), "compact");
     const int64_t cmax = std::min<int64_t>(p->n_cand, n);
     if (cmax > 0) PKV_CUDA(launch_rerank(ix, cmax, ix->shard_offset, s), "rerank");
   }
@@ -395,12 +395,15 @@ pkv_status sparse_attend(pkv_index* ix, const void* q, const void* K, const void
   Workspace* ws = ix->ws;
   const size_t part_slot = (size_t)ix->batch * ix->cfg.n_q_heads * MAX_SPLITS * PART;
   const int slot = ix->comm ? ix->rank : 0;
-  PKV_CUDA(launch_attend_partial(ix, a, splits, ws->part + slot * part_slot, stream), "attend");
-  if (ix->comm) {
-    pkv_status s2 = comm_allgather_u32(ix, reinterpret_cast<uint32_t*>(ws->part), part_slot, stream);
-    if (s2 != PKV_OK) return s2;
+  if (!ix->comm) {
+    PKV_CUDA(launch_attend_partial(ix, a, splits, ws->part, ws->ticket, out, lse, stream), "attend");
+    return PKV_OK;
   }
-  PKV_CUDA(launch_attend_combine(ix, ws->part, splits, ix->comm ? ix->world : 1, out, lse, stream), "combine");
+  PKV_CUDA(launch_attend_partial(ix, a, splits, ws->part + slot * part_slot, nullptr, nullptr, nullptr, stream),
+           "attend");
+  pkv_status s2 = comm_allgather_u32(ix, reinterpret_cast<uint32_t*>(ws->part), part_slot, stream);
+  if (s2 != PKV_OK) return s2;
+  PKV_CUDA(launch_attend_combine(ix, ws->part, splits, ix->world, out, lse, stream), "combine");
   return PKV_OK;
 }
 
@@ -473,7 +476,8 @@ pkv_status pkv_sparse_attend_sharded_local(pkv_index* const* shards, const int64
     }
     AttendArgs a{q, Ks[r], Vs[r], sb, sh, st, idx, k, K_hot, V_hot, r == P - 1 ? n_hot : 0, scale, offsets[r],
                  offsets[r] + shards[r]->n, offsets[r]};
-    PKV_CUDA(launch_attend_partial(shards[r], a, splits, w0->part + r * part_slot, stream), "attend");
+    PKV_CUDA(launch_attend_partial(shards[r], a, splits, w0->part + r * part_slot, nullptr, nullptr, nullptr, stream),
+             "attend");
   }
   PKV_CUDA(launch_attend_combine(shards[0], w0->part, splits, P, out, lse, stream), "combine");
   return PKV_OK;

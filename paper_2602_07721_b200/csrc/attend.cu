@@ -15,7 +15,7 @@ namespace pkv {
 namespace {
 
 constexpr int AT_WARPS = 4;
-constexpr int AT_BATCH = 4;
+constexpr int AT_BATCH = 8;
 constexpr float LOG2E = 1.4426950408889634f;
 
 __device__ __forceinline__ float4 bf16x4(uint2 w) {
@@ -31,23 +31,19 @@ __device__ __forceinline__ float warp_sum(float v) {
 struct SoftState {
   float m, l, o[4];
 };
-
-__device__ __forceinline__ void soft_update(SoftState& s, float x, const float4& v) {
-  const float mn = fmaxf(s.m, x);
-  const float c = exp2f(s.m - mn);
-  const float p = exp2f(x - mn);
-  s.l = s.l * c + p;
-  s.o[0] = s.o[0] * c + p * v.x;
-  s.o[1] = s.o[1] * c + p * v.y;
-  s.o[2] = s.o[2] * c + p * v.z;
-  s.o[3] = s.o[3] * c + p * v.w;
-  s.m = mn;
-}
+static_assert(AT_BATCH * GMAX == 32, "transpose-reduction maps one (row, head) pair per lane");
 
 __global__ void __launch_bounds__(AT_WARPS * 32) attend_partial_kernel(AttendArgs a, int n_q, int n_kv, int G,
-                                                                       int items_per_split, float* __restrict__ part) {
+                                                                       int items_per_split, float* __restrict__ part,
+                                                                       unsigned int* __restrict__ ticket, void* out,
+                                                                       float* lse) {
+  __shared__ __align__(16) float sm_x[AT_WARPS][AT_BATCH * GMAX];
   __shared__ float sm_m[AT_WARPS][GMAX], sm_l[AT_WARPS][GMAX];
   __shared__ float sm_o[AT_WARPS][GMAX][D];
+  __shared__ float sm_w[GMAX][MAX_SPLITS];
+  __shared__ float sm_M[GMAX], sm_L[GMAX];
+  __shared__ int sm_last;
+  pdl_trigger();
   const int split = blockIdx.x, g = blockIdx.y, b = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const float qscale = a.scale * LOG2E;
@@ -76,49 +72,113 @@ __global__ void __launch_bounds__(AT_WARPS * 32) attend_partial_kernel(AttendArg
   const uint16_t* Vb = static_cast<const uint16_t*>(a.V);
   const uint16_t* Kh = static_cast<const uint16_t*>(a.K_hot) + ((int64_t)b * n_kv + g) * a.n_hot * D;
   const uint16_t* Vh = static_cast<const uint16_t*>(a.V_hot) + ((int64_t)b * n_kv + g) * a.n_hot * D;
+  bool waited = false;
   for (int base = i0 + warp * AT_BATCH; base < i1; base += AT_WARPS * AT_BATCH) {
     uint2 kr[AT_BATCH], vr[AT_BATCH];
     int head[AT_BATCH];  // -1: hot row (all heads), -2: skip, else query head within the group
+    // hot rows do not depend on the retrieval: issue them before waiting on the previous kernel
 #pragma unroll
     for (int u = 0; u < AT_BATCH; ++u) {
       const int it = base + u;
       head[u] = -2;
       kr[u] = make_uint2(0, 0);
       vr[u] = make_uint2(0, 0);
-      if (it < i1) {
-        if (it < a.n_hot) {
-          head[u] = -1;
-          kr[u] = ldg_v2(Kh + (int64_t)it * D + 4 * lane);
-          vr[u] = ldg_v2(Vh + (int64_t)it * D + 4 * lane);
-        } else {
-          const int r = it - a.n_hot;
-          const int hh = r / a.k, j = r % a.k;
-          const int id = a.idx[((int64_t)b * n_q + g * G + hh) * a.k + j];
-          if (id >= 0 && id >= a.own_lo && id < a.own_hi) {
-            head[u] = hh;
-            const int64_t row = (int64_t)id - a.id_offset;
-            const int64_t off = (int64_t)b * a.sb + (int64_t)g * a.sh + row * a.st + 4 * lane;
-            kr[u] = ldg_v2(Kb + off);
-            vr[u] = ldg_v2(Vb + off);
-          }
-        }
+      if (it < i1 && it < a.n_hot) {
+        head[u] = -1;
+        kr[u] = ldg_v2(Kh + (int64_t)it * D + 4 * lane);
+        vr[u] = ldg_v2(Vh + (int64_t)it * D + 4 * lane);
+      }
+    }
+    if (!waited) {
+      pdl_wait();  // top-k ids come from the retrieval kernels
+      waited = true;
+    }
+    int id[AT_BATCH];
+#pragma unroll
+    for (int u = 0; u < AT_BATCH; ++u) {
+      const int it = base + u;
+      id[u] = -1;
+      if (it < i1 && it >= a.n_hot) {
+        const int r = it - a.n_hot;
+        id[u] = a.idx[((int64_t)b * n_q + g * G + r / a.k) * a.k + r % a.k];
       }
     }
 #pragma unroll
     for (int u = 0; u < AT_BATCH; ++u) {
-      if (head[u] == -2) continue;
-      const float4 kf = bf16x4(kr[u]);
-      const float4 vf = bf16x4(vr[u]);
-#pragma unroll
-      for (int hh = 0; hh < GMAX; ++hh) {
-        if (hh >= G) break;
-        if (head[u] != -1 && head[u] != hh) continue;
-        float d = kf.x * qv[hh].x + kf.y * qv[hh].y + kf.z * qv[hh].z + kf.w * qv[hh].w;
-        d = warp_sum(d);
-        soft_update(st[hh], d, vf);
+      const int it = base + u;
+      if (it < i1 && it >= a.n_hot && id[u] >= 0 && id[u] >= a.own_lo && id[u] < a.own_hi) {
+        head[u] = (it - a.n_hot) / a.k;
+        const int64_t off = (int64_t)b * a.sb + (int64_t)g * a.sh + ((int64_t)id[u] - a.id_offset) * a.st + 4 * lane;
+        kr[u] = ldg_v2(Kb + off);
+        vr[u] = ldg_v2(Vb + off);
       }
     }
+    // all (row, head) partial dots of the batch, then one transpose-reduction: 31 shuffles leave the full dot
+    // of pair L = (row L/4, head L%4) in lane L (instead of a serial 5-shuffle chain per row and head)
+    float v[AT_BATCH * GMAX];
+#pragma unroll
+    for (int u = 0; u < AT_BATCH; ++u) {
+      const float4 kf = bf16x4(kr[u]);
+#pragma unroll
+      for (int hh = 0; hh < GMAX; ++hh)
+        v[u * GMAX + hh] = kf.x * qv[hh].x + kf.y * qv[hh].y + kf.z * qv[hh].z + kf.w * qv[hh].w;
+    }
+#pragma unroll
+    for (int m = 16, V = 32; m >= 1; m >>= 1, V >>= 1) {
+      const bool upper = (lane & m) != 0;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        if (i < V / 2) {
+          const float send = upper ? v[i] : v[i + V / 2];
+          const float keep = upper ? v[i + V / 2] : v[i];
+          v[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+        }
+      }
+    }
+    sm_x[warp][lane] = v[0];
+    __syncwarp();
+    float x[AT_BATCH * GMAX];
+#pragma unroll
+    for (int i = 0; i < AT_BATCH * GMAX / 4; ++i) {
+      const float4 t4 = reinterpret_cast<const float4*>(sm_x[warp])[i];
+      x[4 * i] = t4.x;
+      x[4 * i + 1] = t4.y;
+      x[4 * i + 2] = t4.z;
+      x[4 * i + 3] = t4.w;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int hh = 0; hh < GMAX; ++hh) {
+      if (hh >= G) break;
+      float mx = st[hh].m;
+#pragma unroll
+      for (int u = 0; u < AT_BATCH; ++u)
+        if (head[u] == -1 || head[u] == hh) mx = fmaxf(mx, x[u * GMAX + hh]);
+      if (mx == -INFINITY) continue;  // no row of this head in the batch
+      const float c = exp2f(st[hh].m - mx);
+      float l = st[hh].l * c;
+      float o0 = st[hh].o[0] * c, o1 = st[hh].o[1] * c, o2 = st[hh].o[2] * c, o3 = st[hh].o[3] * c;
+#pragma unroll
+      for (int u = 0; u < AT_BATCH; ++u) {
+        if (head[u] == -1 || head[u] == hh) {
+          const float pu = exp2f(x[u * GMAX + hh] - mx);
+          const float4 vf = bf16x4(vr[u]);
+          l += pu;
+          o0 = fmaf(pu, vf.x, o0);
+          o1 = fmaf(pu, vf.y, o1);
+          o2 = fmaf(pu, vf.z, o2);
+          o3 = fmaf(pu, vf.w, o3);
+        }
+      }
+      st[hh].m = mx;
+      st[hh].l = l;
+      st[hh].o[0] = o0;
+      st[hh].o[1] = o1;
+      st[hh].o[2] = o2;
+      st[hh].o[3] = o3;
+    }
   }
+  if (!waited) pdl_wait();
   // merge the 4 warps' states
 #pragma unroll
   for (int hh = 0; hh < GMAX; ++hh) {
@@ -149,6 +209,51 @@ __global__ void __launch_bounds__(AT_WARPS * 32) attend_partial_kernel(AttendArg
     }
     p[2 + d] = O;
   }
+  if (ticket == nullptr) return;  // sharded: the LSE merge runs after the all-gather
+  // fused LSE merge: the last CTA of this (sequence, KV head) to finish combines all splits
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int t = atomicAdd(&ticket[b * n_kv + g], 1u);
+    sm_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!sm_last) return;
+  __threadfence();
+  const int nsplits = gridDim.x;
+  if (warp < G) {
+    const int hh = warp;
+    const float* base = part + ((int64_t)b * n_q + g * G + hh) * MAX_SPLITS * PART;
+    float M = -INFINITY;
+    for (int s = lane; s < nsplits; s += 32) M = fmaxf(M, __ldcg(base + (int64_t)s * PART));
+#pragma unroll
+    for (int x = 16; x > 0; x >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, x));
+    float L = 0.f;
+    for (int s = lane; s < nsplits; s += 32) {
+      const float m = __ldcg(base + (int64_t)s * PART);
+      const float c = (m == -INFINITY) ? 0.f : exp2f(m - M);  // partial o is unnormalised: rescale only
+      sm_w[hh][s] = c;
+      L += c * __ldcg(base + (int64_t)s * PART + 1);
+    }
+#pragma unroll
+    for (int x = 16; x > 0; x >>= 1) L += __shfl_xor_sync(0xffffffffu, L, x);
+    if (lane == 0) {
+      sm_M[hh] = M;
+      sm_L[hh] = L;
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < G * D; e += AT_WARPS * 32) {
+    const int hh = e / D, d = e % D;
+    const float* base = part + ((int64_t)b * n_q + g * G + hh) * MAX_SPLITS * PART;
+    float O = 0.f;
+    for (int s = 0; s < nsplits; ++s) O += sm_w[hh][s] * __ldcg(base + (int64_t)s * PART + 2 + d);
+    const float L = sm_L[hh];
+    const int64_t bhq = (int64_t)b * n_q + g * G + hh;
+    static_cast<__nv_bfloat16*>(out)[bhq * D + d] = __float2bfloat16_rn(L > 0.f ? O / L : 0.f);
+    if (lse && d == 0) lse[bhq] = L > 0.f ? (sm_M[hh] + log2f(L)) * 0.6931471805599453f : -INFINITY;
+  }
+  if (threadIdx.x == 0) ticket[b * n_kv + g] = 0u;  // re-arm for the next launch / graph replay
 }
 
 __global__ void __launch_bounds__(D) attend_combine_kernel(const float* __restrict__ parts, int nsplits, int P,
@@ -179,25 +284,23 @@ __global__ void __launch_bounds__(D) attend_combine_kernel(const float* __restri
 }  // namespace
 
 int plan_attend_splits(const pkv_index* ix, int total_items) {
-  const int units = ix->batch * ix->cfg.n_kv_heads;
-  int splits = (2 * ix->num_sms + units - 1) / units;
-  const int max_by_items = (total_items + 15) / 16;
-  if (splits > max_by_items) splits = max_by_items;
+  // one round of AT_BATCH rows per warp: every row load of a CTA is in flight at once
+  (void)ix;
+  int splits = (total_items + AT_WARPS * AT_BATCH - 1) / (AT_WARPS * AT_BATCH);
   if (splits > MAX_SPLITS) splits = MAX_SPLITS;
   if (splits < 1) splits = 1;
   return splits;
 }
 
 cudaError_t launch_attend_partial(const pkv_index* ix, const AttendArgs& a, int splits, float* part_out,
-                                  cudaStream_t stream) {
+                                  unsigned int* ticket, void* out, float* lse, cudaStream_t stream) {
   const int G = ix->dcfg.G;
   const int n_items = a.n_hot + G * a.k;
   const int per = (n_items + splits - 1) / splits;
   dim3 grid(splits, ix->cfg.n_kv_heads, ix->batch);
   ProfScope p_(K_ATTEND, stream);
-  attend_partial_kernel<<<grid, AT_WARPS * 32, 0, stream>>>(a, ix->cfg.n_q_heads, ix->cfg.n_kv_heads, G,
-                                                            per > 0 ? per : 1, part_out);
-  return cudaGetLastError();
+  return pdl_launch(attend_partial_kernel, grid, dim3(AT_WARPS * 32), 0, stream, a, ix->cfg.n_q_heads,
+                    ix->cfg.n_kv_heads, G, per > 0 ? per : 1, part_out, ticket, out, lse);
 }
 
 cudaError_t launch_attend_combine(const pkv_index* ix, const float* parts, int nsplits, int P, void* out, float* lse,

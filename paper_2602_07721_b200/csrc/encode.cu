@@ -90,9 +90,9 @@ __global__ void __launch_bounds__(256) encode_kernel(const uint16_t* __restrict_
       v[i] = sgn[i] ? -nabs : nabs;
     }
     fwht128<int>(v, lane16);
-    const double scale = ldexp(1.0, emax - 150);
+    const double pscale = __longlong_as_double((long long)(1023 + emax - 150) << 52);  // 2^(emax-150), emax >= 1
 #pragma unroll
-    for (int i = 0; i < 8; ++i) y[i] = (double)v[i] * scale;  // exact: |v| < 2^31, power-of-two scale
+    for (int i = 0; i < 8; ++i) y[i] = emax ? (double)v[i] * pscale : 0.0;  // exact: |v| < 2^31
   } else {
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -117,14 +117,9 @@ __global__ void __launch_bounds__(256) encode_kernel(const uint16_t* __restrict_
   uint32_t id = 0, code = 0;
   float dot = 0.f, vn2 = 0.f;
   const bool degenerate = (S == 0.0);
-  // y scaled to a float-safe range for the weight arithmetic (ratios only)
-  int ex = 0;
-  double ymax = 0.0;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) ymax = fmax(ymax, fabs(y[i]));
-#pragma unroll
-  for (int x = 1; x < 16; x <<= 1) ymax = fmax(ymax, shfl_x(ymax, x));
-  frexp(ymax, &ex);
+  // weights in fp32 on y scaled by 2^(119 - emax): |y| < 128 * 2^(emax - 126) so |y * scale| < 1 (ratios only)
+  const double scale = __longlong_as_double((long long)(1023 + 119 - emax) << 52);
+  const double unscale = __longlong_as_double((long long)(1023 - 119 + emax) << 52);
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const bool pos = y[i] >= 0.0;
@@ -142,17 +137,17 @@ __global__ void __launch_bounds__(256) encode_kernel(const uint16_t* __restrict_
     id |= (pos ? 1u : 0u) << i;
     code |= ((sbit << 3) | idx) << (4 * i);
     const float L = cfg.levels[idx];
-    const float yf = (float)ldexp(y[i], -ex);
+    const float yf = (float)(y[i] * scale);
     dot = fmaf(sbit ? L : -L, yf, dot);
     vn2 = fmaf(L, L, vn2);
   }
-  const float Sf = (float)ldexp(S, -2 * ex);
+  const float Sf = (float)(S * scale * scale);
   float wprime = 0.f;
   if (!degenerate) {
     // alpha = dot / (||v~|| sqrt(S)); clamp at 1e-3 (AMB-6)
     const bool clamped = (dot <= 0.f) || (dot * dot < 1e-6f * vn2 * Sf);
     const float w_rel = clamped ? sqrtf(Sf * (1.0f / 128.0f)) / (1e-3f * sqrtf(vn2)) : Sf / (11.313708498984761f * dot);
-    wprime = (float)ldexp((double)w_rel, ex);
+    wprime = (float)((double)w_rel * unscale);
   }
 
   // ---- stores ----

@@ -51,6 +51,7 @@ struct Workspace {
   float* topk_est = nullptr;      // [MAX_RANKS][batch][n_q][MAX_TOPK] (sharded exchange T)
   int32_t* topk_idx = nullptr;    // [MAX_RANKS][batch][n_q][MAX_TOPK]
   float* part = nullptr;          // [MAX_RANKS][batch][n_q][MAX_SPLITS][PART] (exchange A)
+  unsigned int* ticket = nullptr; // [batch][n_kv] split-completion counters of the fused attention merge
   void* base = nullptr;
   size_t bytes = 0;
   int refs = 1;
@@ -82,7 +83,7 @@ struct pkv_index {
 namespace pkv {
 
 // Kernel kinds for launch accounting / optional event timing (profile.cpp)
-enum KernelKind { K_ENCODE, K_QPREP, K_SCAN, K_THRESHOLD, K_COMPACT, K_RERANK, K_TOPK, K_MERGE, K_ATTEND,
+enum KernelKind { K_ENCODE, K_QPREP, K_SCAN, K_SELECT, K_UNUSED4, K_RERANK, K_TOPK, K_MERGE, K_ATTEND,
                   K_COMBINE, K_HEADHIST, K_EXPORT, K_DEBUG, K_NUM_KINDS };
 class ProfScope {  // bracket one kernel launch: counts it, and records events when profiling is on
  public:
@@ -121,11 +122,9 @@ cudaError_t launch_scan(const pkv_index* ix, int64_t n, const ScanPlan& plan, cu
 // Per-head totals of the chunk histograms -> head_hist[slot].
 cudaError_t launch_head_hist(const pkv_index* ix, const ScanPlan& plan, uint32_t* head_hist_out,
                              cudaStream_t stream);
-// Threshold + per-chunk offsets. all_hist: [P][batch][n_q][HB] gathered per-rank totals (P >= 1).
-cudaError_t launch_threshold(const pkv_index* ix, const ScanPlan& plan, const uint32_t* all_hist, int P,
-                             int rank, int64_t C, cudaStream_t stream);
-cudaError_t launch_compact(const pkv_index* ix, int64_t n, const ScanPlan& plan, int64_t id_offset,
-                           int64_t cand_stride, cudaStream_t stream);
+// Fused threshold + compaction. all_hist: [P][batch][n_q][HB] gathered cumulative per-rank totals (P > 1).
+cudaError_t launch_select(const pkv_index* ix, int64_t n, const ScanPlan& plan, const uint32_t* all_hist, int P,
+                          int rank, int64_t C, int64_t id_offset, cudaStream_t stream);
 cudaError_t launch_dbg_scores(const pkv_index* ix, int64_t n, uint8_t* out, cudaStream_t stream);
 cudaError_t launch_rerank(const pkv_index* ix, int64_t C_cap, int64_t id_offset, cudaStream_t stream);
 cudaError_t launch_topk(const pkv_index* ix, int64_t C_cap, int k, int32_t* out_idx, float* out_est,
@@ -150,8 +149,9 @@ struct AttendArgs {
   int64_t id_offset;       // local row = id - id_offset
 };
 int plan_attend_splits(const pkv_index* ix, int total_rows);
+// ticket != nullptr: the last CTA of each (sequence, KV head) also does the LSE merge into out/lse.
 cudaError_t launch_attend_partial(const pkv_index* ix, const AttendArgs& a, int splits, float* part_out,
-                                  cudaStream_t stream);
+                                  unsigned int* ticket, void* out, float* lse, cudaStream_t stream);
 cudaError_t launch_attend_combine(const pkv_index* ix, const float* parts, int nsplits, int P, void* out,
                                   float* lse, cudaStream_t stream);
 

@@ -2,6 +2,7 @@
 // When enabled, every kernel launch is bracketed by two events recorded on the launch stream.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -46,7 +47,7 @@ void drain() {  // caller holds g_mu
   g_recs.clear();
 }
 
-const char* kNames[K_NUM_KINDS] = {"encode", "qprep", "scan", "threshold", "compact", "rerank", "topk",
+const char* kNames[K_NUM_KINDS] = {"encode", "qprep", "scan", "select", "unused", "rerank", "topk",
                                    "topk_merge", "attend", "combine", "head_hist", "export", "debug"};
 
 }  // namespace
@@ -96,3 +97,13 @@ extern "C" pkv_status pkv_profile_read(int32_t kind, int64_t* launches, double* 
 extern "C" const char* pkv_kernel_name(int32_t kind) {
   return (kind >= 0 && kind < pkv::K_NUM_KINDS) ? pkv::kNames[kind] : "";
 }
+
+namespace pkv {
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PKV_NO_PDL");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+}  // namespace pkv

@@ -17,56 +17,91 @@ namespace {
 constexpr int SEL_STRIDE = 4 + 4 * MAX_CHUNKS;
 constexpr int RR_THREADS = 256;
 
+// Two threads per candidate: the even thread decodes subspaces 0-7 (coordinates 0..63), the odd thread
+// subspaces 8-15. Table row of coordinate c lives at physical row 2*(c mod 64) + c/64, so at every step the
+// even lanes read an even row and the odd lanes the adjacent odd row: with 16-word rows the two halves use
+// disjoint 16-bank halves (no conflicts), and the half offset (64 B) folds into the LOP3 that extracts the
+// nibble address, so a lookup is SHF + LOP3 + LDS [reg + imm] + FADD.
+constexpr int RT_ROWS = D;
+
 __global__ void __launch_bounds__(RR_THREADS) rerank_kernel(const uint8_t* __restrict__ rec, const int32_t* __restrict__ cand,
                                                              const int32_t* __restrict__ sel,
                                                              const float* __restrict__ rtab,
                                                              const float* __restrict__ qnorm, int64_t cap, int n_q,
                                                              int n_kv, int G, int64_t cand_stride, int64_t id_offset,
                                                              float* __restrict__ est_out) {
-  __shared__ float T[D * 16];
+  __shared__ __align__(16) float T[RT_ROWS * 16];
+  pdl_trigger();
+  pdl_wait();
   const int h = blockIdx.y, b = blockIdx.z;
   const int g = h / G;
   const int64_t bhq = (int64_t)b * n_q + h;
-  const int C_local = sel[bhq * SEL_STRIDE + 2];
-  if ((int64_t)blockIdx.x * RR_THREADS >= C_local) return;
-  const float* tsrc = rtab + bhq * D * 16;
-  for (int i = threadIdx.x; i < D * 16; i += RR_THREADS) T[i] = tsrc[i];
-  __syncthreads();
-  const float qn = qnorm[bhq];
-  const uint8_t* rec_bh = rec + ((int64_t)b * n_kv + g) * cap * REC;
+  constexpr int PER_CTA = RR_THREADS / 2;
   const int32_t* cd = cand + bhq * cand_stride;
+  int pos = blockIdx.x * PER_CTA + (threadIdx.x >> 1);
+  // one round of independent loads: candidate count, this thread's candidate id (speculative: pos < capacity),
+  // its share of the query table, ||q||
+  const int C_local = sel[bhq * SEL_STRIDE + 2];
+  const int32_t cid0 = pos < cand_stride ? cd[pos] : 0;
+  const float4* tsrc = reinterpret_cast<const float4*>(rtab + bhq * D * 16);
+  float4 tv[D * 4 / RR_THREADS];
+#pragma unroll
+  for (int u = 0; u < D * 4 / RR_THREADS; ++u) tv[u] = tsrc[threadIdx.x + u * RR_THREADS];
+  const float qn = qnorm[bhq];
+  if ((int64_t)blockIdx.x * PER_CTA >= C_local) return;
+#pragma unroll
+  for (int u = 0; u < D * 4 / RR_THREADS; ++u) {  // 4 float4 per row; coordinate c -> physical row 2(c%64)+c/64
+    const int i = threadIdx.x + u * RR_THREADS;
+    const int c = i >> 2;
+    reinterpret_cast<float4*>(T)[(2 * (c & 63) + (c >> 6)) * 4 + (i & 3)] = tv[u];
+  }
+  const uint8_t* rec_bh = rec + ((int64_t)b * n_kv + g) * cap * REC;
   float* eo = est_out + bhq * cand_stride;
-  for (int pos = blockIdx.x * RR_THREADS + threadIdx.x; pos < C_local; pos += gridDim.x * RR_THREADS) {
-    const int64_t t = (int64_t)cd[pos] - id_offset;
-    const uint8_t* r = rec_bh + t * REC;
-    uint4 c4[4], w4[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) c4[i] = ldg_nc_v4(r + 16 * i);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) w4[i] = ldg_nc_v4(r + 64 + 16 * i);
-    const uint32_t cw[16] = {c4[0].x, c4[0].y, c4[0].z, c4[0].w, c4[1].x, c4[1].y, c4[1].z, c4[1].w,
-                             c4[2].x, c4[2].y, c4[2].z, c4[2].w, c4[3].x, c4[3].y, c4[3].z, c4[3].w};
-    const uint32_t ww[16] = {w4[0].x, w4[0].y, w4[0].z, w4[0].w, w4[1].x, w4[1].y, w4[1].z, w4[1].w,
-                             w4[2].x, w4[2].y, w4[2].z, w4[2].w, w4[3].x, w4[3].y, w4[3].z, w4[3].w};
+  const int half = threadIdx.x & 1;
+  const char* Tb = reinterpret_cast<const char*>(T);
+  const uint32_t hoff = half ? 64u : 0u;
+  const unsigned pair_mask = 3u << ((threadIdx.x & 31) & ~1);
+  // the first candidate's record loads are issued before the table is published (__syncthreads)
+  uint4 c0, c1, w0, w1;
+  if (pos < C_local) {
+    const uint8_t* r = rec_bh + ((int64_t)cid0 - id_offset) * REC + 32 * half;
+    c0 = ldg_nc_v4(r);
+    c1 = ldg_nc_v4(r + 16);
+    w0 = ldg_nc_v4(r + 64);
+    w1 = ldg_nc_v4(r + 80);
+  }
+  __syncthreads();
+  for (; pos < C_local; pos += gridDim.x * PER_CTA) {
+    const uint32_t cw[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+    const uint32_t ww[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+    const int nxt = pos + gridDim.x * PER_CTA;
+    if (nxt < C_local) {  // prefetch the next candidate of this thread (rare: grids cover C in one pass)
+      const uint8_t* r = rec_bh + ((int64_t)cd[nxt] - id_offset) * REC + 32 * half;
+      c0 = ldg_nc_v4(r);
+      c1 = ldg_nc_v4(r + 16);
+      w0 = ldg_nc_v4(r + 64);
+      w1 = ldg_nc_v4(r + 80);
+    }
     float est = 0.f;
 #pragma unroll
-    for (int sb = 0; sb < NB; ++sb) {
+    for (int sb = 0; sb < 8; ++sb) {
       float dot = 0.f;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const uint32_t nib = (cw[sb] >> (4 * j)) & 15u;
-        dot += T[(8 * sb + j) * 16 + nib];
+        const uint32_t off = (j == 0 ? (cw[sb] << 2) : (cw[sb] >> (4 * j - 2))) & 0x3cu;
+        dot += *reinterpret_cast<const float*>(Tb + (8 * sb + j) * 128 + (off | hoff));
       }
       est = fmaf(__uint_as_float(ww[sb]), dot, est);
     }
-    eo[pos] = est * qn;
+    est += __shfl_xor_sync(pair_mask, est, 1);
+    if (!half) eo[pos] = est * qn;
   }
 }
 
 // ---------------------------------------------------------------- radix top-k
 constexpr int TK_THREADS = 1024;
 constexpr int TK_CACHE = 12288;  // composite keys cached in (dynamic) smem when the list is short enough
-constexpr int TK_SMEM = TK_CACHE * 8;
+constexpr int TK_SMEM = 16384 * 8;  // >= BS_CACHE * (4 + 4) and TK_CACHE * 8
 
 struct CandSrc {  // unsharded: est/cand arrays of one (b, h); count from sel
   const float* est;
@@ -90,7 +125,7 @@ struct MergeSrc {  // sharded merge: P lists of k entries with stride
 
 template <class Src>
 __device__ void radix_topk(const Src& src, int count, int k, int32_t* out_idx, float* out_est) {
-  extern __shared__ unsigned long long cache[];  // [TK_CACHE]
+  extern __shared__ unsigned long long cache[];  // [TK_CACHE] (aliases the caller's dynamic smem)
   __shared__ unsigned int hist[256];
   __shared__ unsigned long long win[MAX_TOPK];
   __shared__ unsigned long long prefix_s;
@@ -103,7 +138,7 @@ __device__ void radix_topk(const Src& src, int count, int k, int32_t* out_idx, f
     wcount = 0;
   }
   __syncthreads();
-  for (int i = tid; i < count; i += TK_THREADS) {
+  for (int i = tid; i < count; i += blockDim.x) {
     const unsigned long long kk = src.key(i);
     if (cached) cache[i] = kk;
     nv += (kk != 0ull);
@@ -119,11 +154,11 @@ __device__ void radix_topk(const Src& src, int count, int k, int32_t* out_idx, f
   __syncthreads();
   for (int shift = 56; shift >= 0; shift -= 8) {
     if (done_s) break;
-    for (int i = tid; i < 256; i += TK_THREADS) hist[i] = 0u;
+    for (int i = tid; i < 256; i += blockDim.x) hist[i] = 0u;
     __syncthreads();
     const unsigned long long hmask = (shift == 56) ? 0ull : (~0ull << (shift + 8));
     const unsigned long long pre = prefix_s;
-    for (int i = tid; i < count; i += TK_THREADS) {
+    for (int i = tid; i < count; i += blockDim.x) {
       const unsigned long long kk = cached ? cache[i] : src.key(i);
       if (kk != 0ull && (kk & hmask) == pre) atomicAdd(&hist[(kk >> shift) & 255u], 1u);
     }
@@ -163,7 +198,7 @@ __device__ void radix_topk(const Src& src, int count, int k, int32_t* out_idx, f
   }
   const unsigned long long kth = prefix_s;  // k-th largest composite key (or its bucket floor)
   if (kv > 0) {
-    for (int i = tid; i < count; i += TK_THREADS) {
+    for (int i = tid; i < count; i += blockDim.x) {
       const unsigned long long kk = cached ? cache[i] : src.key(i);
       if (kk != 0ull && kk >= kth) {
         const int slot = atomicAdd(&wcount, 1);
@@ -174,12 +209,12 @@ __device__ void radix_topk(const Src& src, int count, int k, int32_t* out_idx, f
   __syncthreads();
   int npow = 1;
   while (npow < kv) npow <<= 1;
-  for (int i = kv + tid; i < npow; i += TK_THREADS) win[i] = 0ull;
+  for (int i = kv + tid; i < npow; i += blockDim.x) win[i] = 0ull;
   __syncthreads();
   // bitonic sort descending
   for (int kk2 = 2; kk2 <= npow; kk2 <<= 1) {
     for (int j = kk2 >> 1; j > 0; j >>= 1) {
-      for (int i = tid; i < npow; i += TK_THREADS) {
+      for (int i = tid; i < npow; i += blockDim.x) {
         const int p = i ^ j;
         if (p > i) {
           const bool desc = (i & kk2) == 0;
@@ -193,7 +228,7 @@ __device__ void radix_topk(const Src& src, int count, int k, int32_t* out_idx, f
       __syncthreads();
     }
   }
-  for (int i = tid; i < k; i += TK_THREADS) {
+  for (int i = tid; i < k; i += blockDim.x) {
     if (i < kv) {
       const unsigned long long kk = win[i];
       out_idx[i] = (int32_t)(uint32_t)(kk & 0xffffffffull);
@@ -205,15 +240,167 @@ __device__ void radix_topk(const Src& src, int count, int k, int32_t* out_idx, f
   }
 }
 
-__global__ void __launch_bounds__(TK_THREADS) topk_kernel(const float* __restrict__ est, const int32_t* __restrict__ cand,
+// Value-range bucket select (no sort over C): min/max of the estimates, a 2048-bin histogram of
+// floor((est - min) * 2048 / (max - min)) (monotone in est, so bins partition the order), the boundary bin
+// holding the k-th largest, and an exact (est, id) selection inside that bin only; the final order comes from
+// rank counting over the k winners (composite keys are unique). Falls back to the radix select when the
+// list does not fit the smem cache or the boundary bin is larger than its buffer.
+constexpr int BS_BINS = 2048;
+constexpr int BS_BND = 1024;
+constexpr int BS_THREADS = 512;
+constexpr int BS_CACHE = 16384;  // estimates cached in dynamic smem (64 KB)
+
+__device__ __forceinline__ unsigned long long ckey(float e, int id) {
+  return ((unsigned long long)ord_f32(e) << 32) | (uint32_t)id;
+}
+
+__global__ void __launch_bounds__(BS_THREADS) topk_kernel(const float* __restrict__ est, const int32_t* __restrict__ cand,
                                                            const int32_t* __restrict__ sel, int n_q,
                                                            int64_t cand_stride, int k, int out_stride,
                                                            int32_t* out_idx, float* out_est) {
+  extern __shared__ float ecache[];  // [BS_CACHE] estimates, then [BS_CACHE] ids
+  int32_t* icache = reinterpret_cast<int32_t*>(ecache + BS_CACHE);
+  __shared__ unsigned int hist[BS_BINS];
+  __shared__ unsigned long long win[MAX_TOPK];
+  __shared__ unsigned long long bnd[BS_BND];
+  __shared__ float red_mn[BS_THREADS / 32], red_mx[BS_THREADS / 32];
+  __shared__ unsigned int wsum[BS_THREADS / 32];
+  __shared__ int s_bstar, s_need, s_wc, s_bc;
+  pdl_trigger();
+  pdl_wait();
   const int h = blockIdx.x, b = blockIdx.y;
   const int64_t bhq = (int64_t)b * n_q + h;
   const int count = sel[bhq * SEL_STRIDE + 2];
-  CandSrc src{est + bhq * cand_stride, cand + bhq * cand_stride};
-  radix_topk(src, count, k, out_idx + bhq * out_stride, out_est + bhq * out_stride);
+  const float* es = est + bhq * cand_stride;
+  const int32_t* ids = cand + bhq * cand_stride;
+  int32_t* oi = out_idx + bhq * out_stride;
+  float* oe = out_est + bhq * out_stride;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = BS_THREADS / 32;
+  const int kv = min(k, count);
+  if (count > BS_CACHE) {  // long lists (1M-token contexts): radix select straight from global memory
+    CandSrc src{es, ids};
+    radix_topk(src, count, k, oi, oe);
+    return;
+  }
+  float mn = INFINITY, mx = -INFINITY;
+  for (int i0 = 0; i0 < count; i0 += 8 * BS_THREADS) {  // 8 estimates + 8 ids in flight per thread
+    float ev[8];
+    int32_t iv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + u * BS_THREADS + tid;
+      ev[u] = i < count ? es[i] : 0.f;
+      iv[u] = i < count ? ids[i] : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + u * BS_THREADS + tid;
+      if (i < count) {
+        ecache[i] = ev[u];
+        icache[i] = iv[u];
+        mn = fminf(mn, ev[u]);
+        mx = fmaxf(mx, ev[u]);
+      }
+    }
+  }
+#pragma unroll
+  for (int x = 16; x > 0; x >>= 1) {
+    mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, x));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, x));
+  }
+  if (lane == 0) {
+    red_mn[warp] = mn;
+    red_mx[warp] = mx;
+  }
+  for (int i = tid; i < BS_BINS; i += BS_THREADS) hist[i] = 0u;
+  if (tid == 0) {
+    s_wc = 0;
+    s_bc = 0;
+    s_bstar = -1;
+    s_need = 0;
+  }
+  __syncthreads();
+  mn = red_mn[lane % NW];
+  mx = red_mx[lane % NW];
+#pragma unroll
+  for (int x = 16; x > 0; x >>= 1) {
+    mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, x));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, x));
+  }
+  const float range = mx - mn;
+  const float scale = (range > 0.f) ? (float)BS_BINS / range : 0.f;
+  auto bin_of = [&](float e) -> int { return min(BS_BINS - 1, (int)((e - mn) * scale)); };
+  if (count > kv) {
+    for (int i = tid; i < count; i += BS_THREADS) atomicAdd(&hist[bin_of(ecache[i])], 1u);
+    __syncthreads();
+    // thread t owns bins [2048 - 4(t+1), 2048 - 4t) (descending order); block suffix scan
+    constexpr int PER = BS_BINS / BS_THREADS;
+    unsigned int c[PER], sum = 0;
+#pragma unroll
+    for (int e = 0; e < PER; ++e) {
+      c[e] = hist[BS_BINS - 1 - PER * tid - e];
+      sum += c[e];
+    }
+    unsigned int inc = sum;
+#pragma unroll
+    for (int x = 1; x < 32; x <<= 1) {
+      const unsigned int o = __shfl_up_sync(0xffffffffu, inc, x);
+      if (lane >= x) inc += o;
+    }
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    unsigned int wbase = 0;
+    for (int w = 0; w < warp; ++w) wbase += wsum[w];
+    const unsigned int before = wbase + inc - sum;
+    if (before < (unsigned)kv && before + sum >= (unsigned)kv) {
+      unsigned int cum = before;
+#pragma unroll
+      for (int e = 0; e < PER; ++e) {
+        if (cum + c[e] >= (unsigned)kv) {
+          s_bstar = BS_BINS - 1 - PER * tid - e;
+          s_need = kv - (int)cum;
+          break;
+        }
+        cum += c[e];
+      }
+    }
+  }
+  __syncthreads();
+  const int bstar = s_bstar;
+  if (bstar >= 0 && (int)hist[bstar] > BS_BND) {  // boundary bin too large (massive ties): exact radix
+    CandSrc src{es, ids};
+    radix_topk(src, count, k, oi, oe);
+    return;
+  }
+  for (int i = tid; i < count; i += BS_THREADS) {
+    const float e = ecache[i];
+    const int bb = (bstar < 0) ? BS_BINS : bin_of(e);
+    if (bb > bstar) win[atomicAdd(&s_wc, 1)] = ckey(e, icache[i]);
+    else if (bb == bstar) bnd[atomicAdd(&s_bc, 1)] = ckey(e, icache[i]);
+  }
+  __syncthreads();
+  const int nb = s_bc, need = s_need, wc = s_wc;
+  // exact selection inside the boundary bin by rank counting (keys are unique)
+  for (int i = tid; i < nb; i += BS_THREADS) {
+    const unsigned long long x = bnd[i];
+    int r = 0;
+    for (int j2 = 0; j2 < nb; ++j2) r += bnd[j2] > x;
+    if (r < need) win[wc + r] = x;
+  }
+  __syncthreads();
+  // final order by rank counting over the kv winners
+  for (int i = tid; i < kv; i += BS_THREADS) {
+    const unsigned long long x = win[i];
+    int r = 0;
+    for (int j2 = 0; j2 < kv; ++j2) r += win[j2] > x;
+    oi[r] = (int32_t)(uint32_t)(x & 0xffffffffull);
+    oe[r] = unord_f32((uint32_t)(x >> 32));
+  }
+  for (int i = kv + tid; i < k; i += BS_THREADS) {
+    oi[i] = -1;
+    oe[i] = -INFINITY;
+  }
 }
 
 __global__ void __launch_bounds__(TK_THREADS) merge_kernel(const float* __restrict__ all_est,
@@ -247,14 +434,14 @@ cudaError_t init_rerank_attrs() {
 
 cudaError_t launch_rerank(const pkv_index* ix, int64_t C_cap, int64_t id_offset, cudaStream_t stream) {
   const Workspace* ws = ix->ws;
-  int64_t tiles = (C_cap + RR_THREADS - 1) / RR_THREADS;
+  int64_t tiles = (C_cap + RR_THREADS / 2 - 1) / (RR_THREADS / 2);
   if (tiles < 1) tiles = 1;
   dim3 grid((unsigned)tiles, ix->cfg.n_q_heads, ix->batch);
   ProfScope p_(K_RERANK, stream);
-  rerank_kernel<<<grid, RR_THREADS, 0, stream>>>(ix->rec, ws->cand, ws->sel, ws->rtab, ws->qnorm, ix->cap,
-                                                 ix->cfg.n_q_heads, ix->cfg.n_kv_heads, ix->dcfg.G, ws->cap,
-                                                 id_offset, ws->est);
-  return cudaGetLastError();
+  return pdl_launch(rerank_kernel, grid, dim3(RR_THREADS), 0, stream, (const uint8_t*)ix->rec,
+                    (const int32_t*)ws->cand, (const int32_t*)ws->sel, (const float*)ws->rtab,
+                    (const float*)ws->qnorm, ix->cap, ix->cfg.n_q_heads, ix->cfg.n_kv_heads, ix->dcfg.G, ws->cap,
+                    id_offset, ws->est);
 }
 
 cudaError_t launch_topk(const pkv_index* ix, int64_t C_cap, int k, int32_t* out_idx, float* out_est,
@@ -263,9 +450,9 @@ cudaError_t launch_topk(const pkv_index* ix, int64_t C_cap, int k, int32_t* out_
   const Workspace* ws = ix->ws;
   dim3 grid(ix->cfg.n_q_heads, ix->batch);
   ProfScope p_(K_TOPK, stream);
-  topk_kernel<<<grid, TK_THREADS, TK_SMEM, stream>>>(ws->est, ws->cand, ws->sel, ix->cfg.n_q_heads, ws->cap, k, out_stride,
-                                               out_idx, out_est);
-  return cudaGetLastError();
+  return pdl_launch(topk_kernel, grid, dim3(BS_THREADS), TK_SMEM, stream, (const float*)ws->est,
+                    (const int32_t*)ws->cand, (const int32_t*)ws->sel, ix->cfg.n_q_heads, ws->cap, k, out_stride,
+                    out_idx, out_est);
 }
 
 cudaError_t launch_topk_merge(const pkv_index* ix, int P, int k, const float* all_est, const int32_t* all_idx,

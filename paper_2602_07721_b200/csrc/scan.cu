@@ -8,9 +8,8 @@
 //                  id row rotated by t mod 16 bytes, so byte i of the row is that subspace; one PRMT builds the
 //                  smem address (id byte -> bits 8..15, table offset -> bits 0..7). Per-warp score histograms
 //                  in shared memory; per-chunk totals to global (deterministic, no global atomics).
-// threshold_kernel s* = max{s : #(score >= s) >= C} per query head from the histograms, ties in the s* bucket
-//                  handed out newest first (AMB-12), per-chunk output offsets.
-// compact_kernel   writes the candidate ids (score > s*, plus each chunk's share of newest s* ties).
+// select_kernel    threshold s* = max{s : #(score >= s) >= C} per query head from cumulative chunk histograms,
+//                  ties in the s* bucket handed out newest first (AMB-12), then the chunk's candidate ids.
 #include "common.cuh"
 
 namespace pkv {
@@ -33,37 +32,64 @@ __device__ __forceinline__ uint32_t lut_load(uint32_t addr, uint32_t lut_base) {
   return v;
 }
 
-template <int RES, bool FAST>
-__device__ __forceinline__ void scan_loop(const uint8_t* __restrict__ ids_bh, uint32_t* __restrict__ scores_bh,
-                                          uint32_t* hist_w, int64_t t_begin, int64_t t_end, int G,
-                                          uint32_t lut_base) {
+template <bool CHECK>
+__device__ __forceinline__ void load_rows(uint4 (&row)[SCAN_UNROLL], const uint8_t* __restrict__ ids_bh, uint32_t base,
+                                          uint32_t t_end) {
+#pragma unroll
+  for (int u = 0; u < SCAN_UNROLL; ++u) {
+    const uint32_t t = base + (uint32_t)u * SCAN_WARPS * 32;
+    row[u] = (!CHECK || t < t_end) ? ldg_nc_v4(ids_bh + (size_t)t * NB) : make_uint4(0, 0, 0, 0);
+  }
+}
+
+// Score one key (16 conflict-free LUT reads) and record it; G query heads packed in the bytes of acc.
+template <int RES, bool FAST, int G>
+__device__ __forceinline__ void score_key(const uint4& r, const uint32_t (&p)[16], uint32_t lut_base,
+                                          uint32_t* __restrict__ scores_bh, uint32_t* hist_w, uint32_t t) {
+  const uint32_t wds[4] = {r.x, r.y, r.z, r.w};
+  uint32_t acc = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const uint32_t a = prmt(wds[i >> 2], p[i], 0x5504u | ((uint32_t)(i & 3) << 4));
+    acc += lut_load<RES, FAST>(a, lut_base);
+  }
+  scores_bh[t] = acc;
+#pragma unroll
+  for (int hh = 0; hh < G; ++hh) atomicAdd(&hist_w[hh * HB + prmt(acc, 0u, 0x4440u | (uint32_t)hh)], 1u);
+}
+
+// Main loop, software-pipelined: rows of the next round are in flight while this round is scored. Full rounds
+// run without per-key bounds checks; only the last round checks.
+template <int RES, bool FAST, int G>
+__device__ __forceinline__ void scan_loop(uint4 (&row)[SCAN_UNROLL], const uint8_t* __restrict__ ids_bh,
+                                          uint32_t* __restrict__ scores_bh, uint32_t* hist_w, uint32_t t_begin,
+                                          uint32_t t_end, uint32_t lut_base) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t p[16];
 #pragma unroll
   for (int i = 0; i < 16; ++i) p[i] = (uint32_t)(lane + i) * 4u;
-  for (int64_t base = t_begin + (int64_t)warp * 32; base < t_end; base += (int64_t)SCAN_WARPS * 32 * SCAN_UNROLL) {
-    uint4 row[SCAN_UNROLL];
+  constexpr uint32_t ROW = SCAN_WARPS * 32;
+  constexpr uint32_t STEP = ROW * SCAN_UNROLL;
+  uint32_t wbase = t_begin + (uint32_t)warp * 32;  // warp-uniform
+  for (; wbase + (SCAN_UNROLL - 1) * ROW + 32 <= t_end; wbase += STEP) {  // all rows of this warp in range
+    uint4 nxt[SCAN_UNROLL];
+    load_rows<true>(nxt, ids_bh, wbase + STEP + lane, t_end);
+#pragma unroll
+    for (int u = 0; u < SCAN_UNROLL; ++u)
+      score_key<RES, FAST, G>(row[u], p, lut_base, scores_bh, hist_w, wbase + lane + u * ROW);
+#pragma unroll
+    for (int u = 0; u < SCAN_UNROLL; ++u) row[u] = nxt[u];
+  }
+  for (; wbase < t_end; wbase += STEP) {
+    uint4 nxt[SCAN_UNROLL];
+    load_rows<true>(nxt, ids_bh, wbase + STEP + lane, t_end);
 #pragma unroll
     for (int u = 0; u < SCAN_UNROLL; ++u) {
-      const int64_t t = base + (int64_t)u * SCAN_WARPS * 32 + lane;
-      if (t < t_end) row[u] = ldg_nc_v4(ids_bh + t * NB);
-      else row[u] = make_uint4(0, 0, 0, 0);
+      const uint32_t t = wbase + lane + u * ROW;
+      if (t < t_end) score_key<RES, FAST, G>(row[u], p, lut_base, scores_bh, hist_w, t);
     }
 #pragma unroll
-    for (int u = 0; u < SCAN_UNROLL; ++u) {
-      const int64_t t = base + (int64_t)u * SCAN_WARPS * 32 + lane;
-      const uint32_t wds[4] = {row[u].x, row[u].y, row[u].z, row[u].w};
-      uint32_t acc = 0;
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const uint32_t a = prmt(wds[i >> 2], p[i], 0x5504u | ((uint32_t)(i & 3) << 4));
-        acc += lut_load<RES, FAST>(a, lut_base);
-      }
-      if (t < t_end) {
-        scores_bh[t] = acc;
-        for (int hh = 0; hh < G; ++hh) atomicAdd(&hist_w[hh * HB + ((acc >> (8 * hh)) & 0xffu)], 1u);
-      }
-    }
+    for (int u = 0; u < SCAN_UNROLL; ++u) row[u] = nxt[u];
   }
 }
 
@@ -77,196 +103,336 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1)
   const int bh = blockIdx.y, j = blockIdx.x;
   const int64_t t_begin = (int64_t)j * chunk;
   const int64_t t_end = min(n, t_begin + chunk);
+  const uint8_t* ids_bh = ids + (int64_t)bh * cap * NB;
+  pdl_trigger();
+  // the centroid ids do not depend on the query: start streaming them before qprep has finished
+  uint4 row[SCAN_UNROLL];
+  load_rows<true>(row, ids_bh, (uint32_t)t_begin + (threadIdx.x >> 5) * 32 + (threadIdx.x & 31), (uint32_t)t_end);
+  for (int i = threadIdx.x; i < SCAN_WARPS * GMAX * HB; i += SCAN_THREADS) hist[i] = 0u;
+  pdl_wait();  // lookup table comes from qprep
   // expand the compact table [c][16] into 4 interleaved replicas: word c*64 + s + 16 r
   const uint32_t* lg = lut_g + (int64_t)bh * NC * NB;
-  for (int i = threadIdx.x; i < NC * NB; i += SCAN_THREADS) {
-    const int c = i >> 4, s = i & 15;
-    const uint32_t v = lg[i];
+  uint32_t lv[NC * NB / SCAN_THREADS];  // all loads in flight before the stores
 #pragma unroll
-    for (int r = 0; r < 4; ++r) lut[c * 64 + s + 16 * ((r + (c & 1)) & 3)] = v;
+  for (int u = 0; u < NC * NB / SCAN_THREADS; ++u) lv[u] = lg[threadIdx.x + u * SCAN_THREADS];
+#pragma unroll
+  for (int u = 0; u < NC * NB / SCAN_THREADS; ++u) {
+    const int i = threadIdx.x + u * SCAN_THREADS;
+    const int c = i >> 4, s = i & 15;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) lut[c * 64 + s + 16 * ((r + (c & 1)) & 3)] = lv[u];
   }
-  for (int i = threadIdx.x; i < SCAN_WARPS * GMAX * HB; i += SCAN_THREADS) hist[i] = 0u;
   __syncthreads();
   const uint32_t lut_base = (uint32_t)__cvta_generic_to_shared(lut);
-  const uint8_t* ids_bh = ids + (int64_t)bh * cap * NB;
   uint32_t* scores_bh = scores + (int64_t)bh * cap;
   uint32_t* hist_w = hist + (threadIdx.x >> 5) * GMAX * HB;
-  if (lut_base == (uint32_t)RES) scan_loop<RES, true>(ids_bh, scores_bh, hist_w, t_begin, t_end, G, lut_base);
-  else scan_loop<RES, false>(ids_bh, scores_bh, hist_w, t_begin, t_end, G, lut_base);
+  const uint32_t tb = (uint32_t)t_begin, te = (uint32_t)t_end;
+  if (lut_base == (uint32_t)RES) {
+    if (G == 4) scan_loop<RES, true, 4>(row, ids_bh, scores_bh, hist_w, tb, te, lut_base);
+    else if (G == 2) scan_loop<RES, true, 2>(row, ids_bh, scores_bh, hist_w, tb, te, lut_base);
+    else if (G == 3) scan_loop<RES, true, 3>(row, ids_bh, scores_bh, hist_w, tb, te, lut_base);
+    else scan_loop<RES, true, 1>(row, ids_bh, scores_bh, hist_w, tb, te, lut_base);
+  } else {
+    scan_loop<RES, false, 4>(row, ids_bh, scores_bh, hist_w, tb, te, lut_base);  // G <= 4: unused bytes are 0
+  }
   __syncthreads();
-  uint32_t* out = chunk_hist + ((int64_t)bh * MAX_CHUNKS + j) * GMAX * HB;
+  // per-CTA totals, then cumulative (suffix) counts cum[s] = #(score >= s), one warp per query head
   for (int i = threadIdx.x; i < GMAX * HB; i += SCAN_THREADS) {
     uint32_t s = 0;
     for (int w = 0; w < SCAN_WARPS; ++w) s += hist[w * GMAX * HB + i];
-    out[i] = s;
+    hist[i] = s;  // warp 0's slot reused: every warp's reads of slot i precede this write (same thread)
+  }
+  __syncthreads();
+  uint32_t* out = chunk_hist + ((int64_t)bh * MAX_CHUNKS + j) * GMAX * HB;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp < GMAX) {
+    // lane l owns bins 4l..4l+3; suffix sums across lanes from the top
+    uint32_t v[4], tot = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      v[e] = hist[warp * HB + 4 * lane + e];
+      tot += v[e];
+    }
+    uint32_t inc = tot;  // inclusive suffix over lanes >= lane
+#pragma unroll
+    for (int x = 1; x < 32; x <<= 1) {
+      const uint32_t o = __shfl_down_sync(0xffffffffu, inc, x);
+      if (lane + x < 32) inc += o;
+    }
+    uint32_t run = inc - tot;  // counts of bins above this lane's range
+#pragma unroll
+    for (int e = 3; e >= 0; --e) {
+      run += v[e];
+      out[warp * HB + 4 * lane + e] = run;
+    }
   }
 }
 
-// sel layout per (b, q head): [0] s*, [1] gt_local, [2] C_local, [3] take_local,
-// then per chunk j: [4+4j] gt_off, [+1] tie_off, [+2] take_j, [+3] eq_j
+// sel layout per (b, q head): [0] s*, [1] gt_local, [2] C_local, [3] take_local (written by chunk 0's CTA)
 constexpr int SEL_STRIDE = 4 + 4 * MAX_CHUNKS;
+constexpr int SEL_THREADS = 1024;
+constexpr int SEL_SMEM = 32 * 8 * 32 * 8;  // 32 warps x 256 entries x uint2
 
-__global__ void __launch_bounds__(HB) threshold_kernel(const uint32_t* __restrict__ chunk_hist,
-                                                        const uint32_t* __restrict__ all_hist, int P, int rank,
-                                                        int nchunks, int n_q, int n_kv, int G, int batch,
-                                                        int64_t C, int32_t* __restrict__ sel) {
-  __shared__ uint32_t tot[HB], loc[HB];
-  __shared__ int s_star_s, take_local_s, gt_local_s;
-  __shared__ int gt_j[MAX_CHUNKS], eq_j[MAX_CHUNKS];
-  const int h = blockIdx.x, b = blockIdx.y;
-  const int g = h / G, hh = h % G;
-  const int bin = threadIdx.x;
-  const uint32_t* ch = chunk_hist + ((int64_t)(b * n_kv + g) * MAX_CHUNKS) * GMAX * HB + hh * HB;
-  uint32_t l = 0;
-  for (int j = 0; j < nchunks; ++j) l += ch[(int64_t)j * GMAX * HB + bin];
-  loc[bin] = l;
-  uint32_t t = l;
-  if (P > 1) {
-    t = 0;
-    for (int r = 0; r < P; ++r) t += all_hist[(((int64_t)r * batch + b) * n_q + h) * HB + bin];
-  }
-  tot[bin] = t;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int64_t ge = 0;
-    int s_star = HB;  // C == 0: nothing selected
-    if (C > 0) {
-      for (int s = HB - 1; s >= 0; --s) {
-        if (ge + tot[s] >= C) { s_star = s; break; }
-        ge += tot[s];
-      }
-    }
-    int64_t need = (s_star < HB) ? C - ge : 0;
-    // ties: newest rank first
-    if (P > 1 && s_star < HB) {
-      for (int r = P - 1; r > rank; --r) {
-        need -= all_hist[(((int64_t)r * batch + b) * n_q + h) * HB + s_star];
-        if (need < 0) need = 0;
-      }
-    }
-    int64_t eq_local = (s_star < HB) ? loc[s_star] : 0;
-    int64_t take_local = need < eq_local ? need : eq_local;
-    int64_t gt_local = 0;
-    for (int s = s_star + 1; s < HB; ++s) gt_local += loc[s];
-    s_star_s = s_star;
-    take_local_s = (int)take_local;
-    gt_local_s = (int)gt_local;
-  }
-  __syncthreads();
-  const int s_star = s_star_s;
-  for (int j = threadIdx.x; j < nchunks; j += blockDim.x) {
-    const uint32_t* cj = ch + (int64_t)j * GMAX * HB;
-    uint32_t gsum = 0;
-    for (int s = s_star + 1; s < HB; ++s) gsum += cj[s];
-    gt_j[j] = (int)gsum;
-    eq_j[j] = (s_star < HB) ? (int)cj[s_star] : 0;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int32_t* o = sel + ((int64_t)b * n_q + h) * SEL_STRIDE;
-    o[0] = s_star;
-    o[1] = gt_local_s;
-    o[2] = gt_local_s + take_local_s;
-    o[3] = take_local_s;
-    int run = 0;
-    for (int j = 0; j < nchunks; ++j) {
-      o[4 + 4 * j] = run;
-      run += gt_j[j];
-    }
-    int rem = take_local_s, toff = gt_local_s;
-    for (int j = nchunks - 1; j >= 0; --j) {
-      const int take = rem < eq_j[j] ? rem : eq_j[j];
-      o[4 + 4 * j + 1] = toff;
-      o[4 + 4 * j + 2] = take;
-      o[4 + 4 * j + 3] = eq_j[j];
-      toff += take;
-      rem -= take;
-    }
-  }
-}
-
-constexpr int CMP_THREADS = 1024;
-
-__global__ void __launch_bounds__(CMP_THREADS) compact_kernel(const uint32_t* __restrict__ scores,
-                                                               const int32_t* __restrict__ sel, int64_t cap,
-                                                               int64_t n, int64_t chunk, int n_q, int n_kv, int G,
-                                                               int64_t id_offset, int64_t cand_stride,
-                                                               int32_t* __restrict__ cand) {
-  __shared__ uint32_t wtot[32][2 * GMAX];
-  __shared__ uint32_t wexc[32][2 * GMAX];
-  __shared__ uint32_t ttot[2 * GMAX];
-  __shared__ int prm[GMAX][5];
+// Fused threshold + compaction (bucket_topk). Chunk histograms are CUMULATIVE:
+// cum_j[h][s] = #(score >= s) in chunk j. Every CTA of a (sequence, KV head) recomputes, for its query heads,
+//   s*      = max{s : sum_j cum_j[s] >= C}            (global over ranks when sharded: all_hist)
+//   ties    : C - #(> s*) taken newest first — newest rank, then newest chunk, then newest key (AMB-12)
+//   offsets : gt_off = sum_{j' < j} #(> s*) in j',  tie quota/offset from the suffix of newer chunks
+// and then writes its chunk's candidates: two passes over the packed scores (L2), warp-level ballots,
+// one block scan of the per-warp counts (no per-tile block synchronisation).
+__global__ void __launch_bounds__(SEL_THREADS) select_kernel(
+    const uint32_t* __restrict__ chunk_hist, const uint32_t* __restrict__ all_hist, int P, int rank, int batch,
+    const uint32_t* __restrict__ scores, int64_t cap, int64_t n, int64_t chunk, int nchunks, int n_q, int n_kv,
+    int G, int64_t C, int64_t id_offset, int64_t cand_stride, int32_t* __restrict__ cand, int32_t* __restrict__ sel) {
+  __shared__ uint32_t Hg[GMAX][HB];   // global cumulative counts
+  __shared__ uint32_t Hl[GMAX][HB];   // this rank's cumulative counts
+  __shared__ int s_star[GMAX], gt_local[GMAX], take_local[GMAX];
+  __shared__ int p_gt_off[GMAX], p_tie_off[GMAX], p_take[GMAX], p_eq[GMAX];
+  __shared__ uint32_t wcnt[32][2 * GMAX];
+  extern __shared__ uint2 sel_list[];  // per-warp compaction lists (VB * 32 entries each), SEL_SMEM bytes
+  pdl_trigger();
+  pdl_wait();
   const int bh = blockIdx.y, j = blockIdx.x;
   const int b = bh / n_kv, g = bh % n_kv;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t t_begin = (int64_t)j * chunk;
-  const int64_t t_end = min(n, t_begin + chunk);
-  if (threadIdx.x < G) {
-    const int32_t* o = sel + ((int64_t)b * n_q + g * G + threadIdx.x) * SEL_STRIDE;
-    prm[threadIdx.x][0] = o[0];
-    prm[threadIdx.x][1] = o[4 + 4 * j];
-    prm[threadIdx.x][2] = o[4 + 4 * j + 1];
-    prm[threadIdx.x][3] = o[4 + 4 * j + 2];
-    prm[threadIdx.x][4] = o[4 + 4 * j + 3];
+  const uint32_t* chb = chunk_hist + (int64_t)bh * MAX_CHUNKS * GMAX * HB;
+  // A1: local and global cumulative totals. Thread (half, hh, s): half of the chunks, loads batched 16 at a time
+  // so that many L2 requests are in flight (a load->add chain per chunk would serialise their latency).
+  __shared__ uint32_t Hpart[GMAX][HB];
+  {
+    const int e = threadIdx.x & (GMAX * HB - 1), half = threadIdx.x / (GMAX * HB);
+    const int hh = e / HB, s = e % HB;
+    const int c_lo = half ? nchunks / 2 : 0, c_hi = half ? nchunks : nchunks / 2;
+    uint32_t l = 0;
+    for (int c0 = c_lo; c0 < c_hi; c0 += 16) {
+      uint32_t v[16];
+#pragma unroll
+      for (int k2 = 0; k2 < 16; ++k2)
+        v[k2] = (hh < G && c0 + k2 < c_hi) ? chb[((int64_t)(c0 + k2) * GMAX + hh) * HB + s] : 0u;
+#pragma unroll
+      for (int k2 = 0; k2 < 16; ++k2) l += v[k2];
+    }
+    if (half) Hpart[hh][s] = l;
+    __syncthreads();
+    if (!half && hh < G) {
+      l += Hpart[hh][s];
+      Hl[hh][s] = l;
+      uint32_t t = l;
+      if (P > 1) {
+        uint32_t v[MAX_RANKS];
+#pragma unroll
+        for (int r = 0; r < MAX_RANKS; ++r)
+          v[r] = r < P ? all_hist[(((int64_t)r * batch + b) * n_q + g * G + hh) * HB + s] : 0u;
+        t = 0;
+#pragma unroll
+        for (int r = 0; r < MAX_RANKS; ++r) t += v[r];
+      }
+      Hg[hh][s] = t;
+    }
   }
   __syncthreads();
-  uint32_t run_gt[GMAX] = {0, 0, 0, 0}, run_eq[GMAX] = {0, 0, 0, 0};
-  const uint32_t lt_mask = (1u << lane) - 1u;
-  const uint32_t* sc = scores + (int64_t)bh * cap;
-  for (int64_t base = t_begin; base < t_end; base += CMP_THREADS) {
-    const int64_t t = base + threadIdx.x;
-    const uint32_t s = (t < t_end) ? sc[t] : 0xffffffffu;
-    bool fgt[GMAX], feq[GMAX];
-    uint32_t pre[2 * GMAX];
+  // A2: threshold per query head (warp hh)
+  if (warp < G) {
+    const int hh = warp;
+    int ss = -1;
+    if (C > 0) {
 #pragma unroll
-    for (int hh = 0; hh < GMAX; ++hh) {
-      const int sv = (int)((s >> (8 * hh)) & 0xffu);
-      const bool valid = (t < t_end) && hh < G;
-      fgt[hh] = valid && sv > prm[hh < G ? hh : 0][0];
-      feq[hh] = valid && sv == prm[hh < G ? hh : 0][0];
-      const uint32_t mg = __ballot_sync(0xffffffffu, fgt[hh]);
-      const uint32_t me = __ballot_sync(0xffffffffu, feq[hh]);
-      pre[2 * hh] = __popc(mg & lt_mask);
-      pre[2 * hh + 1] = __popc(me & lt_mask);
-      if (lane == 0) {
-        wtot[warp][2 * hh] = __popc(mg);
-        wtot[warp][2 * hh + 1] = __popc(me);
+      for (int e = 0; e < HB / 32; ++e) {
+        const int s = lane + 32 * e;
+        const unsigned m = __ballot_sync(0xffffffffu, Hg[hh][s] >= (uint32_t)C);
+        if (m) ss = 32 * e + 31 - __clz(m);
       }
     }
-    __syncthreads();
-    if (warp == 0) {
-#pragma unroll
-      for (int k = 0; k < 2 * GMAX; ++k) {
-        const uint32_t v = wtot[lane][k];
-        uint32_t inc = v;
-#pragma unroll
-        for (int x = 1; x < 32; x <<= 1) {
-          const uint32_t o = __shfl_up_sync(0xffffffffu, inc, x);
-          if (lane >= x) inc += o;
+    if (lane == 0) {
+      int take = 0, gtl = 0, st = HB;
+      if (ss >= 0) {
+        st = ss;
+        const int64_t gt_g = (ss + 1 < HB) ? Hg[hh][ss + 1] : 0;
+        int64_t need = C - gt_g;
+        for (int r = P - 1; r > rank && P > 1; --r) {
+          const uint32_t* hr = all_hist + (((int64_t)r * batch + b) * n_q + g * G + hh) * HB;
+          need -= (int64_t)hr[ss] - (ss + 1 < HB ? hr[ss + 1] : 0);
+          if (need < 0) need = 0;
         }
-        wexc[lane][k] = inc - v;
-        if (lane == 31) ttot[k] = inc;
+        gtl = (ss + 1 < HB) ? (int)Hl[hh][ss + 1] : 0;
+        const int64_t eql = (int64_t)Hl[hh][ss] - gtl;
+        take = (int)(need < eql ? need : eql);
+      }
+      s_star[hh] = st;
+      gt_local[hh] = gtl;
+      take_local[hh] = take;
+    }
+    __syncwarp();
+    // A3: this chunk's offsets: prefix of #(> s*) over older chunks, suffix of ties over newer chunks
+    const int st = s_star[hh];
+    uint32_t gt_before = 0, eq_after = 0;
+    int my_gt = 0, my_eq = 0;
+    for (int jj = lane; jj < nchunks; jj += 32) {
+      const uint32_t* cj = chb + ((int64_t)jj * GMAX + hh) * HB;
+      const uint32_t gtv = (st + 1 < HB) ? cj[st + 1] : 0;
+      const uint32_t eqv = (st < HB) ? cj[st] - gtv : 0;
+      if (jj < j) gt_before += gtv;
+      if (jj > j) eq_after += eqv;
+      if (jj == j) {
+        my_gt = (int)gtv;
+        my_eq = (int)eqv;
       }
     }
-    __syncthreads();
+#pragma unroll
+    for (int x = 16; x > 0; x >>= 1) {
+      gt_before += __shfl_xor_sync(0xffffffffu, gt_before, x);
+      eq_after += __shfl_xor_sync(0xffffffffu, eq_after, x);
+      my_gt += __shfl_xor_sync(0xffffffffu, my_gt, x);
+      my_eq += __shfl_xor_sync(0xffffffffu, my_eq, x);
+    }
+    if (lane == 0) {
+      const int tl = take_local[hh];
+      const int taken_after = (int)eq_after < tl ? (int)eq_after : tl;
+      const int rem = tl - taken_after;
+      p_gt_off[hh] = (int)gt_before;
+      p_tie_off[hh] = gt_local[hh] + taken_after;
+      p_take[hh] = rem < my_eq ? rem : my_eq;
+      p_eq[hh] = my_eq;
+      if (j == 0) {
+        int32_t* o = sel + ((int64_t)b * n_q + g * G + hh) * SEL_STRIDE;
+        o[0] = st;
+        o[1] = gt_local[hh];
+        o[2] = gt_local[hh] + tl;
+        o[3] = tl;
+      }
+      (void)my_gt;
+    }
+  }
+  __syncthreads();
+  // B: compaction of this chunk. Warp w owns the contiguous segment [seg0, seg1).
+  // Packed comparisons (scores <= 127, 4 query heads per u32): with K_gt = 0x7f - s*, K_ge = 0x80 - s* per byte,
+  // bit 7 of byte h of (score + K_gt) is [score_h > s*_h] and of (score + K_ge) is [score_h >= s*_h] — no carries
+  // cross bytes. Unused heads get s* = 127, which no score reaches.
+  const uint32_t t_begin = (uint32_t)j * (uint32_t)chunk;
+  const uint32_t t_end = (uint32_t)min(n, (int64_t)t_begin + chunk);
+  const uint32_t len = t_end - t_begin;
+  const uint32_t seg = ((len + 32 * 32 - 1) / (32 * 32)) * 32;
+  const uint32_t seg0 = t_begin + warp * seg;
+  const uint32_t seg1 = min(t_end, seg0 + seg);
+  const uint32_t* sc = scores + (int64_t)bh * cap;
+  uint32_t kgt = 0, kge = 0;
+#pragma unroll
+  for (int hh = 0; hh < GMAX; ++hh) {
+    const uint32_t st = (hh < G && s_star[hh] < HB) ? (uint32_t)s_star[hh] : 127u;
+    kgt |= (0x7fu - st) << (8 * hh);
+    kge |= (0x80u - st) << (8 * hh);
+  }
+  // pass 1: per-head counts of this warp's segment; the lane's scores are loaded 8 at a time (all in flight)
+  // and kept in registers for pass 2 when the segment is short enough (the 128K case)
+  constexpr int VB = 8;
+  uint32_t vreg[VB];
+  const uint32_t nper = (seg1 > seg0) ? (seg1 - seg0 + 31) / 32 : 0;  // keys per lane (upper bound)
+  uint32_t tot_gt[GMAX] = {0, 0, 0, 0}, tot_eq[GMAX] = {0, 0, 0, 0};
+  for (uint32_t i0 = 0; i0 < nper; i0 += VB) {
+#pragma unroll
+    for (int k2 = 0; k2 < VB; ++k2) {
+      const uint32_t t = seg0 + lane + 32u * (i0 + k2);
+      vreg[k2] = (t < seg1) ? sc[t] : 0u;
+    }
+    uint32_t cgt = 0, ceq = 0;
+#pragma unroll
+    for (int k2 = 0; k2 < VB; ++k2) {
+      const uint32_t t = seg0 + lane + 32u * (i0 + k2);
+      const uint32_t gtb = (vreg[k2] + kgt) & 0x80808080u;
+      const uint32_t geb = (vreg[k2] + kge) & 0x80808080u;
+      if (t < seg1) {
+        cgt += gtb >> 7;
+        ceq += (geb & ~gtb) >> 7;
+      }
+    }
 #pragma unroll
     for (int hh = 0; hh < GMAX; ++hh) {
-      if (hh >= G) break;
-      const int h = g * G + hh;
-      int32_t* cd = cand + ((int64_t)b * n_q + h) * cand_stride;
-      if (fgt[hh]) {
-        const uint32_t pos = prm[hh][1] + run_gt[hh] + wexc[warp][2 * hh] + pre[2 * hh];
-        cd[pos] = (int32_t)(t + id_offset);
-      }
-      if (feq[hh]) {
-        const uint32_t asc = run_eq[hh] + wexc[warp][2 * hh + 1] + pre[2 * hh + 1];
-        const int from_end = prm[hh][4] - 1 - (int)asc;
-        if (from_end < prm[hh][3]) cd[prm[hh][2] + from_end] = (int32_t)(t + id_offset);
-      }
-      run_gt[hh] += ttot[2 * hh];
-      run_eq[hh] += ttot[2 * hh + 1];
+      tot_gt[hh] += (cgt >> (8 * hh)) & 0xffu;
+      tot_eq[hh] += (ceq >> (8 * hh)) & 0xffu;
     }
-    __syncthreads();
+  }
+#pragma unroll
+  for (int hh = 0; hh < GMAX; ++hh) {
+    uint32_t a1 = tot_gt[hh];
+    uint32_t a2 = tot_eq[hh];
+#pragma unroll
+    for (int x = 16; x > 0; x >>= 1) {
+      a1 += __shfl_xor_sync(0xffffffffu, a1, x);
+      a2 += __shfl_xor_sync(0xffffffffu, a2, x);
+    }
+    if (lane == 0) {
+      wcnt[warp][2 * hh] = a1;
+      wcnt[warp][2 * hh + 1] = a2;
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int k = 0; k < 2 * GMAX; ++k) {
+      const uint32_t v = wcnt[lane][k];
+      uint32_t inc = v;
+#pragma unroll
+      for (int x = 1; x < 32; x <<= 1) {
+        const uint32_t o = __shfl_up_sync(0xffffffffu, inc, x);
+        if (lane >= x) inc += o;
+      }
+      wcnt[lane][k] = inc - v;  // exclusive base of warp `lane`
+    }
+  }
+  __syncthreads();
+  uint32_t run_gt[GMAX], run_eq[GMAX];
+#pragma unroll
+  for (int hh = 0; hh < GMAX; ++hh) {
+    run_gt[hh] = wcnt[warp][2 * hh];
+    run_eq[hh] = wcnt[warp][2 * hh + 1];
+  }
+  int32_t* cd[GMAX];
+#pragma unroll
+  for (int hh = 0; hh < GMAX; ++hh) cd[hh] = cand + ((int64_t)b * n_q + g * G + (hh < G ? hh : 0)) * cand_stride;
+  const uint32_t lt = (1u << lane) - 1u;
+  // pass 2: keys with score >= s* for at least one head (~4 x beta of them) are first compacted, in key
+  // order, into a per-warp list; the per-head ballots then run over that list only.
+  uint2* wl = sel_list + warp * (VB * 32);
+  for (uint32_t i0 = 0; i0 < nper; i0 += VB) {
+    if (nper > VB) {
+#pragma unroll
+      for (int k2 = 0; k2 < VB; ++k2) {
+        const uint32_t t = seg0 + lane + 32u * (i0 + k2);
+        vreg[k2] = (t < seg1) ? sc[t] : 0u;
+      }
+    }
+    uint32_t nl = 0;
+#pragma unroll
+    for (int k2 = 0; k2 < VB; ++k2) {
+      const uint32_t t = seg0 + lane + 32u * (i0 + k2);
+      const uint32_t gtb = (vreg[k2] + kgt) & 0x80808080u;
+      const uint32_t geb = (vreg[k2] + kge) & 0x80808080u;
+      const bool keep = (t < seg1) && geb != 0u;
+      const uint32_t m = __ballot_sync(0xffffffffu, keep);
+      if (keep) wl[nl + __popc(m & lt)] = make_uint2(t, gtb | ((geb & ~gtb) >> 1));  // bit7: >, bit6: ==
+      nl += __popc(m);
+    }
+    __syncwarp();
+    for (uint32_t l0 = 0; l0 < nl; l0 += 32) {
+      const bool valid = l0 + lane < nl;
+      const uint2 ent = valid ? wl[l0 + lane] : make_uint2(0u, 0u);
+#pragma unroll
+      for (int hh = 0; hh < GMAX; ++hh) {
+        const bool fg = (ent.y >> (8 * hh + 7)) & 1u;
+        const bool fe = (ent.y >> (8 * hh + 6)) & 1u;
+        const uint32_t mg = __ballot_sync(0xffffffffu, fg);
+        const uint32_t me = __ballot_sync(0xffffffffu, fe);
+        if (fg) cd[hh][p_gt_off[hh] + run_gt[hh] + __popc(mg & lt)] = (int32_t)(ent.x + id_offset);
+        if (fe) {
+          const int asc = (int)(run_eq[hh] + __popc(me & lt));
+          const int from_end = p_eq[hh] - 1 - asc;
+          if (from_end < p_take[hh]) cd[hh][p_tie_off[hh] + from_end] = (int32_t)(ent.x + id_offset);
+        }
+        run_gt[hh] += __popc(mg);
+        run_eq[hh] += __popc(me);
+      }
+    }
+    __syncwarp();
   }
 }
 
@@ -285,13 +451,17 @@ __global__ void dbg_scores_kernel(const uint32_t* __restrict__ scores, int64_t c
 cudaError_t init_scan_attrs() {
   cudaError_t e = cudaFuncSetAttribute(scan_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, SCAN_SMEM);
   if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SEL_SMEM);
+  if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(scan_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, SCAN_SMEM);
 }
 
 ScanPlan plan_scan(const pkv_index* ix, int64_t n) {
+  // One 1024-thread CTA per SM (~114 KB smem): never more CTAs than SMs, so there is no second wave.
   ScanPlan p;
   const int units = ix->batch * ix->cfg.n_kv_heads;
-  int target = (ix->num_sms + units - 1) / units;  // ~1 CTA per SM (1024 threads, ~113 KB smem)
+  int target = ix->num_sms / units;
+  if (target < 1) target = 1;
   int64_t chunk = (n + target - 1) / target;
   if (chunk < 2048) chunk = 2048;
   chunk = (chunk + 31) / 32 * 32;
@@ -312,36 +482,24 @@ cudaError_t launch_scan(const pkv_index* ix, int64_t n, const ScanPlan& plan, cu
   cudaError_t e;
   if (ix->smem_reserved == 1024) {
     ProfScope p_(K_SCAN, stream);
-    scan_kernel<1024><<<grid, SCAN_THREADS, SCAN_SMEM, stream>>>(ix->ids, ws->lut, ws->scores, ws->chunk_hist,
-                                                                  ix->cap, n, plan.chunk, ix->dcfg.G);
+    e = pdl_launch(scan_kernel<1024>, grid, dim3(SCAN_THREADS), SCAN_SMEM, stream, (const uint8_t*)ix->ids,
+                   (const uint32_t*)ws->lut, ws->scores, ws->chunk_hist, ix->cap, n, plan.chunk, ix->dcfg.G);
   } else {
     ProfScope p_(K_SCAN, stream);
-    scan_kernel<0><<<grid, SCAN_THREADS, SCAN_SMEM, stream>>>(ix->ids, ws->lut, ws->scores, ws->chunk_hist,
-                                                               ix->cap, n, plan.chunk, ix->dcfg.G);
+    e = pdl_launch(scan_kernel<0>, grid, dim3(SCAN_THREADS), SCAN_SMEM, stream, (const uint8_t*)ix->ids,
+                   (const uint32_t*)ws->lut, ws->scores, ws->chunk_hist, ix->cap, n, plan.chunk, ix->dcfg.G);
   }
-  e = cudaGetLastError();
   return e;
 }
 
-cudaError_t launch_threshold(const pkv_index* ix, const ScanPlan& plan, const uint32_t* all_hist, int P, int rank,
-                             int64_t C, cudaStream_t stream) {
-  const Workspace* ws = ix->ws;
-  dim3 grid(ix->cfg.n_q_heads, ix->batch);
-  ProfScope p_(K_THRESHOLD, stream);
-  threshold_kernel<<<grid, HB, 0, stream>>>(ws->chunk_hist, all_hist, P, rank, plan.nchunks, ix->cfg.n_q_heads,
-                                            ix->cfg.n_kv_heads, ix->dcfg.G, ix->batch, C, ws->sel);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_compact(const pkv_index* ix, int64_t n, const ScanPlan& plan, int64_t id_offset,
-                           int64_t cand_stride, cudaStream_t stream) {
+cudaError_t launch_select(const pkv_index* ix, int64_t n, const ScanPlan& plan, const uint32_t* all_hist, int P,
+                          int rank, int64_t C, int64_t id_offset, cudaStream_t stream) {
   const Workspace* ws = ix->ws;
   dim3 grid(plan.nchunks, ix->batch * ix->cfg.n_kv_heads);
-  ProfScope p_(K_COMPACT, stream);
-  compact_kernel<<<grid, CMP_THREADS, 0, stream>>>(ws->scores, ws->sel, ix->cap, n, plan.chunk, ix->cfg.n_q_heads,
-                                                   ix->cfg.n_kv_heads, ix->dcfg.G, id_offset, cand_stride,
-                                                   ws->cand);
-  return cudaGetLastError();
+  ProfScope p_(K_SELECT, stream);
+  return pdl_launch(select_kernel, grid, dim3(SEL_THREADS), SEL_SMEM, stream, (const uint32_t*)ws->chunk_hist, all_hist, P,
+                    rank, ix->batch, (const uint32_t*)ws->scores, ix->cap, n, plan.chunk, plan.nchunks,
+                    ix->cfg.n_q_heads, ix->cfg.n_kv_heads, ix->dcfg.G, C, id_offset, ws->cap, ws->cand, ws->sel);
 }
 
 cudaError_t launch_dbg_scores(const pkv_index* ix, int64_t n, uint8_t* out, cudaStream_t stream) {

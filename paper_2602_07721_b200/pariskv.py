@@ -73,7 +73,7 @@ _lib.pkv_kernel_name.restype = ctypes.c_char_p
 _lib.pkv_kernel_name.argtypes = [_i32]
 
 EXPORTED = tuple(_sigs) + ("pkv_last_error", "pkv_version", "pkv_kernel_name")
-KERNEL_KINDS = ("encode", "qprep", "scan", "threshold", "compact", "rerank", "topk", "topk_merge", "attend",
+KERNEL_KINDS = ("encode", "qprep", "scan", "select", "unused", "rerank", "topk", "topk_merge", "attend",
                 "combine", "head_hist", "export", "debug")
 
 
