@@ -39,6 +39,10 @@ CONFIGS = {
     "128k": dict(batch=1, context=131072, workload="llama3.1-8b-shape bs1 ctx131072 decode step, 32 layers"),
     # BASELINE configs[2]: bs=8 at 32K
     "32k_bs8": dict(batch=8, context=32768, workload="llama3.1-8b-shape bs8 ctx32768 decode step, 32 layers"),
+    # BASELINE configs[4]: 1M-token context, full-precision K/V in pinned host memory read through UVA
+    # (P:515-517); 32 per-layer indices in HBM built from 4 distinct datasets (4 x 4.3 GB of host K/V)
+    "1m": dict(batch=1, context=1048576, uva=True, datasets=4,
+               workload="llama3.1-8b-shape bs1 ctx1048576 decode step, 32 layers, K/V in pinned host memory (UVA)"),
 }
 
 
@@ -138,23 +142,34 @@ def run_ours(args):
     cfg = pkv.config_init(N_Q, N_KV, synth.rotation_sign_bits())
     L = args.layers
 
-    # ---- synthetic inputs (HBM resident), per layer distinct buffers ----
+    # ---- synthetic inputs, per layer distinct indices (> L2 touched per step) ----
+    uva = cfgw.get("uva", False)
+    n_data = min(L, cfgw.get("datasets", L))
     layers = []
+    data = []
     for l in range(L):
-        seed = 1000 * l
-        stats = synth.head_stats(seed, N_KV, device=dev)
-        K = synth.llm_keys(seed, batch, N_KV, n, device=dev, stats=stats)
-        q = synth.llm_queries(seed, batch, N_Q, N_KV, device=dev, stats=stats)
-        synth.plant(K, q, seed)
-        V = synth.values(seed, batch, N_KV, n, device=dev)
-        Kl, Vl = K[:, :, lo:hi].contiguous(), V[:, :, lo:hi].contiguous()
-        del K, V
-        Kh = synth.isotropic(seed + 7, (batch, N_KV, n_hot, D), device=dev)
-        Vh = synth.isotropic(seed + 8, (batch, N_KV, n_hot, D), device=dev)
+        if l < n_data:
+            seed = 1000 * l
+            stats = synth.head_stats(seed, N_KV, device=dev)
+            K = synth.llm_keys(seed, batch, N_KV, n, device=dev, stats=stats)
+            q = synth.llm_queries(seed, batch, N_Q, N_KV, device=dev, stats=stats)
+            synth.plant(K, q, seed)
+            V = synth.values(seed, batch, N_KV, n, device=dev)
+            Kl, Vl = K[:, :, lo:hi].contiguous(), V[:, :, lo:hi].contiguous()
+            del K, V
+            Kh = synth.isotropic(seed + 7, (batch, N_KV, n_hot, D), device=dev)
+            Vh = synth.isotropic(seed + 8, (batch, N_KV, n_hot, D), device=dev)
+            if uva:  # full-precision K/V live in pinned host memory; the GPU keeps only summaries + hot rows
+                Kd, Vd = Kl, Vl
+                Kl, Vl = Kl.cpu().pin_memory(), Vl.cpu().pin_memory()
+                data.append(dict(K=Kl, V=Vl, Kd=Kd, Kh=Kh, Vh=Vh, q=q.contiguous()))
+            else:
+                data.append(dict(K=Kl, V=Vl, Kd=Kl, Kh=Kh, Vh=Vh, q=q.contiguous()))
+        d = data[l % n_data]
         ix = pkv.Index(cfg, batch, n_loc, device=local)
         if layers:
             ix.share_workspace(layers[0]["ix"])
-        layers.append(dict(ix=ix, K=Kl, V=Vl, Kh=Kh, Vh=Vh, q=q.contiguous(),
+        layers.append(dict(ix=ix, K=d["K"], V=d["V"], Kd=d["Kd"], Kh=d["Kh"], Vh=d["Vh"], q=d["q"],
                            idx=torch.empty(batch, N_Q, TOP_K, dtype=torch.int32, device=dev),
                            est=torch.empty(batch, N_Q, TOP_K, dtype=torch.float32, device=dev),
                            out=torch.empty(batch, N_Q, D, dtype=torch.bfloat16, device=dev),
@@ -171,17 +186,32 @@ def run_ours(args):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for ly in layers:
-        pkv.encode_keys(ly["ix"], ly["K"])
+        pkv.encode_keys(ly["ix"], ly["Kd"])
     e1.record()
     torch.cuda.synchronize()
     enc_ms_layer = e0.elapsed_time(e1) / L
-
-    def step():
+    if uva:  # the device copies were only needed to build the summaries
+        for d in data:
+            d["Kd"] = None
         for ly in layers:
+            ly["Kd"] = None
+        torch.cuda.empty_cache()
+
+    fused = world == 1 and not args.two_calls
+
+    def layer_call(ly):
+        if fused:  # one decode step of one layer: retrieval + attention scheduled as one unit
+            pkv.retrieve_and_attend(ly["ix"], ly["q"], ly["K"], ly["V"], TOP_K, ly["Kh"], ly["Vh"], probes_T=T,
+                                    n_cand=C, out_idx=ly["idx"], out_est=ly["est"], out=ly["out"], lse=ly["lse"])
+        else:
             pkv.retrieve_topk(ly["ix"], ly["q"], TOP_K, probes_T=T, n_cand=C, n_global=n, out_idx=ly["idx"],
                               out_est=ly["est"])
             pkv.sparse_attend(ly["ix"], ly["q"], ly["K"], ly["V"], ly["idx"], ly["Kh"], ly["Vh"], out=ly["out"],
                               lse=ly["lse"])
+
+    def step():
+        for ly in layers:
+            layer_call(ly)
 
     # warm-up (eager) + launch accounting
     for _ in range(max(1, args.warmup)):
@@ -253,10 +283,7 @@ def run_ours(args):
     def step_e2e():
         for ly, qh, oh in zip(layers, q_host, o_host):
             ly["q"].copy_(qh, non_blocking=True)
-            pkv.retrieve_topk(ly["ix"], ly["q"], TOP_K, probes_T=T, n_cand=C, n_global=n, out_idx=ly["idx"],
-                              out_est=ly["est"])
-            pkv.sparse_attend(ly["ix"], ly["q"], ly["K"], ly["V"], ly["idx"], ly["Kh"], ly["Vh"], out=ly["out"],
-                              lse=ly["lse"])
+            layer_call(ly)
             oh.copy_(ly["out"], non_blocking=True)
 
     if use_graph:
@@ -277,14 +304,36 @@ def run_ours(args):
     e2e_ms = timed(run2, args.steps) / args.steps
     e2e_eager_ms = timed(step_e2e, max(3, min(args.steps, 20))) / max(3, min(args.steps, 20))
 
+    # ---- context: dense decode attention over the same retrieval-zone K/V (PyTorch SDPA, Eq. 1) ----
+    dense_us = None
+    if not uva and world == 1 and not args.no_dense:
+        import torch.nn.functional as F
+        qs = [ly["q"].unsqueeze(2) for ly in layers]
+
+        def dense_step():
+            for ly, q4 in zip(layers, qs):
+                F.scaled_dot_product_attention(q4, ly["K"], ly["V"], enable_gqa=True)
+
+        try:
+            for _ in range(2):
+                dense_step()
+            dense_us = round(timed(dense_step, 5) / 5 * 1000.0 / L, 2)
+        except Exception as e:  # SDPA GQA path unavailable: report why instead of a number
+            dense_us = f"unavailable: {type(e).__name__}"
+
     # ---- roofline of the dominant kernel (algorithmic bytes / measured average launch time) ----
     hbm_peak, peak_kind = peaks()
     alg = {
-        "scan": batch * N_KV * n_loc * 16,                                    # 16 B ids per key per KV head
-        "rerank": batch * N_Q * min(C, n_loc) * (128 + 8),                    # 128 B record + id/est per cand
-        "attend": batch * (N_Q * TOP_K * 512 + (N_KV * n_hot * 512 if rank == world - 1 else 0)),
-        "topk": batch * N_Q * min(C, n_loc) * 8,
-        "compact": batch * N_KV * n_loc * 4,
+        # 16 B of centroid ids per (key, KV head)
+        "scan": batch * N_KV * n_loc * 16,
+        # bucket_topk reads the packed scores (4 B per key and KV head); the fused RSQ-IP rerank gathers one
+        # 128 B record and writes id + estimate (8 B) per (candidate, query head)
+        "select": batch * N_KV * n_loc * 4 + batch * N_Q * min(C, n_loc) * (128 + 8),
+        # fused path: top-k over (est, id) pairs + gather of the k selected K/V rows (512 B per row and head);
+        # two-call path: top-k only
+        "topk": batch * N_Q * min(C, n_loc) * 8 + (batch * N_Q * TOP_K * 512 if fused else 0),
+        # fused path: hot rows only (read once per KV head); two-call path: hot + retrieved rows
+        "attend": batch * ((0 if fused else N_Q * TOP_K * 512) + (N_KV * n_hot * 512 if rank == world - 1 else 0)),
     }
     kern = {}
     for name, (cnt, ms) in prof.items():
@@ -327,6 +376,7 @@ def run_ours(args):
             "kernels": kern,
             "encode_us_per_layer": round(enc_ms_layer * 1000.0, 2),
             "encode_gbs": round(batch * N_KV * n_loc * 400 / (enc_ms_layer * 1e-3) / 1e9, 1),
+            "dense_sdpa_us_per_layer": dense_us,
             "e2e": {"value": round(e2e_ms * 1000.0 / L, 3), "unit": UNIT, "h2d_bytes_per_step": L * batch * N_Q * D * 2,
                     "d2h_bytes_per_step": L * batch * N_Q * D * 2, "cuda_graph": use_graph,
                     "eager_value": round(e2e_eager_ms * 1000.0 / L, 3)},
@@ -439,7 +489,9 @@ def main():
     ap.add_argument("--config", default="128k", choices=sorted(CONFIGS))
     ap.add_argument("--layers", type=int, default=N_LAYERS)
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--two-calls", action="store_true", help="retrieve_topk + sparse_attend instead of the fused call")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     args = ap.parse_args()
     args.warmup = max(3, args.warmup) if args.impl == "ours" else args.warmup

@@ -155,6 +155,18 @@ pkv_status sparse_attend(pkv_index* index, const void* q, const void* K, const v
                          int64_t st, const int32_t* idx, int32_t k, const void* K_hot, const void* V_hot,
                          int32_t n_hot, float scale, void* out, float* lse, cudaStream_t stream);
 
+/* (3)+(4) retrieve_and_attend — one decode step of one layer: exactly retrieve_topk followed by sparse_attend
+ * with the same arguments (K/V rows strided as above, HBM or UVA), scheduled as one unit: the hot-row attention
+ * runs on a library-owned forked stream concurrently with the retrieval kernels (fork/join through events on
+ * the caller's stream, CUDA-graph capturable), and the final top-k selection is fused with the gather and
+ * attention of the selected rows and the merge with the hot-row partials. out_idx/out_est are identical to
+ * retrieve_topk's; out/lse equal sparse_attend's up to fp32 summation order. When sequence-sharded it simply
+ * calls the two entry points. */
+pkv_status retrieve_and_attend(pkv_index* index, const void* q, const pkv_retrieve_params* params, const void* K,
+                               const void* V, int64_t sb, int64_t sh, int64_t st, const void* K_hot,
+                               const void* V_hot, int32_t n_hot, float scale, int32_t* out_idx, float* out_est,
+                               void* out, float* lse, cudaStream_t stream);
+
 /* Diagnostics: copy metadata of positions [start, start+count) into caller device buffers in the
  * canonical layout: ids uint8 [batch][n_kv][count][16] (subspace order), codes uint8
  * [batch][n_kv][count][64] (coordinate c -> byte c>>1, low nibble for even c; nibble = sign<<3 | idx),

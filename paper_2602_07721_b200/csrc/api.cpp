@@ -93,7 +93,7 @@ pkv_status alloc_workspace(Workspace* ws, int batch, int n_q, int n_kv, int64_t 
   ws->n_kv = n_kv;
   ws->cap = cap;
   const size_t bq = (size_t)batch * n_q, bk = (size_t)batch * n_kv;
-  size_t sizes[14] = {
+  size_t sizes[17] = {
       bk * NC * NB * 4,                                  // lut
       bq * D * 16 * 4,                                   // rtab
       bq * 4,                                            // qnorm
@@ -107,7 +107,10 @@ pkv_status alloc_workspace(Workspace* ws, int batch, int n_q, int n_kv, int64_t 
       (size_t)MAX_RANKS * bq * MAX_TOPK * 4,             // topk_est
       (size_t)MAX_RANKS * bq * MAX_TOPK * 4,             // topk_idx
       (size_t)MAX_RANKS * bq * MAX_SPLITS * PART * 4,    // part
-      bk * 4};                                           // ticket
+      bk * 4,                                            // ticket
+      bq * MAX_SPLITS * PART * 4,                        // hot_part
+      (size_t)MAX_RANKS * bq * MAX_TOPK * 4,             // seg_est
+      (size_t)MAX_RANKS * bq * MAX_TOPK * 4};            // seg_idx
   size_t total = 0;
   for (size_t s : sizes) total += align_up(s);
   void* base = nullptr;
@@ -133,10 +136,17 @@ pkv_status alloc_workspace(Workspace* ws, int batch, int n_q, int n_kv, int64_t 
   ws->topk_idx = reinterpret_cast<int32_t*>(take(11));
   ws->part = reinterpret_cast<float*>(take(12));
   ws->ticket = reinterpret_cast<unsigned int*>(take(13));
+  ws->hot_part = reinterpret_cast<float*>(take(14));
+  ws->seg_est = reinterpret_cast<float*>(take(15));
+  ws->seg_idx = reinterpret_cast<int32_t*>(take(16));
   ws->base = base;
   ws->bytes = total;
   e = cudaMemset(base, 0, total);
   if (e != cudaSuccess) return cuda_status(e, "workspace memset");
+  e = cudaStreamCreateWithFlags(&ws->side, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ws->ev_fork, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ws->ev_join, cudaEventDisableTiming);
+  if (e != cudaSuccess) return cuda_status(e, "workspace stream/events");
   return PKV_OK;
 }
 
@@ -144,6 +154,9 @@ void release_workspace(Workspace* ws) {
   if (!ws) return;
   if (--ws->refs == 0) {
     if (ws->base) cudaFree(ws->base);
+    if (ws->ev_fork) cudaEventDestroy(ws->ev_fork);
+    if (ws->ev_join) cudaEventDestroy(ws->ev_join);
+    if (ws->side) cudaStreamDestroy(ws->side);
     delete ws;
   }
 }
@@ -404,6 +417,57 @@ pkv_status sparse_attend(pkv_index* ix, const void* q, const void* K, const void
   pkv_status s2 = comm_allgather_u32(ix, reinterpret_cast<uint32_t*>(ws->part), part_slot, stream);
   if (s2 != PKV_OK) return s2;
   PKV_CUDA(launch_attend_combine(ix, ws->part, splits, ix->world, out, lse, stream), "combine");
+  return PKV_OK;
+}
+
+pkv_status retrieve_and_attend(pkv_index* ix, const void* q, const pkv_retrieve_params* p, const void* K, const void* V,
+                               int64_t sb, int64_t sh, int64_t st, const void* K_hot, const void* V_hot, int32_t n_hot,
+                               float scale, int32_t* out_idx, float* out_est, void* out, float* lse,
+                               cudaStream_t stream) {
+  if (!ix) return set_error(PKV_ERR_INVALID_ARG, "retrieve_and_attend: null index");
+  if (ix->comm) {  // sequence-sharded: the exchanges sit between the phases; use the two calls
+    pkv_status st1 = retrieve_topk(ix, q, p, out_idx, out_est, stream);
+    if (st1 != PKV_OK) return st1;
+    return sparse_attend(ix, q, K, V, sb, sh, st, out_idx, p->top_k, K_hot, V_hot, n_hot, scale, out, lse, stream);
+  }
+  pkv_status st0 = check_retrieve(ix, q, p, ix->n, out_idx, out_est);
+  if (st0 != PKV_OK) return st0;
+  if (!out) return set_error(PKV_ERR_INVALID_ARG, "retrieve_and_attend: null out");
+  st0 = check_kv_layout(K, sb, sh, st, "retrieve_and_attend(K)");
+  if (st0 == PKV_OK) st0 = check_kv_layout(V, sb, sh, st, "retrieve_and_attend(V)");
+  if (st0 != PKV_OK) return st0;
+  if (n_hot < 0 || (n_hot > 0 && (!K_hot || !V_hot || !aligned16(K_hot) || !aligned16(V_hot))))
+    return set_error(PKV_ERR_INVALID_ARG, "retrieve_and_attend: bad hot rows");
+  DeviceGuard g(ix->device);
+  Workspace* ws = ix->ws;
+  int hsplits = 0;
+  if (n_hot > 0) {  // fork: hot-row attention does not depend on the retrieval
+    hsplits = plan_attend_splits(ix, n_hot);
+    PKV_CUDA(cudaEventRecord(ws->ev_fork, stream), "fork");
+    PKV_CUDA(cudaStreamWaitEvent(ws->side, ws->ev_fork, 0), "fork wait");
+    AttendArgs a{q, nullptr, nullptr, 0, 0, 0, nullptr, 0, K_hot, V_hot, n_hot, scale, 0, INT64_MAX, 0};
+    PKV_CUDA(launch_attend_partial(ix, a, hsplits, ws->hot_part, nullptr, nullptr, nullptr, ws->side), "hot attend");
+    PKV_CUDA(cudaEventRecord(ws->ev_join, ws->side), "join");
+  }
+  ScanPlan plan;
+  st0 = phase_scan(ix, q, p, plan, stream);
+  if (st0 != PKV_OK) return st0;
+  st0 = phase_select_rerank(ix, p, plan, nullptr, 1, 0, stream);
+  if (st0 != PKV_OK) return st0;
+  if (n_hot > 0) PKV_CUDA(cudaStreamWaitEvent(stream, ws->ev_join, 0), "join wait");
+  if (topk_segments(std::min<int64_t>(p->n_cand, ix->n)) > 1) {
+    // long candidate lists (1M-token contexts): segmented top-k + merge, then attention over the retrieved rows
+    // merged with the hot partials already computed on the side stream
+    PKV_CUDA(launch_topk(ix, p->n_cand, p->top_k, out_idx, out_est, p->top_k, stream), "topk");
+    PKV_CUDA(launch_topk_attend_rows(ix, p->top_k, out_idx, q, K, V, sb, sh, st, scale, ws->hot_part, hsplits, out,
+                                     lse, stream),
+             "attend rows");
+  } else {
+    PKV_CUDA(launch_topk_attend(ix, p->top_k, out_idx, out_est, q, K, V, sb, sh, st, scale, ws->hot_part, hsplits,
+                                out, lse, stream),
+             "topk+attend");
+  }
+  if (p->dbg_cand || p->dbg_est) PKV_CUDA(launch_dbg_cand(ix, p->n_cand, p->dbg_cand, p->dbg_est, stream), "dbg cand");
   return PKV_OK;
 }
 

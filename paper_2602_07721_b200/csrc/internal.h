@@ -52,6 +52,11 @@ struct Workspace {
   int32_t* topk_idx = nullptr;    // [MAX_RANKS][batch][n_q][MAX_TOPK]
   float* part = nullptr;          // [MAX_RANKS][batch][n_q][MAX_SPLITS][PART] (exchange A)
   unsigned int* ticket = nullptr; // [batch][n_kv] split-completion counters of the fused attention merge
+  float* hot_part = nullptr;      // [batch][n_q][MAX_SPLITS][PART] hot-row partials of retrieve_and_attend
+  float* seg_est = nullptr;       // [MAX_RANKS][batch][n_q][MAX_TOPK] segmented top-k of long candidate lists
+  int32_t* seg_idx = nullptr;
+  cudaStream_t side = nullptr;    // forked stream for the hot-row attention
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   void* base = nullptr;
   size_t bytes = 0;
   int refs = 1;
@@ -125,10 +130,22 @@ cudaError_t launch_head_hist(const pkv_index* ix, const ScanPlan& plan, uint32_t
 // Fused threshold + compaction. all_hist: [P][batch][n_q][HB] gathered cumulative per-rank totals (P > 1).
 cudaError_t launch_select(const pkv_index* ix, int64_t n, const ScanPlan& plan, const uint32_t* all_hist, int P,
                           int rank, int64_t C, int64_t id_offset, cudaStream_t stream);
-cudaError_t launch_dbg_scores(const pkv_index* ix, int64_t n, uint8_t* out, cudaStream_t stream);
 cudaError_t launch_rerank(const pkv_index* ix, int64_t C_cap, int64_t id_offset, cudaStream_t stream);
+cudaError_t launch_dbg_scores(const pkv_index* ix, int64_t n, uint8_t* out, cudaStream_t stream);
 cudaError_t launch_topk(const pkv_index* ix, int64_t C_cap, int k, int32_t* out_idx, float* out_est,
                         int out_stride, cudaStream_t stream);
+// Final top-k fused with the gather + attention of the selected rows and the merge with hot-row partials
+// (hot_part: [batch][n_q][MAX_SPLITS][PART], hsplits entries per head).
+cudaError_t launch_topk_attend(const pkv_index* ix, int k, int32_t* out_idx, float* out_est, const void* q,
+                               const void* K, const void* V, int64_t sb, int64_t sh, int64_t st, float scale,
+                               const float* hot_part, int hsplits, void* out, float* lse, cudaStream_t stream);
+int topk_segments(int64_t C_cap);
+// Attention over the given top-k rows (no selection) merged with hot partials.
+cudaError_t launch_topk_attend_rows(const pkv_index* ix, int k, const int32_t* idx, const void* q, const void* K,
+                                    const void* V, int64_t sb, int64_t sh, int64_t st, float scale,
+                                    const float* hot_part, int hsplits, void* out, float* lse, cudaStream_t stream);  // > 1: long lists take the segmented top-k + merge (no fused attend)
+cudaError_t launch_topk_merge_strided(const pkv_index* ix, int P, int k, const float* all_est, const int32_t* all_idx,
+                                      int32_t* out_idx, float* out_est, int out_stride, cudaStream_t stream);
 cudaError_t launch_topk_merge(const pkv_index* ix, int P, int k, const float* all_est, const int32_t* all_idx,
                               int32_t* out_idx, float* out_est, cudaStream_t stream);
 cudaError_t launch_dbg_cand(const pkv_index* ix, int64_t C, int32_t* dbg_cand, float* dbg_est,

@@ -19,8 +19,6 @@ struct KV {
   uint32_t id;
 };
 
-__device__ __forceinline__ bool kv_less(const KV& a, const KV& b) { return a.k < b.k || (a.k == b.k && a.id < b.id); }
-
 __device__ __forceinline__ KV shfl_kv(const KV& v, int m) {
   KV o;
   o.k = __shfl_xor_sync(0xffffffffu, v.k, m);
@@ -29,11 +27,13 @@ __device__ __forceinline__ KV shfl_kv(const KV& v, int m) {
 }
 
 // One stage (k, j) for the element at position p held by this thread, partner value `o` at position p ^ j.
+// Branch-free: (key, id) pairs are distinct, so "mine < o" == !(o < mine).
 __device__ __forceinline__ void ce(KV& mine, const KV& o, int p, int k, int j) {
-  const bool lower = (p & j) == 0;
-  const bool asc = (p & k) == 0;
-  const bool take_other = (asc == lower) ? kv_less(o, mine) : kv_less(mine, o);
-  if (take_other) mine = o;
+  const bool keep_min = (((p & j) == 0) == ((p & k) == 0));
+  const bool o_less = (o.k < mine.k) | ((o.k == mine.k) & (o.id < mine.id));
+  const bool take = keep_min == o_less;
+  mine.k = take ? o.k : mine.k;
+  mine.id = take ? o.id : mine.id;
 }
 
 __global__ void __launch_bounds__(QP_THREADS) qprep_kernel(const uint16_t* __restrict__ q, int T, DevCfg cfg,

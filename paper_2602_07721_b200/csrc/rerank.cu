@@ -1,10 +1,9 @@
 // Stage II on the GPU: RSQ-IP rerank (a5) and final top-k (a6) — PAPER §4.1.3 Eq. 8-10, §4.2.2 (2),
 // P:409-425, P:482-486, P:526 ("fused reranking kernel (gather+unpack+score)").
 //
-// rerank_kernel  one thread per candidate: gathers the key's 128-byte record (64 B of 4-bit codes + 16 fp32
-//                w' = w/||sign*L[idx]||), decodes each nibble through a per-query table
-//                T[j][nibble] = sign*L[idx]*q~_j held in shared memory (all lanes read the same 16-word row j,
-//                which spans 16 distinct banks: conflict-free), est = ||q|| sum_b w'_b sum_j T[8b+j][nib].
+// rerank_kernel  two threads per candidate gather its 128-byte record (64 B of 4-bit codes + 16 fp32
+//                w' = w/||sign*L[idx]||) and decode each nibble through a per-query table
+//                T[j][nibble] = sign*L[idx]*q~_j in shared memory: est = ||q|| sum_b w'_b sum_j T[8b+j][nib].
 // topk_kernel    per (sequence, query head): MSB-first radix select (8-bit digits) on the 64-bit composite key
 //                (order-preserving fp32 bits of est << 32 | id), so ties in est go to the larger id;
 //                the k winners are then bitonic-sorted descending. Also used to merge the ranks' local top-k
@@ -254,10 +253,9 @@ __device__ __forceinline__ unsigned long long ckey(float e, int id) {
   return ((unsigned long long)ord_f32(e) << 32) | (uint32_t)id;
 }
 
-__global__ void __launch_bounds__(BS_THREADS) topk_kernel(const float* __restrict__ est, const int32_t* __restrict__ cand,
-                                                           const int32_t* __restrict__ sel, int n_q,
-                                                           int64_t cand_stride, int k, int out_stride,
-                                                           int32_t* out_idx, float* out_est) {
+// Top-k of the `count` (estimate, id) pairs at es / ids, written in order to oi / oe (k entries, -1 padded).
+__device__ __forceinline__ void topk_select(const float* __restrict__ es, const int32_t* __restrict__ ids, int count,
+                                            int k, int32_t* oi, float* oe) {
   extern __shared__ float ecache[];  // [BS_CACHE] estimates, then [BS_CACHE] ids
   int32_t* icache = reinterpret_cast<int32_t*>(ecache + BS_CACHE);
   __shared__ unsigned int hist[BS_BINS];
@@ -266,15 +264,6 @@ __global__ void __launch_bounds__(BS_THREADS) topk_kernel(const float* __restric
   __shared__ float red_mn[BS_THREADS / 32], red_mx[BS_THREADS / 32];
   __shared__ unsigned int wsum[BS_THREADS / 32];
   __shared__ int s_bstar, s_need, s_wc, s_bc;
-  pdl_trigger();
-  pdl_wait();
-  const int h = blockIdx.x, b = blockIdx.y;
-  const int64_t bhq = (int64_t)b * n_q + h;
-  const int count = sel[bhq * SEL_STRIDE + 2];
-  const float* es = est + bhq * cand_stride;
-  const int32_t* ids = cand + bhq * cand_stride;
-  int32_t* oi = out_idx + bhq * out_stride;
-  float* oe = out_est + bhq * out_stride;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = BS_THREADS / 32;
   const int kv = min(k, count);
@@ -403,13 +392,155 @@ __global__ void __launch_bounds__(BS_THREADS) topk_kernel(const float* __restric
   }
 }
 
+
+struct AttendEpi {  // gather + attention over the selected rows, merged with precomputed hot-row partials
+  const void* q;
+  const void* K;
+  const void* V;
+  int64_t sb, sh, st;
+  float scale;
+  const float* hot_part;  // [batch][n_q][MAX_SPLITS][PART], hsplits valid entries per head (may be 0)
+  int hsplits;
+  void* out;
+  float* lse;
+  int G;
+};
+
+// Grid (n_q, batch, nseg). nseg == 1: the whole candidate list of a head, output at out_idx + bhq*out_stride.
+// nseg > 1 (very long lists, e.g. 1M-token contexts): CTA z takes candidates [z*BS_CACHE, (z+1)*BS_CACHE) and
+// writes its local top-k to slot z of out (slot stride seg_stride), to be merged by merge_kernel.
+template <bool ATTEND, bool SELECT = true>
+__global__ void __launch_bounds__(BS_THREADS) topk_kernel(const float* __restrict__ est, const int32_t* __restrict__ cand,
+                                                           const int32_t* __restrict__ sel, int n_q,
+                                                           int64_t cand_stride, int k, int out_stride,
+                                                           int32_t* out_idx, float* out_est, AttendEpi ep,
+                                                           int64_t seg_stride) {
+  pdl_trigger();
+  pdl_wait();
+  if (SELECT) {
+    const int h = blockIdx.x, b = blockIdx.y, z = blockIdx.z;
+    const int64_t bhq = (int64_t)b * n_q + h;
+    const int total = sel[bhq * SEL_STRIDE + 2];
+    const int begin = gridDim.z > 1 ? z * BS_CACHE : 0;
+    const int count = gridDim.z > 1 ? max(0, min(BS_CACHE, total - begin)) : total;
+    topk_select(est + bhq * cand_stride + begin, cand + bhq * cand_stride + begin, count, k,
+                out_idx + z * seg_stride + bhq * out_stride, out_est + z * seg_stride + bhq * out_stride);
+  }
+  if constexpr (ATTEND) {
+    __syncthreads();  // out_idx of this head written by this CTA
+    extern __shared__ float ecache[];
+    float* sm_o = ecache;                       // [16][128]
+    float* sm_ml = ecache + 16 * D;             // [16][2]
+    const int h = blockIdx.x, b = blockIdx.y;
+    const int g = h / ep.G;
+    const int n_kv = n_q / ep.G;
+    const int64_t bhq = (int64_t)b * n_q + h;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int NW = BS_THREADS / 32;
+    const float qscale = ep.scale * 1.4426950408889634f;
+    const uint2 qraw = ldg_v2(static_cast<const uint16_t*>(ep.q) + bhq * D + 4 * lane);
+    const float q0 = bf16_lo(qraw.x) * qscale, q1 = bf16_hi(qraw.x) * qscale;
+    const float q2 = bf16_lo(qraw.y) * qscale, q3 = bf16_hi(qraw.y) * qscale;
+    const int32_t* oi = out_idx + bhq * out_stride;  // (ATTEND is only launched with nseg == 1)
+    const uint16_t* Kb = static_cast<const uint16_t*>(ep.K) + (int64_t)b * ep.sb + (int64_t)g * ep.sh + 4 * lane;
+    const uint16_t* Vb = static_cast<const uint16_t*>(ep.V) + (int64_t)b * ep.sb + (int64_t)g * ep.sh + 4 * lane;
+    float m = -INFINITY, l = 0.f, o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f;
+    constexpr int RB = 8;
+    for (int r0 = warp; r0 < k; r0 += NW * RB) {
+      int id[RB];
+#pragma unroll
+      for (int u = 0; u < RB; ++u) id[u] = (r0 + u * NW < k) ? oi[r0 + u * NW] : -1;
+      uint2 kr[RB], vr[RB];
+#pragma unroll
+      for (int u = 0; u < RB; ++u) {
+        kr[u] = make_uint2(0, 0);
+        vr[u] = make_uint2(0, 0);
+        if (id[u] >= 0) {
+          kr[u] = ldg_v2(Kb + (int64_t)id[u] * ep.st);
+          vr[u] = ldg_v2(Vb + (int64_t)id[u] * ep.st);
+        }
+      }
+      float x[RB];
+#pragma unroll
+      for (int u = 0; u < RB; ++u)
+        x[u] = bf16_lo(kr[u].x) * q0 + bf16_hi(kr[u].x) * q1 + bf16_lo(kr[u].y) * q2 + bf16_hi(kr[u].y) * q3;
+#pragma unroll
+      for (int xm = 16; xm > 0; xm >>= 1) {
+#pragma unroll
+        for (int u = 0; u < RB; ++u) x[u] += __shfl_xor_sync(0xffffffffu, x[u], xm);
+      }
+      float mx = m;
+#pragma unroll
+      for (int u = 0; u < RB; ++u)
+        if (id[u] >= 0) mx = fmaxf(mx, x[u]);
+      if (mx == -INFINITY) continue;
+      const float c = exp2f(m - mx);
+      l *= c;
+      o0 *= c;
+      o1 *= c;
+      o2 *= c;
+      o3 *= c;
+#pragma unroll
+      for (int u = 0; u < RB; ++u) {
+        if (id[u] >= 0) {
+          const float pu = exp2f(x[u] - mx);
+          l += pu;
+          o0 = fmaf(pu, bf16_lo(vr[u].x), o0);
+          o1 = fmaf(pu, bf16_hi(vr[u].x), o1);
+          o2 = fmaf(pu, bf16_lo(vr[u].y), o2);
+          o3 = fmaf(pu, bf16_hi(vr[u].y), o3);
+        }
+      }
+      m = mx;
+    }
+    sm_o[warp * D + 4 * lane] = o0;
+    sm_o[warp * D + 4 * lane + 1] = o1;
+    sm_o[warp * D + 4 * lane + 2] = o2;
+    sm_o[warp * D + 4 * lane + 3] = o3;
+    if (lane == 0) {
+      sm_ml[2 * warp] = m;
+      sm_ml[2 * warp + 1] = l;
+    }
+    __syncthreads();
+    if (threadIdx.x < D) {
+      const int d = threadIdx.x;
+      const float* hp = ep.hot_part + bhq * MAX_SPLITS * PART;
+      float M = -INFINITY;
+      for (int w = 0; w < NW; ++w) M = fmaxf(M, sm_ml[2 * w]);
+      for (int s2 = 0; s2 < ep.hsplits; ++s2) M = fmaxf(M, __ldcg(hp + (int64_t)s2 * PART));
+      float L = 0.f, O = 0.f;
+      if (M != -INFINITY) {
+        for (int w = 0; w < NW; ++w) {
+          const float mw = sm_ml[2 * w];
+          if (mw == -INFINITY) continue;
+          const float cw = exp2f(mw - M);
+          L += cw * sm_ml[2 * w + 1];
+          O += cw * sm_o[w * D + d];
+        }
+        for (int s2 = 0; s2 < ep.hsplits; ++s2) {
+          const float* pp = hp + (int64_t)s2 * PART;
+          const float ms = __ldcg(pp);
+          if (ms == -INFINITY) continue;
+          const float cs = exp2f(ms - M);
+          L += cs * __ldcg(pp + 1);
+          O += cs * __ldcg(pp + 2 + d);
+        }
+      }
+      static_cast<__nv_bfloat16*>(ep.out)[bhq * D + d] = __float2bfloat16_rn(L > 0.f ? O / L : 0.f);
+      if (ep.lse && d == 0) ep.lse[bhq] = L > 0.f ? (M + log2f(L)) * 0.6931471805599453f : -INFINITY;
+    }
+    (void)n_kv;
+  }
+}
+
 __global__ void __launch_bounds__(TK_THREADS) merge_kernel(const float* __restrict__ all_est,
                                                             const int32_t* __restrict__ all_idx, int P, int batch,
-                                                            int n_q, int k, int32_t* out_idx, float* out_est) {
+                                                            int n_q, int k, int32_t* out_idx, float* out_est,
+                                                            int out_stride) {
   const int h = blockIdx.x, b = blockIdx.y;
   const int64_t bhq = (int64_t)b * n_q + h;
   MergeSrc src{all_est + bhq * MAX_TOPK, all_idx + bhq * MAX_TOPK, k, (int64_t)batch * n_q * MAX_TOPK};
-  radix_topk(src, P * k, k, out_idx + bhq * k, out_est + bhq * k);
+  radix_topk(src, P * k, k, out_idx + bhq * out_stride, out_est + bhq * out_stride);
 }
 
 __global__ void dbg_cand_kernel(const int32_t* __restrict__ cand, const float* __restrict__ est,
@@ -426,8 +557,16 @@ __global__ void dbg_cand_kernel(const int32_t* __restrict__ cand, const float* _
 
 }  // namespace
 
+int topk_segments(int64_t C_cap) {
+  return C_cap > BS_CACHE ? (int)((C_cap + BS_CACHE - 1) / BS_CACHE) : 1;
+}
+
 cudaError_t init_rerank_attrs() {
-  cudaError_t e = cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TK_SMEM);
+  cudaError_t e = cudaFuncSetAttribute(topk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TK_SMEM);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(topk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TK_SMEM);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(topk_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TK_SMEM);
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TK_SMEM);
 }
@@ -450,9 +589,32 @@ cudaError_t launch_topk(const pkv_index* ix, int64_t C_cap, int k, int32_t* out_
   const Workspace* ws = ix->ws;
   dim3 grid(ix->cfg.n_q_heads, ix->batch);
   ProfScope p_(K_TOPK, stream);
-  return pdl_launch(topk_kernel, grid, dim3(BS_THREADS), TK_SMEM, stream, (const float*)ws->est,
+  AttendEpi ep{};
+  const int nseg = topk_segments(C_cap);
+  if (nseg > 1) {  // long candidate lists: per-segment top-k into the exchange slots, then the merge kernel
+    const size_t slot = (size_t)ix->batch * ix->cfg.n_q_heads * MAX_TOPK;
+    dim3 g3(ix->cfg.n_q_heads, ix->batch, nseg);
+    cudaError_t e = pdl_launch(topk_kernel<false>, g3, dim3(BS_THREADS), TK_SMEM, stream, (const float*)ws->est,
+                               (const int32_t*)ws->cand, (const int32_t*)ws->sel, ix->cfg.n_q_heads, ws->cap, k,
+                               MAX_TOPK, ws->seg_idx, ws->seg_est, ep, (int64_t)slot);
+    if (e != cudaSuccess) return e;
+    return launch_topk_merge_strided(ix, nseg, k, ws->seg_est, ws->seg_idx, out_idx, out_est, out_stride, stream);
+  }
+  return pdl_launch(topk_kernel<false>, grid, dim3(BS_THREADS), TK_SMEM, stream, (const float*)ws->est,
                     (const int32_t*)ws->cand, (const int32_t*)ws->sel, ix->cfg.n_q_heads, ws->cap, k, out_stride,
-                    out_idx, out_est);
+                    out_idx, out_est, ep, (int64_t)0);
+}
+
+cudaError_t launch_topk_attend(const pkv_index* ix, int k, int32_t* out_idx, float* out_est, const void* q,
+                               const void* K, const void* V, int64_t sb, int64_t sh, int64_t st, float scale,
+                               const float* hot_part, int hsplits, void* out, float* lse, cudaStream_t stream) {
+  const Workspace* ws = ix->ws;
+  dim3 grid(ix->cfg.n_q_heads, ix->batch);
+  ProfScope p_(K_TOPK, stream);
+  AttendEpi ep{q, K, V, sb, sh, st, scale, hot_part, hsplits, out, lse, ix->dcfg.G};
+  return pdl_launch(topk_kernel<true>, grid, dim3(BS_THREADS), TK_SMEM, stream, (const float*)ws->est,
+                    (const int32_t*)ws->cand, (const int32_t*)ws->sel, ix->cfg.n_q_heads, ws->cap, k, k, out_idx,
+                    out_est, ep, (int64_t)0);
 }
 
 cudaError_t launch_topk_merge(const pkv_index* ix, int P, int k, const float* all_est, const int32_t* all_idx,
@@ -460,7 +622,28 @@ cudaError_t launch_topk_merge(const pkv_index* ix, int P, int k, const float* al
   dim3 grid(ix->cfg.n_q_heads, ix->batch);
   ProfScope p_(K_MERGE, stream);
   merge_kernel<<<grid, TK_THREADS, TK_SMEM, stream>>>(all_est, all_idx, P, ix->batch, ix->cfg.n_q_heads, k, out_idx,
-                                                out_est);
+                                                out_est, k);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_topk_attend_rows(const pkv_index* ix, int k, const int32_t* idx, const void* q, const void* K,
+                                    const void* V, int64_t sb, int64_t sh, int64_t st, float scale,
+                                    const float* hot_part, int hsplits, void* out, float* lse, cudaStream_t stream) {
+  const Workspace* ws = ix->ws;
+  dim3 grid(ix->cfg.n_q_heads, ix->batch);
+  ProfScope p_(K_ATTEND, stream);
+  AttendEpi ep{q, K, V, sb, sh, st, scale, hot_part, hsplits, out, lse, ix->dcfg.G};
+  return pdl_launch(topk_kernel<true, false>, grid, dim3(BS_THREADS), TK_SMEM, stream, (const float*)ws->est,
+                    (const int32_t*)ws->cand, (const int32_t*)ws->sel, ix->cfg.n_q_heads, ws->cap, k, k,
+                    const_cast<int32_t*>(idx), (float*)nullptr, ep, (int64_t)0);
+}
+
+cudaError_t launch_topk_merge_strided(const pkv_index* ix, int P, int k, const float* all_est, const int32_t* all_idx,
+                                      int32_t* out_idx, float* out_est, int out_stride, cudaStream_t stream) {
+  dim3 grid(ix->cfg.n_q_heads, ix->batch);
+  ProfScope p_(K_MERGE, stream);
+  merge_kernel<<<grid, TK_THREADS, TK_SMEM, stream>>>(all_est, all_idx, P, ix->batch, ix->cfg.n_q_heads, k, out_idx,
+                                                out_est, out_stride);
   return cudaGetLastError();
 }
 

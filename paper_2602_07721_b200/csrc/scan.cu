@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1)
 // sel layout per (b, q head): [0] s*, [1] gt_local, [2] C_local, [3] take_local (written by chunk 0's CTA)
 constexpr int SEL_STRIDE = 4 + 4 * MAX_CHUNKS;
 constexpr int SEL_THREADS = 1024;
-constexpr int SEL_SMEM = 32 * 8 * 32 * 8;  // 32 warps x 256 entries x uint2
+constexpr int SEL_SMEM = 32 * 8 * 32 * 8;  // per-warp compaction lists
 
 // Fused threshold + compaction (bucket_topk). Chunk histograms are CUMULATIVE:
 // cum_j[h][s] = #(score >= s) in chunk j. Every CTA of a (sequence, KV head) recomputes, for its query heads,
@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(
   __shared__ uint32_t Hg[GMAX][HB];   // global cumulative counts
   __shared__ uint32_t Hl[GMAX][HB];   // this rank's cumulative counts
   __shared__ int s_star[GMAX], gt_local[GMAX], take_local[GMAX];
-  __shared__ int p_gt_off[GMAX], p_tie_off[GMAX], p_take[GMAX], p_eq[GMAX];
+  __shared__ int p_gt_off[GMAX], p_tie_off[GMAX], p_take[GMAX], p_eq[GMAX], p_gt_cnt[GMAX];
   __shared__ uint32_t wcnt[32][2 * GMAX];
   extern __shared__ uint2 sel_list[];  // per-warp compaction lists (VB * 32 entries each), SEL_SMEM bytes
   pdl_trigger();
@@ -293,6 +293,7 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(
       p_tie_off[hh] = gt_local[hh] + taken_after;
       p_take[hh] = rem < my_eq ? rem : my_eq;
       p_eq[hh] = my_eq;
+      p_gt_cnt[hh] = my_gt;
       if (j == 0) {
         int32_t* o = sel + ((int64_t)b * n_q + g * G + hh) * SEL_STRIDE;
         o[0] = st;
@@ -300,7 +301,6 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(
         o[2] = gt_local[hh] + tl;
         o[3] = tl;
       }
-      (void)my_gt;
     }
   }
   __syncthreads();

@@ -52,6 +52,8 @@ _sigs = {
     "append_decode_keys": [_vp, _vp, _i64, _i64, _i64, _i64, _vp],
     "retrieve_topk": [_vp, _vp, ctypes.POINTER(RetrieveParams), _vp, _vp, _vp],
     "sparse_attend": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _i32, _vp, _vp, _i32, _f32, _vp, _vp, _vp],
+    "retrieve_and_attend": [_vp, _vp, ctypes.POINTER(RetrieveParams), _vp, _vp, _i64, _i64, _i64, _vp, _vp, _i32, _f32,
+                            _vp, _vp, _vp, _vp, _vp],
     "pkv_index_export": [_vp, _i64, _i64, _vp, _vp, _vp, _vp],
     "pkv_nccl_unique_id": [_vp],
     "pkv_comm_init": [_vp, _vp, _i32, _i32, _i64],
@@ -250,6 +252,41 @@ def sparse_attend(index: Index, q: torch.Tensor, K: torch.Tensor | None, V: torc
     _check(_lib.sparse_attend(index.handle, _ptr(q), _vp(K_ptr), _vp(V_ptr), sb, sh, st, _ptr(idx), k,
                               _ptr(K_hot), _ptr(V_hot), n_hot, scale, _ptr(out), _ptr(lse), _stream(stream)))
     return out, lse
+
+
+def retrieve_and_attend(index: Index, q: torch.Tensor, K, V, top_k: int, K_hot=None, V_hot=None,
+                        scale: float | None = None, probes_T: int | None = None, n_cand: int | None = None,
+                        out_idx=None, out_est=None, out=None, lse=None, strides=None, K_ptr=None, V_ptr=None,
+                        stream=None):
+    """(3)+(4) in one call: retrieval and attention of one decode step and layer, with the hot-row attention
+    overlapped with the retrieval and the final top-k fused with the gather/attention. Returns
+    (idx, est, out, lse)."""
+    assert q.dtype == torch.bfloat16 and q.is_contiguous() and q.shape[-1] == D
+    n = len(index)
+    T0, C0 = schedule(n, top_k)
+    T = T0 if probes_T is None else probes_T
+    C = C0 if n_cand is None else n_cand
+    dev = q.device
+    if out_idx is None:
+        out_idx = torch.empty(index.batch, index.n_q, top_k, dtype=torch.int32, device=dev)
+    if out_est is None:
+        out_est = torch.empty(index.batch, index.n_q, top_k, dtype=torch.float32, device=dev)
+    if out is None:
+        out = torch.empty(index.batch, index.n_q, D, dtype=torch.bfloat16, device=dev)
+    if lse is None:
+        lse = torch.empty(index.batch, index.n_q, dtype=torch.float32, device=dev)
+    if K_ptr is None:
+        sb, sh, st = _kv_strides(K)
+        K_ptr, V_ptr = K.data_ptr(), V.data_ptr()
+    else:
+        sb, sh, st = strides
+    n_hot = 0 if K_hot is None else K_hot.shape[2]
+    scale = 1.0 / np.sqrt(D) if scale is None else scale
+    p = RetrieveParams(T, C, top_k, None, None, None, None)
+    _check(_lib.retrieve_and_attend(index.handle, _ptr(q), ctypes.byref(p), _vp(K_ptr), _vp(V_ptr), sb, sh, st,
+                                    _ptr(K_hot), _ptr(V_hot), n_hot, scale, _ptr(out_idx), _ptr(out_est), _ptr(out),
+                                    _ptr(lse), _stream(stream)))
+    return out_idx, out_est, out, lse
 
 
 def nccl_unique_id() -> bytes:

@@ -297,3 +297,49 @@ def test_full_size_128k_sampled_head(pkv):
         o, l = pipeline.attend(qf, Kf, bf16_f64(V[0, g]), idx[0, h].cpu().numpy())
         og = out[0, h].float().cpu().numpy()
         assert np.all(np.abs(og - o) <= ATT_ABS + 2.0 ** -8 * np.abs(o))
+
+
+@pytest.mark.parametrize("n,n_hot,k", [(4096, 272, 100), (777, 0, 64), (50, 16, 64), (20000, 300, 100)])
+def test_retrieve_and_attend_matches_two_calls(pkv, n, n_hot, k):
+    """The fused schedule (hot attention on a forked stream, top-k fused with gather+attention) returns the
+    same ids/estimates as retrieve_topk and attention within the AMB-17 bar of the oracle."""
+    K, q, V = make_problem(16 + n, 1, 8, 2, n, plant=n >= 200)
+    cfg = pkv.config_init(8, 2, SB)
+    ix = pkv.Index(cfg, 1, n)
+    pkv.encode_keys(ix, K)
+    Kh = Vh = None
+    if n_hot:
+        Kh = synth.isotropic(95, (1, 2, n_hot, 128), device="cuda")
+        Vh = synth.isotropic(96, (1, 2, n_hot, 128), device="cuda")
+    i0, e0, _ = pkv.retrieve_topk(ix, q, k)
+    o0, l0 = pkv.sparse_attend(ix, q, K, V, i0, Kh, Vh)
+    i1, e1, o1, l1 = pkv.retrieve_and_attend(ix, q, K, V, k, Kh, Vh)
+    torch.cuda.synchronize()
+    assert torch.equal(i0, i1) and torch.equal(e0, e1)
+    assert torch.allclose(l0, l1, atol=1e-4, rtol=1e-5)
+    for h in range(8):
+        qf = bf16_f64(q[0, h])
+        o, lse = pipeline.attend(qf, bf16_f64(K[0, h // 4]), bf16_f64(V[0, h // 4]), i1[0, h].cpu().numpy(),
+                                 None if Kh is None else bf16_f64(Kh[0, h // 4]),
+                                 None if Vh is None else bf16_f64(Vh[0, h // 4]))
+        og = o1[0, h].float().cpu().numpy()
+        assert np.all(np.abs(og - o) <= ATT_ABS + 2.0 ** -8 * np.abs(o))
+        assert abs(float(l1[0, h]) - lse) <= 1e-3 * max(1.0, abs(lse))
+
+
+def test_segmented_topk_long_candidate_list(pkv):
+    """C > 16384 (the 1M-token regime): per-segment top-k + merge must equal the oracle top-k up to ties, and
+    retrieve_and_attend must take the same ids."""
+    n, C = 60000, 40000
+    K, q, V = make_problem(17, 1, 4, 1, n)
+    run_and_check(pkv, K, q, V, k=100, C=C, check_all_heads=False)
+    cfg = pkv.config_init(4, 1, SB)
+    ix = pkv.Index(cfg, 1, n)
+    pkv.encode_keys(ix, K)
+    i0, e0, _ = pkv.retrieve_topk(ix, q, 100, n_cand=C)
+    Kh = synth.isotropic(97, (1, 1, 40, 128), device="cuda")
+    Vh = synth.isotropic(98, (1, 1, 40, 128), device="cuda")
+    o0, l0 = pkv.sparse_attend(ix, q, K, V, i0, Kh, Vh)
+    i1, e1, o1, l1 = pkv.retrieve_and_attend(ix, q, K, V, 100, Kh, Vh, n_cand=C)
+    assert torch.equal(i0, i1) and torch.equal(e0, e1)
+    assert torch.allclose(o0.float(), o1.float(), atol=4e-3) and torch.allclose(l0, l1, atol=1e-4)
