@@ -20,13 +20,18 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", f"-I{os.pa
          "-Xptxas", "-v", "--expt-relaxed-constexpr"]
 
 
+# PKV_PHASE_PROFILE=1: compile the globaltimer phase marks in (scripts/phase_profile.py); never for benchmarks
+DEFS = ["-DPKV_PHASE_PROFILE"] if os.environ.get("PKV_PHASE_PROFILE") == "1" else []
+STAMP = os.path.join(BUILD, "defs.txt")
+
+
 def sources():
     return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cu", ".cpp")))
 
 
 def _compile(src: str) -> tuple[str, str]:
     obj = os.path.join(BUILD, os.path.basename(src) + ".o")
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+    cmd = [NVCC, *ARCH, *FLAGS, *DEFS, "-c", src, "-o", obj]
     if src.endswith(".cpp"):
         cmd = [NVCC, *ARCH, "-O3", "-std=c++17", "-Xcompiler", "-fPIC,-O3", f"-I{os.path.join(ROOT, 'include')}",
                "-x", "cu", "-c", src, "-o", obj]
@@ -38,6 +43,12 @@ def _compile(src: str) -> tuple[str, str]:
 
 def up_to_date() -> bool:
     if not os.path.exists(OUT):
+        return False
+    try:
+        with open(STAMP) as f:
+            if f.read() != " ".join(DEFS):
+                return False
+    except OSError:
         return False
     t = os.path.getmtime(OUT)
     deps = sources() + [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(ROOT, "include", "pariskv.h"),
@@ -62,6 +73,8 @@ def build(verbose: bool = False, force: bool = False) -> str:
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
     os.replace(tmp, OUT)
+    with open(STAMP, "w") as f:
+        f.write(" ".join(DEFS))
     return OUT
 
 

@@ -172,10 +172,11 @@ pkv_status check_kv_layout(const void* K, int64_t sb, int64_t sh, int64_t st, co
 }
 
 // -------------------------------------------------------------- retrieval phases (shared by all modes)
-pkv_status phase_scan(pkv_index* ix, const void* q, const pkv_retrieve_params* p, ScanPlan& plan,
-                      cudaStream_t s) {
+pkv_status phase_scan(pkv_index* ix, const void* q, const pkv_retrieve_params* p, ScanPlan& plan, cudaStream_t s,
+                      const HotArgs* ha = nullptr) {
   const int64_t n = ix->n;
-  PKV_CUDA(launch_qprep(ix, q, p->probes_T, p->dbg_q_rot, s), "qprep");
+  const HotArgs none{nullptr, nullptr, 0, 0.f, nullptr};
+  PKV_CUDA(launch_qprep(ix, q, p->probes_T, p->dbg_q_rot, ha ? *ha : none, s), "qprep");
   plan = plan_scan(ix, n > 0 ? n : 1);
   if (n > 0) {
     PKV_CUDA(launch_scan(ix, n, plan, s), "scan");
@@ -438,32 +439,24 @@ pkv_status retrieve_and_attend(pkv_index* ix, const void* q, const pkv_retrieve_
   if (st0 != PKV_OK) return st0;
   if (n_hot < 0 || (n_hot > 0 && (!K_hot || !V_hot || !aligned16(K_hot) || !aligned16(V_hot))))
     return set_error(PKV_ERR_INVALID_ARG, "retrieve_and_attend: bad hot rows");
+  if (n_hot > 16 * 64) return set_error(PKV_ERR_UNSUPPORTED, "retrieve_and_attend: n_hot must be <= 1024");
   DeviceGuard g(ix->device);
-  Workspace* ws = ix->ws;
-  int hsplits = 0;
-  if (n_hot > 0) {  // fork: hot-row attention does not depend on the retrieval
-    hsplits = plan_attend_splits(ix, n_hot);
-    PKV_CUDA(cudaEventRecord(ws->ev_fork, stream), "fork");
-    PKV_CUDA(cudaStreamWaitEvent(ws->side, ws->ev_fork, 0), "fork wait");
-    AttendArgs a{q, nullptr, nullptr, 0, 0, 0, nullptr, 0, K_hot, V_hot, n_hot, scale, 0, INT64_MAX, 0};
-    PKV_CUDA(launch_attend_partial(ix, a, hsplits, ws->hot_part, nullptr, nullptr, nullptr, ws->side), "hot attend");
-    PKV_CUDA(cudaEventRecord(ws->ev_join, ws->side), "join");
-  }
   ScanPlan plan;
-  st0 = phase_scan(ix, q, p, plan, stream);
+  // the hot-row attention rides in the query-prep kernel (16 partials per head, merged by the last kernel)
+  const HotArgs ha{K_hot, V_hot, n_hot, scale, n_hot > 0 ? ix->ws->hot_part : nullptr};
+  st0 = phase_scan(ix, q, p, plan, stream, &ha);
   if (st0 != PKV_OK) return st0;
   st0 = phase_select_rerank(ix, p, plan, nullptr, 1, 0, stream);
   if (st0 != PKV_OK) return st0;
-  if (n_hot > 0) PKV_CUDA(cudaStreamWaitEvent(stream, ws->ev_join, 0), "join wait");
+  const int hsplits = n_hot > 0 ? NB : 0;
   if (topk_segments(std::min<int64_t>(p->n_cand, ix->n)) > 1) {
-    // long candidate lists (1M-token contexts): segmented top-k + merge, then attention over the retrieved rows
-    // merged with the hot partials already computed on the side stream
+    // long candidate lists (1M-token contexts): segmented top-k + merge, then the attention kernel
     PKV_CUDA(launch_topk(ix, p->n_cand, p->top_k, out_idx, out_est, p->top_k, stream), "topk");
-    PKV_CUDA(launch_topk_attend_rows(ix, p->top_k, out_idx, q, K, V, sb, sh, st, scale, ws->hot_part, hsplits, out,
-                                     lse, stream),
+    PKV_CUDA(launch_topk_attend_rows(ix, p->top_k, out_idx, q, K, V, sb, sh, st, scale, ix->ws->hot_part, hsplits,
+                                     out, lse, stream),
              "attend rows");
-  } else {
-    PKV_CUDA(launch_topk_attend(ix, p->top_k, out_idx, out_est, q, K, V, sb, sh, st, scale, ws->hot_part, hsplits,
+  } else {  // top-k selection fused with the gather + attention of hot U selected rows, one CTA per head
+    PKV_CUDA(launch_topk_attend(ix, p->top_k, out_idx, out_est, q, K, V, sb, sh, st, scale, ix->ws->hot_part, hsplits,
                                 out, lse, stream),
              "topk+attend");
   }

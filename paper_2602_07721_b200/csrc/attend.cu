@@ -37,6 +37,7 @@ __global__ void __launch_bounds__(AT_WARPS * 32) attend_partial_kernel(AttendArg
                                                                        int items_per_split, float* __restrict__ part,
                                                                        unsigned int* __restrict__ ticket, void* out,
                                                                        float* lse) {
+  phase_mark(K_ATTEND, 0);
   __shared__ __align__(16) float sm_x[AT_WARPS][AT_BATCH * GMAX];
   __shared__ float sm_m[AT_WARPS][GMAX], sm_l[AT_WARPS][GMAX];
   __shared__ float sm_o[AT_WARPS][GMAX][D];
@@ -91,6 +92,7 @@ __global__ void __launch_bounds__(AT_WARPS * 32) attend_partial_kernel(AttendArg
     }
     if (!waited) {
       pdl_wait();  // top-k ids come from the retrieval kernels
+      phase_mark(K_ATTEND, 1);
       waited = true;
     }
     int id[AT_BATCH];
@@ -209,6 +211,7 @@ __global__ void __launch_bounds__(AT_WARPS * 32) attend_partial_kernel(AttendArg
     }
     p[2 + d] = O;
   }
+  phase_mark(K_ATTEND, 2);
   if (ticket == nullptr) return;  // sharded: the LSE merge runs after the all-gather
   // fused LSE merge: the last CTA of this (sequence, KV head) to finish combines all splits
   __threadfence();
@@ -311,5 +314,7 @@ cudaError_t launch_attend_combine(const pkv_index* ix, const float* parts, int n
   attend_combine_kernel<<<grid, D, 0, stream>>>(parts, nsplits, P, rank_stride, ix->cfg.n_q_heads, out, lse);
   return cudaGetLastError();
 }
+
+cudaError_t set_phase_attend(unsigned long long* p) { return set_phase_ptr_tu(p); }
 
 }  // namespace pkv

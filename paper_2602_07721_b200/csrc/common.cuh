@@ -69,6 +69,37 @@ __device__ __forceinline__ int sign_bit(const DevCfg& c, int d) { return (c.sign
 
 namespace pkv {
 
+// Optional phase timestamps (clock64 of CTA (0,0,0), thread 0) for kernel anatomy studies; enabled through
+// pkv_phase_profile(). Slot layout: g_phase[kind * 16 + phase].
+static __device__ unsigned long long* g_phase = nullptr;  // one copy per translation unit
+static inline cudaError_t set_phase_ptr_tu(unsigned long long* p) {
+  return cudaMemcpyToSymbol(g_phase, &p, sizeof(p));
+}
+#ifdef PKV_PHASE_PROFILE
+__device__ __forceinline__ void phase_mark(int kind, int ph) {
+  if (g_phase && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_phase[kind * 16 + ph] = t;
+  }
+}
+
+// Per-CTA end timestamps of one kernel kind (slots 256.. of the phase buffer) for imbalance studies.
+__device__ __forceinline__ void cta_mark(int kind, int which) {
+  if (g_phase && threadIdx.x == 0) {
+    const unsigned cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    if (cta < 2048) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      g_phase[256 + 4096 * which + 2 * cta + (kind == K_RERANK ? 1 : 0)] = t;
+    }
+  }
+}
+#else  // marks compile away in the product build (build with PKV_PHASE_PROFILE=1 for scripts/phase_profile.py)
+__device__ __forceinline__ void phase_mark(int, int) {}
+__device__ __forceinline__ void cta_mark(int, int) {}
+#endif
+
 // Programmatic dependent launch: a kernel launched with pdl_launch may start while the previous kernel on the
 // stream drains; it must call pdl_wait() before touching that kernel's outputs. Disable with PKV_NO_PDL=1.
 bool pdl_enabled();

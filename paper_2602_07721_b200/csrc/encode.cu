@@ -206,4 +206,6 @@ cudaError_t launch_export(const pkv_index* ix, int64_t start, int64_t count, uin
   return cudaGetLastError();
 }
 
+cudaError_t set_phase_encode(unsigned long long* p) { return set_phase_ptr_tu(p); }
+
 }  // namespace pkv

@@ -101,6 +101,12 @@ class ProfScope {  // bracket one kernel launch: counts it, and records events w
   cudaEvent_t a_ = nullptr;
 };
 
+cudaError_t set_phase_scan(unsigned long long* p);
+cudaError_t set_phase_rerank(unsigned long long* p);
+cudaError_t set_phase_qprep(unsigned long long* p);
+cudaError_t set_phase_attend(unsigned long long* p);
+cudaError_t set_phase_encode(unsigned long long* p);
+
 // Error plumbing (api.cpp)
 pkv_status set_error(pkv_status s, const std::string& msg);
 pkv_status cuda_status(cudaError_t e, const char* what);
@@ -114,7 +120,17 @@ cudaError_t launch_encode(const pkv_index* ix, const void* K, int64_t sb, int64_
                           int64_t count, cudaStream_t stream);
 cudaError_t launch_export(const pkv_index* ix, int64_t start, int64_t count, uint8_t* ids, uint8_t* codes,
                           float* w, cudaStream_t stream);
-cudaError_t launch_qprep(const pkv_index* ix, const void* q, int T, float* dbg_q_rot, cudaStream_t stream);
+// Optional hot-row attention done by qprep: CTA (subspace sb, head h) attends rows [sb*ceil(n/16), ...) of the
+// hot segment and writes its partial (m, l, o) to part[b][h][sb] (log2 domain). part == nullptr: skipped.
+struct HotArgs {
+  const void* K_hot;
+  const void* V_hot;
+  int n_hot;
+  float scale;
+  float* part;
+};
+cudaError_t launch_qprep(const pkv_index* ix, const void* q, int T, float* dbg_q_rot, const HotArgs& ha,
+                         cudaStream_t stream);
 
 struct ScanPlan {
   int nchunks;

@@ -107,3 +107,12 @@ bool pdl_enabled() {
   return on;
 }
 }  // namespace pkv
+
+extern "C" pkv_status pkv_phase_profile(unsigned long long* device_buf) {
+  cudaError_t e = pkv::set_phase_scan(device_buf);
+  if (e == cudaSuccess) e = pkv::set_phase_rerank(device_buf);
+  if (e == cudaSuccess) e = pkv::set_phase_qprep(device_buf);
+  if (e == cudaSuccess) e = pkv::set_phase_attend(device_buf);
+  if (e == cudaSuccess) e = pkv::set_phase_encode(device_buf);
+  return pkv::cuda_status(e, "pkv_phase_profile");
+}

@@ -29,9 +29,12 @@ __global__ void __launch_bounds__(RR_THREADS) rerank_kernel(const uint8_t* __res
                                                              const float* __restrict__ qnorm, int64_t cap, int n_q,
                                                              int n_kv, int G, int64_t cand_stride, int64_t id_offset,
                                                              float* __restrict__ est_out) {
+  phase_mark(K_RERANK, 0);
+  cta_mark(K_RERANK, 1);
   __shared__ __align__(16) float T[RT_ROWS * 16];
   pdl_trigger();
   pdl_wait();
+  phase_mark(K_RERANK, 1);
   const int h = blockIdx.y, b = blockIdx.z;
   const int g = h / G;
   const int64_t bhq = (int64_t)b * n_q + h;
@@ -71,6 +74,7 @@ __global__ void __launch_bounds__(RR_THREADS) rerank_kernel(const uint8_t* __res
   }
   __syncthreads();
   for (; pos < C_local; pos += gridDim.x * PER_CTA) {
+  phase_mark(K_RERANK, 2);
     const uint32_t cw[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
     const uint32_t ww[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
     const int nxt = pos + gridDim.x * PER_CTA;
@@ -95,6 +99,8 @@ __global__ void __launch_bounds__(RR_THREADS) rerank_kernel(const uint8_t* __res
     est += __shfl_xor_sync(pair_mask, est, 1);
     if (!half) eo[pos] = est * qn;
   }
+  phase_mark(K_RERANK, 3);
+  cta_mark(K_RERANK, 0);
 }
 
 // ---------------------------------------------------------------- radix top-k
@@ -267,23 +273,24 @@ __device__ __forceinline__ void topk_select(const float* __restrict__ es, const 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = BS_THREADS / 32;
   const int kv = min(k, count);
+  phase_mark(K_TOPK, 2);
   if (count > BS_CACHE) {  // long lists (1M-token contexts): radix select straight from global memory
     CandSrc src{es, ids};
     radix_topk(src, count, k, oi, oe);
     return;
   }
   float mn = INFINITY, mx = -INFINITY;
-  for (int i0 = 0; i0 < count; i0 += 8 * BS_THREADS) {  // 8 estimates + 8 ids in flight per thread
-    float ev[8];
-    int32_t iv[8];
+  for (int i0 = 0; i0 < count; i0 += 16 * BS_THREADS) {  // 16 estimates + 16 ids in flight per thread
+    float ev[16];
+    int32_t iv[16];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < 16; ++u) {
       const int i = i0 + u * BS_THREADS + tid;
       ev[u] = i < count ? es[i] : 0.f;
       iv[u] = i < count ? ids[i] : 0;
     }
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < 16; ++u) {
       const int i = i0 + u * BS_THREADS + tid;
       if (i < count) {
         ecache[i] = ev[u];
@@ -317,6 +324,7 @@ __device__ __forceinline__ void topk_select(const float* __restrict__ es, const 
     mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, x));
     mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, x));
   }
+  phase_mark(K_TOPK, 3);
   const float range = mx - mn;
   const float scale = (range > 0.f) ? (float)BS_BINS / range : 0.f;
   auto bin_of = [&](float e) -> int { return min(BS_BINS - 1, (int)((e - mn) * scale)); };
@@ -356,6 +364,7 @@ __device__ __forceinline__ void topk_select(const float* __restrict__ es, const 
     }
   }
   __syncthreads();
+  phase_mark(K_TOPK, 4);
   const int bstar = s_bstar;
   if (bstar >= 0 && (int)hist[bstar] > BS_BND) {  // boundary bin too large (massive ties): exact radix
     CandSrc src{es, ids};
@@ -369,6 +378,7 @@ __device__ __forceinline__ void topk_select(const float* __restrict__ es, const 
     else if (bb == bstar) bnd[atomicAdd(&s_bc, 1)] = ckey(e, icache[i]);
   }
   __syncthreads();
+  phase_mark(K_TOPK, 5);
   const int nb = s_bc, need = s_need, wc = s_wc;
   // exact selection inside the boundary bin by rank counting (keys are unique)
   for (int i = tid; i < nb; i += BS_THREADS) {
@@ -378,11 +388,26 @@ __device__ __forceinline__ void topk_select(const float* __restrict__ es, const 
     if (r < need) win[wc + r] = x;
   }
   __syncthreads();
-  // final order by rank counting over the kv winners
+  phase_mark(K_TOPK, 6);
+  // final order by rank counting over the kv winners: 4 threads per winner, each counting a quarter
+  __shared__ int rk[MAX_TOPK];
+  for (int i = tid; i < kv; i += BS_THREADS) rk[i] = 0;
+  __syncthreads();
+  {
+    const int per = (kv + 3) / 4;
+    for (int e = tid; e < 4 * kv; e += BS_THREADS) {
+      const int i = e % kv, part = e / kv;
+      const unsigned long long x = win[i];
+      int r = 0;
+      const int j1 = min(kv, (part + 1) * per);
+      for (int j2 = part * per; j2 < j1; ++j2) r += win[j2] > x;
+      if (r) atomicAdd(&rk[i], r);
+    }
+  }
+  __syncthreads();
   for (int i = tid; i < kv; i += BS_THREADS) {
     const unsigned long long x = win[i];
-    int r = 0;
-    for (int j2 = 0; j2 < kv; ++j2) r += win[j2] > x;
+    const int r = rk[i];
     oi[r] = (int32_t)(uint32_t)(x & 0xffffffffull);
     oe[r] = unord_f32((uint32_t)(x >> 32));
   }
@@ -401,6 +426,9 @@ struct AttendEpi {  // gather + attention over the selected rows, merged with pr
   float scale;
   const float* hot_part;  // [batch][n_q][MAX_SPLITS][PART], hsplits valid entries per head (may be 0)
   int hsplits;
+  const void* K_hot;      // [batch][n_kv][n_hot][D] hot rows attended in this kernel (may be null)
+  const void* V_hot;
+  int n_hot;
   void* out;
   float* lse;
   int G;
@@ -415,8 +443,10 @@ __global__ void __launch_bounds__(BS_THREADS) topk_kernel(const float* __restric
                                                            int64_t cand_stride, int k, int out_stride,
                                                            int32_t* out_idx, float* out_est, AttendEpi ep,
                                                            int64_t seg_stride) {
+  phase_mark(K_TOPK, 0);
   pdl_trigger();
   pdl_wait();
+  phase_mark(K_TOPK, 1);
   if (SELECT) {
     const int h = blockIdx.x, b = blockIdx.y, z = blockIdx.z;
     const int64_t bhq = (int64_t)b * n_q + h;
@@ -446,16 +476,27 @@ __global__ void __launch_bounds__(BS_THREADS) topk_kernel(const float* __restric
     const uint16_t* Vb = static_cast<const uint16_t*>(ep.V) + (int64_t)b * ep.sb + (int64_t)g * ep.sh + 4 * lane;
     float m = -INFINITY, l = 0.f, o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f;
     constexpr int RB = 8;
-    for (int r0 = warp; r0 < k; r0 += NW * RB) {
+    // rows of this head: the n_hot hot rows (sink + local + buffer) then the k retrieved rows
+    const uint16_t* Khb = static_cast<const uint16_t*>(ep.K_hot) + ((int64_t)b * n_kv + g) * ep.n_hot * D + 4 * lane;
+    const uint16_t* Vhb = static_cast<const uint16_t*>(ep.V_hot) + ((int64_t)b * n_kv + g) * ep.n_hot * D + 4 * lane;
+    const int nrows = ep.n_hot + k;
+    for (int r0 = warp; r0 < nrows; r0 += NW * RB) {
       int id[RB];
 #pragma unroll
-      for (int u = 0; u < RB; ++u) id[u] = (r0 + u * NW < k) ? oi[r0 + u * NW] : -1;
+      for (int u = 0; u < RB; ++u) {
+        const int r = r0 + u * NW;
+        id[u] = (r < ep.n_hot) ? r : (r < nrows ? oi[r - ep.n_hot] : -1);
+      }
       uint2 kr[RB], vr[RB];
 #pragma unroll
       for (int u = 0; u < RB; ++u) {
+        const int r = r0 + u * NW;
         kr[u] = make_uint2(0, 0);
         vr[u] = make_uint2(0, 0);
-        if (id[u] >= 0) {
+        if (r < ep.n_hot) {
+          kr[u] = ldg_v2(Khb + (int64_t)r * D);
+          vr[u] = ldg_v2(Vhb + (int64_t)r * D);
+        } else if (id[u] >= 0) {
           kr[u] = ldg_v2(Kb + (int64_t)id[u] * ep.st);
           vr[u] = ldg_v2(Vb + (int64_t)id[u] * ep.st);
         }
@@ -493,6 +534,7 @@ __global__ void __launch_bounds__(BS_THREADS) topk_kernel(const float* __restric
       }
       m = mx;
     }
+    phase_mark(K_TOPK, 8);
     sm_o[warp * D + 4 * lane] = o0;
     sm_o[warp * D + 4 * lane + 1] = o1;
     sm_o[warp * D + 4 * lane + 2] = o2;
@@ -504,10 +546,8 @@ __global__ void __launch_bounds__(BS_THREADS) topk_kernel(const float* __restric
     __syncthreads();
     if (threadIdx.x < D) {
       const int d = threadIdx.x;
-      const float* hp = ep.hot_part + bhq * MAX_SPLITS * PART;
       float M = -INFINITY;
       for (int w = 0; w < NW; ++w) M = fmaxf(M, sm_ml[2 * w]);
-      for (int s2 = 0; s2 < ep.hsplits; ++s2) M = fmaxf(M, __ldcg(hp + (int64_t)s2 * PART));
       float L = 0.f, O = 0.f;
       if (M != -INFINITY) {
         for (int w = 0; w < NW; ++w) {
@@ -517,19 +557,43 @@ __global__ void __launch_bounds__(BS_THREADS) topk_kernel(const float* __restric
           L += cw * sm_ml[2 * w + 1];
           O += cw * sm_o[w * D + d];
         }
-        for (int s2 = 0; s2 < ep.hsplits; ++s2) {
-          const float* pp = hp + (int64_t)s2 * PART;
-          const float ms = __ldcg(pp);
-          if (ms == -INFINITY) continue;
-          const float cs = exp2f(ms - M);
-          L += cs * __ldcg(pp + 1);
-          O += cs * __ldcg(pp + 2 + d);
+      }
+      // hot-row partials written by qprep (one per subspace CTA): all loads issued together, then one rescale
+      for (int s0 = 0; s0 < ep.hsplits; s0 += 16) {
+        const float* hp = ep.hot_part + (bhq * MAX_SPLITS + s0) * PART;
+        float ms[16], ls[16], os[16];
+#pragma unroll
+        for (int s2 = 0; s2 < 16; ++s2) {
+          ms[s2] = -INFINITY;
+          ls[s2] = os[s2] = 0.f;
+          if (s0 + s2 < ep.hsplits) {
+            ms[s2] = __ldcg(hp + s2 * PART);
+            ls[s2] = __ldcg(hp + s2 * PART + 1);
+            os[s2] = __ldcg(hp + s2 * PART + 2 + d);
+          }
+        }
+        float Mn = M;
+#pragma unroll
+        for (int s2 = 0; s2 < 16; ++s2) Mn = fmaxf(Mn, ms[s2]);
+        if (Mn != -INFINITY) {
+          const float c0 = (M == -INFINITY) ? 0.f : exp2f(M - Mn);
+          L *= c0;
+          O *= c0;
+#pragma unroll
+          for (int s2 = 0; s2 < 16; ++s2) {
+            if (ms[s2] == -INFINITY) continue;
+            const float cs = exp2f(ms[s2] - Mn);
+            L = fmaf(cs, ls[s2], L);
+            O = fmaf(cs, os[s2], O);
+          }
+          M = Mn;
         }
       }
       static_cast<__nv_bfloat16*>(ep.out)[bhq * D + d] = __float2bfloat16_rn(L > 0.f ? O / L : 0.f);
       if (ep.lse && d == 0) ep.lse[bhq] = L > 0.f ? (M + log2f(L)) * 0.6931471805599453f : -INFINITY;
     }
-    (void)n_kv;
+
+  phase_mark(K_TOPK, 9);    (void)n_kv;
   }
 }
 
@@ -573,6 +637,8 @@ cudaError_t init_rerank_attrs() {
 
 cudaError_t launch_rerank(const pkv_index* ix, int64_t C_cap, int64_t id_offset, cudaStream_t stream) {
   const Workspace* ws = ix->ws;
+  // Grid covers the candidates (one per thread pair): more resident threads than a one-wave grid whose threads
+  // loop over several candidates, because each candidate is a dependent id -> record load chain.
   int64_t tiles = (C_cap + RR_THREADS / 2 - 1) / (RR_THREADS / 2);
   if (tiles < 1) tiles = 1;
   dim3 grid((unsigned)tiles, ix->cfg.n_q_heads, ix->batch);
@@ -611,7 +677,7 @@ cudaError_t launch_topk_attend(const pkv_index* ix, int k, int32_t* out_idx, flo
   const Workspace* ws = ix->ws;
   dim3 grid(ix->cfg.n_q_heads, ix->batch);
   ProfScope p_(K_TOPK, stream);
-  AttendEpi ep{q, K, V, sb, sh, st, scale, hot_part, hsplits, out, lse, ix->dcfg.G};
+  AttendEpi ep{q, K, V, sb, sh, st, scale, hot_part, hsplits, nullptr, nullptr, 0, out, lse, ix->dcfg.G};
   return pdl_launch(topk_kernel<true>, grid, dim3(BS_THREADS), TK_SMEM, stream, (const float*)ws->est,
                     (const int32_t*)ws->cand, (const int32_t*)ws->sel, ix->cfg.n_q_heads, ws->cap, k, k, out_idx,
                     out_est, ep, (int64_t)0);
@@ -632,7 +698,7 @@ cudaError_t launch_topk_attend_rows(const pkv_index* ix, int k, const int32_t* i
   const Workspace* ws = ix->ws;
   dim3 grid(ix->cfg.n_q_heads, ix->batch);
   ProfScope p_(K_ATTEND, stream);
-  AttendEpi ep{q, K, V, sb, sh, st, scale, hot_part, hsplits, out, lse, ix->dcfg.G};
+  AttendEpi ep{q, K, V, sb, sh, st, scale, hot_part, hsplits, nullptr, nullptr, 0, out, lse, ix->dcfg.G};
   return pdl_launch(topk_kernel<true, false>, grid, dim3(BS_THREADS), TK_SMEM, stream, (const float*)ws->est,
                     (const int32_t*)ws->cand, (const int32_t*)ws->sel, ix->cfg.n_q_heads, ws->cap, k, k,
                     const_cast<int32_t*>(idx), (float*)nullptr, ep, (int64_t)0);
@@ -655,5 +721,7 @@ cudaError_t launch_dbg_cand(const pkv_index* ix, int64_t C, int32_t* dbg_cand, f
                                             dbg_cand, dbg_est);
   return cudaGetLastError();
 }
+
+cudaError_t set_phase_rerank(unsigned long long* p) { return set_phase_ptr_tu(p); }
 
 }  // namespace pkv

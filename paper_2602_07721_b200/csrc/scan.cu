@@ -105,11 +105,13 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1)
   const int64_t t_end = min(n, t_begin + chunk);
   const uint8_t* ids_bh = ids + (int64_t)bh * cap * NB;
   pdl_trigger();
+  phase_mark(K_SCAN, 0);
   // the centroid ids do not depend on the query: start streaming them before qprep has finished
   uint4 row[SCAN_UNROLL];
   load_rows<true>(row, ids_bh, (uint32_t)t_begin + (threadIdx.x >> 5) * 32 + (threadIdx.x & 31), (uint32_t)t_end);
   for (int i = threadIdx.x; i < SCAN_WARPS * GMAX * HB; i += SCAN_THREADS) hist[i] = 0u;
   pdl_wait();  // lookup table comes from qprep
+  phase_mark(K_SCAN, 1);
   // expand the compact table [c][16] into 4 interleaved replicas: word c*64 + s + 16 r
   const uint32_t* lg = lut_g + (int64_t)bh * NC * NB;
   uint32_t lv[NC * NB / SCAN_THREADS];  // all loads in flight before the stores
@@ -124,6 +126,7 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1)
   }
   __syncthreads();
   const uint32_t lut_base = (uint32_t)__cvta_generic_to_shared(lut);
+  phase_mark(K_SCAN, 2);
   uint32_t* scores_bh = scores + (int64_t)bh * cap;
   uint32_t* hist_w = hist + (threadIdx.x >> 5) * GMAX * HB;
   const uint32_t tb = (uint32_t)t_begin, te = (uint32_t)t_end;
@@ -136,6 +139,7 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1)
     scan_loop<RES, false, 4>(row, ids_bh, scores_bh, hist_w, tb, te, lut_base);  // G <= 4: unused bytes are 0
   }
   __syncthreads();
+  phase_mark(K_SCAN, 3);
   // per-CTA totals, then cumulative (suffix) counts cum[s] = #(score >= s), one warp per query head
   for (int i = threadIdx.x; i < GMAX * HB; i += SCAN_THREADS) {
     uint32_t s = 0;
@@ -166,6 +170,7 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1)
       out[warp * HB + 4 * lane + e] = run;
     }
   }
+  phase_mark(K_SCAN, 4);
 }
 
 // sel layout per (b, q head): [0] s*, [1] gt_local, [2] C_local, [3] take_local (written by chunk 0's CTA)
@@ -184,6 +189,8 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(
     const uint32_t* __restrict__ chunk_hist, const uint32_t* __restrict__ all_hist, int P, int rank, int batch,
     const uint32_t* __restrict__ scores, int64_t cap, int64_t n, int64_t chunk, int nchunks, int n_q, int n_kv,
     int G, int64_t C, int64_t id_offset, int64_t cand_stride, int32_t* __restrict__ cand, int32_t* __restrict__ sel) {
+  phase_mark(K_SELECT, 0);
+  cta_mark(K_SELECT, 1);
   __shared__ uint32_t Hg[GMAX][HB];   // global cumulative counts
   __shared__ uint32_t Hl[GMAX][HB];   // this rank's cumulative counts
   __shared__ int s_star[GMAX], gt_local[GMAX], take_local[GMAX];
@@ -192,6 +199,7 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(
   extern __shared__ uint2 sel_list[];  // per-warp compaction lists (VB * 32 entries each), SEL_SMEM bytes
   pdl_trigger();
   pdl_wait();
+  phase_mark(K_SELECT, 1);
   const int bh = blockIdx.y, j = blockIdx.x;
   const int b = bh / n_kv, g = bh % n_kv;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -231,6 +239,7 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(
     }
   }
   __syncthreads();
+  phase_mark(K_SELECT, 2);
   // A2: threshold per query head (warp hh)
   if (warp < G) {
     const int hh = warp;
@@ -304,6 +313,7 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(
     }
   }
   __syncthreads();
+  phase_mark(K_SELECT, 3);
   // B: compaction of this chunk. Warp w owns the contiguous segment [seg0, seg1).
   // Packed comparisons (scores <= 127, 4 query heads per u32): with K_gt = 0x7f - s*, K_ge = 0x80 - s* per byte,
   // bit 7 of byte h of (score + K_gt) is [score_h > s*_h] and of (score + K_ge) is [score_h >= s*_h] — no carries
@@ -390,6 +400,7 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(
 #pragma unroll
   for (int hh = 0; hh < GMAX; ++hh) cd[hh] = cand + ((int64_t)b * n_q + g * G + (hh < G ? hh : 0)) * cand_stride;
   const uint32_t lt = (1u << lane) - 1u;
+  phase_mark(K_SELECT, 4);
   // pass 2: keys with score >= s* for at least one head (~4 x beta of them) are first compacted, in key
   // order, into a per-warp list; the per-head ballots then run over that list only.
   uint2* wl = sel_list + warp * (VB * 32);
@@ -434,6 +445,8 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(
     }
     __syncwarp();
   }
+  phase_mark(K_SELECT, 5);
+  cta_mark(K_SELECT, 0);
 }
 
 __global__ void dbg_scores_kernel(const uint32_t* __restrict__ scores, int64_t cap, int64_t n, int n_q, int n_kv,
@@ -528,5 +541,7 @@ cudaError_t launch_head_hist(const pkv_index* ix, const ScanPlan& plan, uint32_t
                                             ix->cfg.n_kv_heads, ix->dcfg.G, head_hist_out);
   return cudaGetLastError();
 }
+
+cudaError_t set_phase_scan(unsigned long long* p) { return set_phase_ptr_tu(p); }
 
 }  // namespace pkv
