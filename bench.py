@@ -326,9 +326,12 @@ def run_ours(args):
     alg = {
         # 16 B of centroid ids per (key, KV head)
         "scan": batch * N_KV * n_loc * 16,
-        # bucket_topk reads the packed scores (4 B per key and KV head); the fused RSQ-IP rerank gathers one
-        # 128 B record and writes id + estimate (8 B) per (candidate, query head)
-        "select": batch * N_KV * n_loc * 4 + batch * N_Q * min(C, n_loc) * (128 + 8),
+        # bucket_topk reads the packed per-key scores (4 query heads x u8 = 4 B per key and KV head) and writes
+        # one candidate id (4 B) per (candidate, query head)
+        "select": batch * N_KV * n_loc * 4 + batch * N_Q * min(C, n_loc) * 4,
+        # fused RSQ-IP rerank: reads the candidate id and gathers its 128 B record, writes the estimate (4 B),
+        # per (candidate, query head)
+        "rerank": batch * N_Q * min(C, n_loc) * (4 + 128 + 4),
         # fused path: top-k over (est, id) pairs + gather of the k selected K/V rows (512 B per row and head);
         # two-call path: top-k only
         "topk": batch * N_Q * min(C, n_loc) * 8 + (batch * N_Q * TOP_K * 512 if fused else 0),
