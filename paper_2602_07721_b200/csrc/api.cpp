@@ -456,7 +456,7 @@ pkv_status retrieve_and_attend(pkv_index* ix, const void* q, const pkv_retrieve_
                                      out, lse, stream),
              "attend rows");
   } else {  // top-k selection fused with the gather + attention of hot U selected rows, one CTA per head
-    PKV_CUDA(launch_topk_attend(ix, p->top_k, out_idx, out_est, q, K, V, sb, sh, st, scale, ix->ws->hot_part, hsplits,
+    PKV_CUDA(launch_topk_attend(ix, std::min<int64_t>(p->n_cand, ix->n), p->top_k, out_idx, out_est, q, K, V, sb, sh, st, scale, ix->ws->hot_part, hsplits,
                                 out, lse, stream),
              "topk+attend");
   }

@@ -152,7 +152,7 @@ cudaError_t launch_topk(const pkv_index* ix, int64_t C_cap, int k, int32_t* out_
                         int out_stride, cudaStream_t stream);
 // Final top-k fused with the gather + attention of the selected rows and the merge with hot-row partials
 // (hot_part: [batch][n_q][MAX_SPLITS][PART], hsplits entries per head).
-cudaError_t launch_topk_attend(const pkv_index* ix, int k, int32_t* out_idx, float* out_est, const void* q,
+cudaError_t launch_topk_attend(const pkv_index* ix, int64_t C_cap, int k, int32_t* out_idx, float* out_est, const void* q,
                                const void* K, const void* V, int64_t sb, int64_t sh, int64_t st, float scale,
                                const float* hot_part, int hsplits, void* out, float* lse, cudaStream_t stream);
 int topk_segments(int64_t C_cap);

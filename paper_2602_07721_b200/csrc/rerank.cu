@@ -8,6 +8,10 @@
 //                (order-preserving fp32 bits of est << 32 | id), so ties in est go to the larger id;
 //                the k winners are then bitonic-sorted descending. Also used to merge the ranks' local top-k
 //                lists when sequence-sharded.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace pkv {
@@ -129,14 +133,15 @@ struct MergeSrc {  // sharded merge: P lists of k entries with stride
 };
 
 template <class Src>
-__device__ void radix_topk(const Src& src, int count, int k, int32_t* out_idx, float* out_est) {
-  extern __shared__ unsigned long long cache[];  // [TK_CACHE] (aliases the caller's dynamic smem)
+__device__ void radix_topk(const Src& src, int count, int k, int32_t* out_idx, float* out_est,
+                           int cache_cap = TK_CACHE) {
+  extern __shared__ unsigned long long cache[];  // [cache_cap] (aliases the caller's dynamic smem)
   __shared__ unsigned int hist[256];
   __shared__ unsigned long long win[MAX_TOPK];
   __shared__ unsigned long long prefix_s;
   __shared__ int need_s, done_s, nvalid_s, wcount;
   const int tid = threadIdx.x;
-  const bool cached = count <= TK_CACHE;
+  const bool cached = count <= cache_cap;
   int nv = 0;
   if (tid == 0) {
     nvalid_s = 0;
@@ -597,6 +602,416 @@ __global__ void __launch_bounds__(BS_THREADS) topk_kernel(const float* __restric
   }
 }
 
+// ---------------------------------------------------------------- cluster top-k (+ gather/attention)
+// One thread-block cluster of R CTAs per (sequence, query head). CTA r owns candidates [r*per, (r+1)*per)
+// (per = ceil(count/R)), caches them in shared memory and selects their local top-k with the value-range
+// bucket select (exact, composite keys), sorted descending. The global top-k is contained in the union of the
+// R local lists, so after one cluster barrier every CTA copies its peers' lists (at most R*k*8 bytes of
+// distributed shared memory — DSMEM bandwidth is ~20 B/clk per SM, so only these short lists cross it) and
+// ranks its own entries by binary search in them: global rank = local index + #peer entries greater. Entries
+// with rank < k are a prefix of the local list; the CTA writes them to out[rank] and, when ATTEND, gathers and
+// attends those rows (plus hot partials r, r+R, ...), sending one (m, l, o) partial to CTA 0, which merges the
+// R partials (log2 domain) after the second and last cluster barrier.
+constexpr int CL_MAX = 8;
+constexpr int CL_SLICE = 16384;  // candidates per CTA (est + id cached: 8 B each)
+constexpr int CL_PARTS = 8;      // threads counting one local winner's rank
+constexpr int CL_HOT = 4;        // hot partials per CTA prefetched into registers
+
+struct SmemCand {  // radix fallback source: the CTA's cached slice
+  const float* est;
+  const int32_t* idx;
+  __device__ __forceinline__ unsigned long long key(int i) const { return ckey(est[i], idx[i]); }
+};
+
+template <bool ATTEND>
+__global__ void __launch_bounds__(BS_THREADS) topk_cl_kernel(const float* __restrict__ est,
+                                                              const int32_t* __restrict__ cand,
+                                                              const int32_t* __restrict__ sel, int n_q,
+                                                              int64_t cand_stride, int k, int out_stride,
+                                                              int32_t* out_idx, float* out_est, AttendEpi ep,
+                                                              int slice_cap) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  constexpr int NW = BS_THREADS / 32;
+  // dynamic: [slice_cap] estimates + [slice_cap] ids; after the local select: the peers' lists, then the
+  // per-warp attention partials
+  extern __shared__ float ecache[];
+  int32_t* icache = reinterpret_cast<int32_t*>(ecache + slice_cap);
+  __shared__ unsigned int hist[BS_BINS];
+  __shared__ unsigned long long win[MAX_TOPK];
+  __shared__ unsigned long long lst[MAX_TOPK];  // local top-k, descending (read by the peers)
+  __shared__ unsigned long long bnd[BS_BND];
+  int* rk = reinterpret_cast<int*>(hist);  // [MAX_TOPK] local ranks (the histogram is dead by then)
+  __shared__ float cpart[CL_MAX][PART];  // CTA 0: the cluster's attention partials
+  __shared__ float red_mn[NW], red_mx[NW];
+  __shared__ unsigned int wsum[NW];
+  __shared__ int s_wc, s_bc, s_bstar, s_need, s_bcount, s_kl, s_nwin;
+  const int R = (int)cl.num_blocks(), r = (int)cl.block_rank();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int h = blockIdx.y, b = blockIdx.z;
+  const int64_t bhq = (int64_t)b * n_q + h;
+  phase_mark(K_TOPK, 0);
+  pdl_trigger();
+  float q0 = 0.f, q1 = 0.f, q2 = 0.f, q3 = 0.f;
+  if constexpr (ATTEND) {  // the query is an input of the layer, complete before the retrieval chain started
+    const float qscale = ep.scale * 1.4426950408889634f;
+    const uint2 qraw = ldg_v2(static_cast<const uint16_t*>(ep.q) + bhq * D + 4 * lane);
+    q0 = bf16_lo(qraw.x) * qscale;
+    q1 = bf16_hi(qraw.x) * qscale;
+    q2 = bf16_lo(qraw.y) * qscale;
+    q3 = bf16_hi(qraw.y) * qscale;
+  }
+  pdl_wait();
+  phase_mark(K_TOPK, 1);
+  const int count = sel[bhq * SEL_STRIDE + 2];
+  const int kv = min(k, count);
+  const int per = (count + R - 1) / R;
+  const int lo = min(count, r * per), n_loc = min(count, lo + per) - lo;
+  const int kl = min(k, n_loc);
+  const float* es = est + bhq * cand_stride;
+  const int32_t* ids = cand + bhq * cand_stride;
+  int32_t* oi = out_idx + bhq * out_stride;
+  float* oe = out_est + bhq * out_stride;
+  // hot-row partials owned by this CTA (written by qprep, complete once pdl_wait returned): prefetched
+  float hpm[CL_HOT], hpl[CL_HOT], hpo[CL_HOT];
+  if constexpr (ATTEND) {
+#pragma unroll
+    for (int u = 0; u < CL_HOT; ++u) {
+      const int s2 = r + u * R;
+      hpm[u] = -INFINITY;
+      hpl[u] = hpo[u] = 0.f;
+      if (s2 < ep.hsplits && tid < D) {
+        const float* pp = ep.hot_part + (bhq * MAX_SPLITS + s2) * PART;
+        hpm[u] = __ldcg(pp);
+        hpl[u] = __ldcg(pp + 1);
+        hpo[u] = __ldcg(pp + 2 + tid);
+      }
+    }
+  }
+
+  // ---- 1. cache the slice, min / max
+  float mn = INFINITY, mx = -INFINITY;
+  for (int i0 = 0; i0 < n_loc; i0 += 8 * BS_THREADS) {
+    float ev[8];
+    int32_t iv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + u * BS_THREADS + tid;
+      ev[u] = i < n_loc ? es[lo + i] : 0.f;
+      iv[u] = i < n_loc ? ids[lo + i] : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + u * BS_THREADS + tid;
+      if (i < n_loc) {
+        ecache[i] = ev[u];
+        icache[i] = iv[u];
+        mn = fminf(mn, ev[u]);
+        mx = fmaxf(mx, ev[u]);
+      }
+    }
+  }
+#pragma unroll
+  for (int x = 16; x > 0; x >>= 1) {
+    mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, x));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, x));
+  }
+  if (lane == 0) {
+    red_mn[warp] = mn;
+    red_mx[warp] = mx;
+  }
+  for (int i = tid; i < BS_BINS; i += BS_THREADS) hist[i] = 0u;
+  if (tid == 0) {
+    s_wc = 0;
+    s_bc = 0;
+    s_bstar = -1;
+    s_need = 0;
+    s_bcount = 0;
+    s_nwin = 0;
+  }
+  __syncthreads();
+  mn = red_mn[lane % NW];
+  mx = red_mx[lane % NW];
+#pragma unroll
+  for (int x = 16; x > 0; x >>= 1) {
+    mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, x));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, x));
+  }
+  phase_mark(K_TOPK, 2);
+  const float range = mx - mn;
+  const float scale = (range > 0.f) ? (float)BS_BINS / range : 0.f;
+  auto bin_of = [&](float e) -> int { return min(BS_BINS - 1, (int)((e - mn) * scale)); };
+
+  // ---- 2. local boundary bin (the kl-th largest) by a 2048-bin histogram
+  if (n_loc > kl) {
+    for (int i = tid; i < n_loc; i += BS_THREADS) atomicAdd(&hist[bin_of(ecache[i])], 1u);
+    __syncthreads();
+    constexpr int PER = BS_BINS / BS_THREADS;  // thread t owns bins [2048 - 4(t+1), 2048 - 4t)
+    unsigned int c[PER], sum = 0;
+#pragma unroll
+    for (int e = 0; e < PER; ++e) {
+      c[e] = hist[BS_BINS - 1 - PER * tid - e];
+      sum += c[e];
+    }
+    unsigned int inc = sum;
+#pragma unroll
+    for (int x = 1; x < 32; x <<= 1) {
+      const unsigned int o = __shfl_up_sync(0xffffffffu, inc, x);
+      if (lane >= x) inc += o;
+    }
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    unsigned int wbase = 0;
+    for (int w = 0; w < warp; ++w) wbase += wsum[w];
+    const unsigned int before = wbase + inc - sum;
+    if (before < (unsigned)kl && before + sum >= (unsigned)kl) {
+      unsigned int cum = before;
+#pragma unroll
+      for (int e = 0; e < PER; ++e) {
+        if (cum + c[e] >= (unsigned)kl) {
+          s_bstar = BS_BINS - 1 - PER * tid - e;
+          s_need = kl - (int)cum;
+          s_bcount = (int)c[e];
+          break;
+        }
+        cum += c[e];
+      }
+    }
+    __syncthreads();
+  }
+  phase_mark(K_TOPK, 3);
+  const int bstar = s_bstar;
+  if (s_bcount > BS_BND) {  // massive ties in one bin: exact radix select over the cached slice
+    int32_t* tix = reinterpret_cast<int32_t*>(bnd);
+    float* tes = reinterpret_cast<float*>(bnd) + MAX_TOPK;
+    radix_topk(SmemCand{ecache, icache}, n_loc, kl, tix, tes, 0);
+    __syncthreads();
+    for (int i = tid; i < kl; i += BS_THREADS) lst[i] = ckey(tes[i], tix[i]);
+  } else {
+    // ---- 3. partition: above the boundary bin -> win, inside it -> bnd (warp-aggregated smem atomics)
+    for (int i0 = 0; i0 < n_loc; i0 += BS_THREADS) {
+      const int i = i0 + tid;
+      float e = 0.f;
+      int bb = -2;
+      if (i < n_loc) {
+        e = ecache[i];
+        bb = (bstar < 0) ? BS_BINS : bin_of(e);
+      }
+      const unsigned mw = __ballot_sync(0xffffffffu, i < n_loc && bb > bstar);
+      const unsigned mb = __ballot_sync(0xffffffffu, i < n_loc && bb == bstar);
+      int basew = 0, baseb = 0;
+      if (lane == 0) {
+        if (mw) basew = atomicAdd(&s_wc, __popc(mw));
+        if (mb) baseb = atomicAdd(&s_bc, __popc(mb));
+      }
+      basew = __shfl_sync(0xffffffffu, basew, 0);
+      baseb = __shfl_sync(0xffffffffu, baseb, 0);
+      const unsigned below = (1u << lane) - 1u;
+      if ((mw >> lane) & 1u) win[basew + __popc(mw & below)] = ckey(e, icache[i]);
+      if ((mb >> lane) & 1u) bnd[baseb + __popc(mb & below)] = ckey(e, icache[i]);
+    }
+    __syncthreads();
+    // ---- 4. exact selection inside the boundary bin (keys are unique), then the local order
+    const int wc = s_wc, nb = s_bc, need = s_need;
+    for (int i = tid; i < nb; i += BS_THREADS) {
+      const unsigned long long x = bnd[i];
+      int rr = 0;
+      for (int j2 = 0; j2 < nb; ++j2) rr += bnd[j2] > x;
+      if (rr < need) win[wc + rr] = x;
+    }
+    __syncthreads();  // histogram reads done before it is reused as rk
+    for (int i = tid; i < kl; i += BS_THREADS) rk[i] = 0;
+    __syncthreads();
+    const int seg = (kl + CL_PARTS - 1) / CL_PARTS;
+    for (int e = tid; e < CL_PARTS * kl; e += BS_THREADS) {
+      const int i = e % kl, part = e / kl;
+      const unsigned long long x = win[i];
+      int rr = 0;
+      const int j1 = min(kl, (part + 1) * seg);
+      for (int j2 = part * seg; j2 < j1; ++j2) rr += win[j2] > x;
+      if (rr) atomicAdd(&rk[i], rr);
+    }
+    __syncthreads();
+    for (int i = tid; i < kl; i += BS_THREADS) lst[rk[i]] = win[i];
+  }
+  if (tid == 0) s_kl = kl;
+  phase_mark(K_TOPK, 4);
+  cl.sync();  // #1: every CTA's sorted local list is published
+  phase_mark(K_TOPK, 5);
+
+  // ---- 5. peers' lists copied in (DSMEM), global rank of the local entries by binary search
+  unsigned long long* plist = reinterpret_cast<unsigned long long*>(ecache);  // [R][k]
+  __shared__ int pk[CL_MAX];
+  if (tid < R) pk[tid] = (tid == r) ? 0 : *cl.map_shared_rank(&s_kl, tid);
+  __syncthreads();
+  for (int pr = 0; pr < R; ++pr) {
+    if (pr == r) continue;
+    const unsigned long long* src = cl.map_shared_rank(lst, pr);
+    for (int i = tid; i < pk[pr]; i += BS_THREADS) plist[pr * k + i] = src[i];
+  }
+  __syncthreads();
+  phase_mark(K_TOPK, 6);
+  for (int i = tid; i < kl; i += BS_THREADS) {
+    const unsigned long long x = lst[i];
+    int rank = i;
+    for (int pr = 0; pr < R; ++pr) {
+      const unsigned long long* L = plist + pr * k;
+      int a = 0, z = pk[pr];  // number of entries > x in the descending list L[0..pk)
+      while (a < z) {
+        const int m = (a + z) >> 1;
+        if (L[m] > x) a = m + 1;
+        else z = m;
+      }
+      rank += a;
+    }
+    if (rank < kv) {
+      oi[rank] = (int32_t)(uint32_t)(x & 0xffffffffull);
+      oe[rank] = unord_f32((uint32_t)(x >> 32));
+      atomicMax(&s_nwin, i + 1);
+    }
+  }
+  if (r == 0)
+    for (int i = kv + tid; i < k; i += BS_THREADS) {
+      oi[i] = -1;
+      oe[i] = -INFINITY;
+    }
+  __syncthreads();
+  phase_mark(K_TOPK, 7);
+
+  if constexpr (ATTEND) {
+    // ---- 6. attention over the local winners lst[0..nwin), merged with the owned hot partials
+    const int nwin = s_nwin;
+    const int g = h / ep.G;
+    const uint16_t* Kb = static_cast<const uint16_t*>(ep.K) + (int64_t)b * ep.sb + (int64_t)g * ep.sh + 4 * lane;
+    const uint16_t* Vb = static_cast<const uint16_t*>(ep.V) + (int64_t)b * ep.sb + (int64_t)g * ep.sh + 4 * lane;
+    float m = -INFINITY, l = 0.f, o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f;
+    constexpr int RB = 4;
+    for (int j0 = warp; j0 < nwin; j0 += NW * RB) {
+      int id[RB];
+#pragma unroll
+      for (int u = 0; u < RB; ++u) {
+        const int j = j0 + u * NW;
+        id[u] = j < nwin ? (int)(uint32_t)(lst[j] & 0xffffffffull) : -1;
+      }
+      uint2 kr[RB], vr[RB];
+#pragma unroll
+      for (int u = 0; u < RB; ++u) {
+        kr[u] = make_uint2(0, 0);
+        vr[u] = make_uint2(0, 0);
+        if (id[u] >= 0) {
+          kr[u] = ldg_v2(Kb + (int64_t)id[u] * ep.st);
+          vr[u] = ldg_v2(Vb + (int64_t)id[u] * ep.st);
+        }
+      }
+      float x[RB];
+#pragma unroll
+      for (int u = 0; u < RB; ++u)
+        x[u] = bf16_lo(kr[u].x) * q0 + bf16_hi(kr[u].x) * q1 + bf16_lo(kr[u].y) * q2 + bf16_hi(kr[u].y) * q3;
+#pragma unroll
+      for (int xm = 16; xm > 0; xm >>= 1) {
+#pragma unroll
+        for (int u = 0; u < RB; ++u) x[u] += __shfl_xor_sync(0xffffffffu, x[u], xm);
+      }
+      float mxx = m;
+#pragma unroll
+      for (int u = 0; u < RB; ++u)
+        if (id[u] >= 0) mxx = fmaxf(mxx, x[u]);
+      const float c = exp2f(m - mxx);
+      l *= c;
+      o0 *= c;
+      o1 *= c;
+      o2 *= c;
+      o3 *= c;
+#pragma unroll
+      for (int u = 0; u < RB; ++u) {
+        if (id[u] >= 0) {
+          const float pu = exp2f(x[u] - mxx);
+          l += pu;
+          o0 = fmaf(pu, bf16_lo(vr[u].x), o0);
+          o1 = fmaf(pu, bf16_hi(vr[u].x), o1);
+          o2 = fmaf(pu, bf16_lo(vr[u].y), o2);
+          o3 = fmaf(pu, bf16_hi(vr[u].y), o3);
+        }
+      }
+      m = mxx;
+    }
+    phase_mark(K_TOPK, 8);
+    float* sm_o = ecache + 2 * CL_MAX * k;         // [NW][D] (after the peers' lists)
+    float* sm_ml = sm_o + NW * D;                  // [NW][2]
+    sm_o[warp * D + 4 * lane] = o0;
+    sm_o[warp * D + 4 * lane + 1] = o1;
+    sm_o[warp * D + 4 * lane + 2] = o2;
+    sm_o[warp * D + 4 * lane + 3] = o3;
+    if (lane == 0) {
+      sm_ml[2 * warp] = m;
+      sm_ml[2 * warp + 1] = l;
+    }
+    __syncthreads();
+    if (tid < D) {
+      const int d = tid;
+      float M = -INFINITY;
+      for (int w = 0; w < NW; ++w) M = fmaxf(M, sm_ml[2 * w]);
+#pragma unroll
+      for (int u = 0; u < CL_HOT; ++u) M = fmaxf(M, hpm[u]);
+      for (int s2 = r + CL_HOT * R; s2 < ep.hsplits; s2 += R)
+        M = fmaxf(M, __ldcg(ep.hot_part + (bhq * MAX_SPLITS + s2) * PART));
+      float L = 0.f, O = 0.f;
+      if (M != -INFINITY) {
+        for (int w = 0; w < NW; ++w) {
+          const float mw = sm_ml[2 * w];
+          if (mw == -INFINITY) continue;
+          const float cw = exp2f(mw - M);
+          L = fmaf(cw, sm_ml[2 * w + 1], L);
+          O = fmaf(cw, sm_o[w * D + d], O);
+        }
+#pragma unroll
+        for (int u = 0; u < CL_HOT; ++u) {
+          if (hpm[u] == -INFINITY) continue;
+          const float cs = exp2f(hpm[u] - M);
+          L = fmaf(cs, hpl[u], L);
+          O = fmaf(cs, hpo[u], O);
+        }
+        for (int s2 = r + CL_HOT * R; s2 < ep.hsplits; s2 += R) {
+          const float* pp = ep.hot_part + (bhq * MAX_SPLITS + s2) * PART;
+          const float ms = __ldcg(pp);
+          if (ms == -INFINITY) continue;
+          const float cs = exp2f(ms - M);
+          L = fmaf(cs, __ldcg(pp + 1), L);
+          O = fmaf(cs, __ldcg(pp + 2 + d), O);
+        }
+      }
+      float* cp = cl.map_shared_rank(&cpart[r][0], 0);
+      if (d == 0) {
+        cp[0] = M;
+        cp[1] = L;
+      }
+      cp[2 + d] = O;
+    }
+  }
+  phase_mark(K_TOPK, 9);
+  cl.sync();  // #2: no CTA reads a peer's shared memory past this point; CTA 0 holds the R partials
+  phase_mark(K_TOPK, 10);
+  if constexpr (ATTEND) {
+    if (r == 0 && tid < D) {
+      const int d = tid;
+      float M = -INFINITY;
+      for (int pr = 0; pr < R; ++pr) M = fmaxf(M, cpart[pr][0]);
+      float L = 0.f, O = 0.f;
+      if (M != -INFINITY) {
+        for (int pr = 0; pr < R; ++pr) {
+          if (cpart[pr][0] == -INFINITY) continue;
+          const float c = exp2f(cpart[pr][0] - M);
+          L = fmaf(c, cpart[pr][1], L);
+          O = fmaf(c, cpart[pr][2 + d], O);
+        }
+      }
+      static_cast<__nv_bfloat16*>(ep.out)[bhq * D + d] = __float2bfloat16_rn(L > 0.f ? O / L : 0.f);
+      if (ep.lse && d == 0) ep.lse[bhq] = L > 0.f ? (M + log2f(L)) * 0.6931471805599453f : -INFINITY;
+    }
+  }
+  phase_mark(K_TOPK, 11);
+}
+
 __global__ void __launch_bounds__(TK_THREADS) merge_kernel(const float* __restrict__ all_est,
                                                             const int32_t* __restrict__ all_idx, int P, int batch,
                                                             int n_q, int k, int32_t* out_idx, float* out_est,
@@ -621,8 +1036,26 @@ __global__ void dbg_cand_kernel(const int32_t* __restrict__ cand, const float* _
 
 }  // namespace
 
+// Cluster size for the top-k of C_cap candidates per head: enough CTAs to fill the SMs once (at most 8),
+// and enough that each slice fits CL_SLICE. 0: too long for one cluster (segmented top-k + merge instead).
+static int topk_cluster(const pkv_index* ix, int64_t C_cap, int* slice) {
+  const int64_t heads = (int64_t)ix->cfg.n_q_heads * ix->batch;
+  int R = (int)std::max<int64_t>(1, std::min<int64_t>(CL_MAX, ix->num_sms / heads));
+  if (C_cap < 1) C_cap = 1;
+  while (R < CL_MAX && (C_cap + R - 1) / R > CL_SLICE) ++R;
+  if ((C_cap + R - 1) / R > CL_SLICE) return 0;
+  *slice = (int)((C_cap + R - 1) / R);
+  return R;
+}
+
+static size_t topk_cluster_smem(int slice, int k) {
+  // max(candidate cache, peers' lists [CL_MAX][k] u64 + per-warp attention partials)
+  const size_t need = (size_t)slice * 8, lists = (size_t)CL_MAX * k * 8 + (size_t)(BS_THREADS / 32) * (D + 2) * 4;
+  return need > lists ? need : lists;
+}
+
 int topk_segments(int64_t C_cap) {
-  return C_cap > BS_CACHE ? (int)((C_cap + BS_CACHE - 1) / BS_CACHE) : 1;
+  return C_cap > (int64_t)CL_MAX * CL_SLICE ? (int)((C_cap + BS_CACHE - 1) / BS_CACHE) : 1;
 }
 
 cudaError_t init_rerank_attrs() {
@@ -631,6 +1064,12 @@ cudaError_t init_rerank_attrs() {
   e = cudaFuncSetAttribute(topk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TK_SMEM);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(topk_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TK_SMEM);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(topk_cl_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, CL_SLICE * 8);
+  if (e != cudaSuccess) return e;
+  static_assert(CL_SLICE * 8 >= CL_MAX * MAX_TOPK * 8 + (BS_THREADS / 32) * (D + 2) * 4, "cluster top-k smem");
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(topk_cl_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, CL_SLICE * 8);
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TK_SMEM);
 }
@@ -656,6 +1095,13 @@ cudaError_t launch_topk(const pkv_index* ix, int64_t C_cap, int k, int32_t* out_
   dim3 grid(ix->cfg.n_q_heads, ix->batch);
   ProfScope p_(K_TOPK, stream);
   AttendEpi ep{};
+  int slice = 0;
+  const int R = topk_cluster(ix, C_cap, &slice);
+  if (R > 0)
+    return pdl_launch_cluster(topk_cl_kernel<false>, dim3(R, ix->cfg.n_q_heads, ix->batch), dim3(BS_THREADS),
+                              topk_cluster_smem(slice, k), stream, R, (const float*)ws->est, (const int32_t*)ws->cand,
+                              (const int32_t*)ws->sel, ix->cfg.n_q_heads, ws->cap, k, out_stride, out_idx, out_est,
+                              ep, slice);
   const int nseg = topk_segments(C_cap);
   if (nseg > 1) {  // long candidate lists: per-segment top-k into the exchange slots, then the merge kernel
     const size_t slot = (size_t)ix->batch * ix->cfg.n_q_heads * MAX_TOPK;
@@ -671,13 +1117,20 @@ cudaError_t launch_topk(const pkv_index* ix, int64_t C_cap, int k, int32_t* out_
                     out_idx, out_est, ep, (int64_t)0);
 }
 
-cudaError_t launch_topk_attend(const pkv_index* ix, int k, int32_t* out_idx, float* out_est, const void* q,
+cudaError_t launch_topk_attend(const pkv_index* ix, int64_t C_cap, int k, int32_t* out_idx, float* out_est, const void* q,
                                const void* K, const void* V, int64_t sb, int64_t sh, int64_t st, float scale,
                                const float* hot_part, int hsplits, void* out, float* lse, cudaStream_t stream) {
   const Workspace* ws = ix->ws;
   dim3 grid(ix->cfg.n_q_heads, ix->batch);
   ProfScope p_(K_TOPK, stream);
   AttendEpi ep{q, K, V, sb, sh, st, scale, hot_part, hsplits, nullptr, nullptr, 0, out, lse, ix->dcfg.G};
+  int slice = 0;
+  const int R = topk_cluster(ix, C_cap, &slice);
+  if (R > 0)
+    return pdl_launch_cluster(topk_cl_kernel<true>, dim3(R, ix->cfg.n_q_heads, ix->batch), dim3(BS_THREADS),
+                              topk_cluster_smem(slice, k), stream, R, (const float*)ws->est, (const int32_t*)ws->cand,
+                              (const int32_t*)ws->sel, ix->cfg.n_q_heads, ws->cap, k, k, out_idx, out_est, ep,
+                              slice);
   return pdl_launch(topk_kernel<true>, grid, dim3(BS_THREADS), TK_SMEM, stream, (const float*)ws->est,
                     (const int32_t*)ws->cand, (const int32_t*)ws->sel, ix->cfg.n_q_heads, ws->cap, k, k, out_idx,
                     out_est, ep, (int64_t)0);

@@ -327,10 +327,11 @@ def test_retrieve_and_attend_matches_two_calls(pkv, n, n_hot, k):
         assert abs(float(l1[0, h]) - lse) <= 1e-3 * max(1.0, abs(lse))
 
 
-def test_segmented_topk_long_candidate_list(pkv):
-    """C > 16384 (the 1M-token regime): per-segment top-k + merge must equal the oracle top-k up to ties, and
+@pytest.mark.parametrize("n,C", [(60000, 40000), (150000, 140000)])
+def test_segmented_topk_long_candidate_list(pkv, n, C):
+    """Long candidate lists (the 1M-token regime): C = 40000 takes the cluster top-k (several CTAs per head),
+    C = 140000 > 8 x 16384 the per-segment top-k + merge. Both must equal the oracle top-k up to ties, and
     retrieve_and_attend must take the same ids."""
-    n, C = 60000, 40000
     K, q, V = make_problem(17, 1, 4, 1, n)
     run_and_check(pkv, K, q, V, k=100, C=C, check_all_heads=False)
     cfg = pkv.config_init(4, 1, SB)
@@ -343,3 +344,18 @@ def test_segmented_topk_long_candidate_list(pkv):
     i1, e1, o1, l1 = pkv.retrieve_and_attend(ix, q, K, V, 100, Kh, Vh, n_cand=C)
     assert torch.equal(i0, i1) and torch.equal(e0, e1)
     assert torch.allclose(o0.float(), o1.float(), atol=4e-3) and torch.allclose(l0, l1, atol=1e-4)
+
+
+def test_topk_massive_estimate_ties(pkv):
+    """3000 identical keys near the query: their estimates tie exactly, so the top-k boundary bin overflows
+    and the cluster top-k takes its exact radix fallback; ties resolve to the larger id."""
+    K, q, V = make_problem(23, 1, 4, 1, 6000, plant=False)
+    K[0, 0, 1000:4000] = (q[0, 0].float() * 3.0).to(torch.bfloat16)
+    ix, idx, est, dbg = run_and_check(pkv, K, q, V, k=100, C=4500, check_all_heads=False)
+    ig = idx[0, 0].cpu().numpy()
+    dup = ig[(ig >= 1000) & (ig < 4000)]  # the tied duplicates taken: the newest ones, newest first
+    assert len(dup) > 50 and np.array_equal(dup, np.arange(3999, 3999 - len(dup), -1)), ig[:10]
+    Kh = synth.isotropic(97, (1, 1, 16, 128), device="cuda")
+    Vh = synth.isotropic(98, (1, 1, 16, 128), device="cuda")
+    i1, e1, o1, l1 = pkv.retrieve_and_attend(ix, q, K, V, 100, Kh, Vh, n_cand=4500)
+    assert torch.equal(i1, idx) and torch.equal(e1, est)
