@@ -156,16 +156,72 @@ pkv_status sparse_attend(pkv_index* index, const void* q, const void* K, const v
                          int32_t n_hot, float scale, void* out, float* lse, cudaStream_t stream);
 
 /* (3)+(4) retrieve_and_attend — one decode step of one layer: exactly retrieve_topk followed by sparse_attend
- * with the same arguments (K/V rows strided as above, HBM or UVA), scheduled as one unit: the hot-row attention
- * runs on a library-owned forked stream concurrently with the retrieval kernels (fork/join through events on
- * the caller's stream, CUDA-graph capturable), and the final top-k selection is fused with the gather and
- * attention of the selected rows and the merge with the hot-row partials. out_idx/out_est are identical to
- * retrieve_topk's; out/lse equal sparse_attend's up to fp32 summation order. When sequence-sharded it simply
- * calls the two entry points. */
+ * with the same arguments (K/V rows strided as above, HBM or UVA), scheduled as one unit on the caller's
+ * stream (CUDA-graph capturable, no host sync): the hot-row attention (sink + local + buffer) runs
+ * inside the query-prep kernel, 16 partial softmax states per query head, and the final top-k selection is
+ * fused with the gather and attention of the selected rows and the merge with the hot partials (one
+ * thread-block cluster per query head). out_idx/out_est are identical to retrieve_topk's; out/lse equal
+ * sparse_attend's up to fp32 summation order. n_hot <= 1024. When sequence-sharded it calls the two entry
+ * points. Ordering: K_hot/V_hot are read before the kernels wait on their stream predecessor's completion
+ * (programmatic dependent launch), so a producer kernel that itself triggers early must not write them. */
 pkv_status retrieve_and_attend(pkv_index* index, const void* q, const pkv_retrieve_params* params, const void* K,
                                const void* V, int64_t sb, int64_t sh, int64_t st, const void* K_hot,
                                const void* V_hot, int32_t n_hot, float scale, int32_t* out_idx, float* out_est,
                                void* out, float* lse, cudaStream_t stream);
+
+/* retrieve_and_attend with hot rows stored with a row capacity hot_rows >= n_hot per (sequence, KV head):
+ * hot row t of (b, h) at K_hot + ((b*n_kv + h)*hot_rows + t)*128 (the region manager's layout). Not
+ * supported on a sequence-sharded index unless hot_rows == n_hot. */
+pkv_status retrieve_and_attend_rows(pkv_index* index, const void* q, const pkv_retrieve_params* params,
+                                    const void* K, const void* V, int64_t sb, int64_t sh, int64_t st,
+                                    const void* K_hot, const void* V_hot, int32_t n_hot, int32_t hot_rows,
+                                    float scale, int32_t* out_idx, float* out_est, void* out, float* lse,
+                                    cudaStream_t stream);
+
+/* ---------------------------------------------------------------------------------------------------
+ * Streaming decode: the four-region KV cache of PAPER §4.2.3 "Buffer Update".
+ *   Sink      the first `sink` tokens, kept on the GPU (full precision, always attended)
+ *   Retrieval every older token: indexed (centroid ids, 4-bit codes, w) in `index`, full-precision K/V in a
+ *             store owned by the stream — HBM, or pinned host memory read through UVA (offload setting)
+ *   Local     the newest `local_size` tokens before the buffer, on the GPU, always attended
+ *   Update    up to `update_size` newly generated tokens, on the GPU, always attended
+ * Each decode token is appended to the Update buffer; when it holds update_size tokens the oldest tokens of
+ * Local U Update beyond local_size are evicted into Retrieval: their keys are encoded and appended to the
+ * index (append_decode_keys, on the GPU) and their K/V rows copied to the store, and the rest is shifted to
+ * become the new Local. Retrieval ids returned by pkv_stream_decode are store positions:
+ * retrieval id i is token sink + i of the sequence. All copies and kernels run on the caller's stream
+ * (asynchronous to the host); decode steps without a flush are CUDA-graph capturable.
+ * ------------------------------------------------------------------------------------------------- */
+typedef struct pkv_stream pkv_stream; /* opaque */
+typedef struct {
+  int32_t sink;         /* 16 */
+  int32_t local_size;   /* 256 (Table 1) */
+  int32_t update_size;  /* 512 (Table 1 "Update"; the flush size m of P:458) */
+  int32_t offload_host; /* 0: retrieval K/V in HBM; 1: in pinned host memory (UVA reads) */
+} pkv_stream_config;
+/* Create a stream over `index` (which it uses but does not own; its capacity bounds the retrieval zone).
+ * Allocates the hot buffer [batch][n_kv][sink + local_size + update_size][128] bf16 (K and V) and the
+ * retrieval store [batch][n_kv][capacity][128] bf16 (K and V). Errors: INVALID_ARG (sizes < 0, sink +
+ * local_size + update_size > 1024 or update_size < 1), CUDA (allocation). */
+pkv_status pkv_stream_create(pkv_index* index, const pkv_stream_config* config, pkv_stream** out);
+pkv_status pkv_stream_destroy(pkv_stream* s);
+/* Prefill with n_tokens >= sink tokens (K, V device bf16, element (b,h,t,d) at base + b*sb + h*sh + t*st + d):
+ * tokens [0, sink) -> Sink, the newest min(local_size, n_tokens - sink) -> Local, the rest -> Retrieval
+ * (encode_keys + store copy). Replaces any previous content. Errors: INVALID_ARG, CAPACITY. */
+pkv_status pkv_stream_prefill(pkv_stream* s, const void* K, const void* V, int64_t sb, int64_t sh, int64_t st,
+                              int64_t n_tokens, cudaStream_t stream);
+/* One decode step of this layer: append (k_new, v_new) (device bf16 [batch][n_kv][128]) to the Update buffer,
+ * flush when it is full, then retrieve_and_attend with q over Sink U Local U Update (hot rows) and the
+ * retrieved rows of the store. params: probes_T/n_cand <= 0 take the schedule for the current retrieval
+ * length (pkv_schedule). Outputs as retrieve_and_attend. CAPACITY if a flush would overflow the index (no
+ * side effect). */
+pkv_status pkv_stream_decode(pkv_stream* s, const void* q, const void* k_new, const void* v_new,
+                             const pkv_retrieve_params* params, float scale, int32_t* out_idx, float* out_est,
+                             void* out, float* lse, cudaStream_t stream);
+/* Region sizes: retrieval tokens, local tokens, buffered tokens, and the retrieval store's device-visible
+ * K/V base pointers ([batch][n_kv][capacity][128] bf16) and hot buffer pointers. Any output may be NULL. */
+pkv_status pkv_stream_state(const pkv_stream* s, int64_t* n_retrieval, int32_t* n_local, int32_t* n_buffer,
+                            const void** K_store, const void** V_store, const void** K_hot, const void** V_hot);
 
 /* Diagnostics: copy metadata of positions [start, start+count) into caller device buffers in the
  * canonical layout: ids uint8 [batch][n_kv][count][16] (subspace order), codes uint8

@@ -12,8 +12,10 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
-OUT = os.path.join(HERE, "libpariskv.so")
-BUILD = os.path.join(HERE, "build")
+# PKV_LIB_TAG=x builds libpariskv_x.so from build_x/ (experiment variants; the binding loads it with PKV_LIB=x)
+_TAG = os.environ.get("PKV_LIB_TAG", "")
+OUT = os.path.join(HERE, f"libpariskv_{_TAG}.so" if _TAG else "libpariskv.so")
+BUILD = os.path.join(HERE, f"build_{_TAG}" if _TAG else "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", f"-I{os.path.join(ROOT, 'include')}",
@@ -22,6 +24,7 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", f"-I{os.pa
 
 # PKV_PHASE_PROFILE=1: compile the globaltimer phase marks in (scripts/phase_profile.py); never for benchmarks
 DEFS = ["-DPKV_PHASE_PROFILE"] if os.environ.get("PKV_PHASE_PROFILE") == "1" else []
+DEFS += [f"-D{d}" for d in os.environ.get("PKV_BUILD_DEFS", "").split()]  # experiment switches
 STAMP = os.path.join(BUILD, "defs.txt")
 
 

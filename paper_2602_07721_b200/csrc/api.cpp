@@ -175,7 +175,7 @@ pkv_status check_kv_layout(const void* K, int64_t sb, int64_t sh, int64_t st, co
 pkv_status phase_scan(pkv_index* ix, const void* q, const pkv_retrieve_params* p, ScanPlan& plan, cudaStream_t s,
                       const HotArgs* ha = nullptr) {
   const int64_t n = ix->n;
-  const HotArgs none{nullptr, nullptr, 0, 0.f, nullptr};
+  const HotArgs none{nullptr, nullptr, 0, 0.f, nullptr, 0};
   PKV_CUDA(launch_qprep(ix, q, p->probes_T, p->dbg_q_rot, ha ? *ha : none, s), "qprep");
   plan = plan_scan(ix, n > 0 ? n : 1);
   if (n > 0) {
@@ -425,8 +425,17 @@ pkv_status retrieve_and_attend(pkv_index* ix, const void* q, const pkv_retrieve_
                                int64_t sb, int64_t sh, int64_t st, const void* K_hot, const void* V_hot, int32_t n_hot,
                                float scale, int32_t* out_idx, float* out_est, void* out, float* lse,
                                cudaStream_t stream) {
+  return retrieve_and_attend_rows(ix, q, p, K, V, sb, sh, st, K_hot, V_hot, n_hot, n_hot, scale, out_idx, out_est, out,
+                                  lse, stream);
+}
+
+pkv_status retrieve_and_attend_rows(pkv_index* ix, const void* q, const pkv_retrieve_params* p, const void* K,
+                                    const void* V, int64_t sb, int64_t sh, int64_t st, const void* K_hot,
+                                    const void* V_hot, int32_t n_hot, int32_t hot_rows, float scale, int32_t* out_idx,
+                                    float* out_est, void* out, float* lse, cudaStream_t stream) {
   if (!ix) return set_error(PKV_ERR_INVALID_ARG, "retrieve_and_attend: null index");
-  if (ix->comm) {  // sequence-sharded: the exchanges sit between the phases; use the two calls
+  if (ix->comm) {
+    if (hot_rows != n_hot) return set_error(PKV_ERR_UNSUPPORTED, "retrieve_and_attend: strided hot rows when sharded");  // sequence-sharded: the exchanges sit between the phases; use the two calls
     pkv_status st1 = retrieve_topk(ix, q, p, out_idx, out_est, stream);
     if (st1 != PKV_OK) return st1;
     return sparse_attend(ix, q, K, V, sb, sh, st, out_idx, p->top_k, K_hot, V_hot, n_hot, scale, out, lse, stream);
@@ -443,7 +452,8 @@ pkv_status retrieve_and_attend(pkv_index* ix, const void* q, const pkv_retrieve_
   DeviceGuard g(ix->device);
   ScanPlan plan;
   // the hot-row attention rides in the query-prep kernel (16 partials per head, merged by the last kernel)
-  const HotArgs ha{K_hot, V_hot, n_hot, scale, n_hot > 0 ? ix->ws->hot_part : nullptr};
+  if (hot_rows < n_hot) return set_error(PKV_ERR_INVALID_ARG, "retrieve_and_attend: hot_rows < n_hot");
+  const HotArgs ha{K_hot, V_hot, n_hot, scale, n_hot > 0 ? ix->ws->hot_part : nullptr, hot_rows};
   st0 = phase_scan(ix, q, p, plan, stream, &ha);
   if (st0 != PKV_OK) return st0;
   st0 = phase_select_rerank(ix, p, plan, nullptr, 1, 0, stream);

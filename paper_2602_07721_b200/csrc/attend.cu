@@ -34,8 +34,8 @@ struct SoftState {
 static_assert(AT_BATCH * GMAX == 32, "transpose-reduction maps one (row, head) pair per lane");
 
 __global__ void __launch_bounds__(AT_WARPS * 32) attend_partial_kernel(AttendArgs a, int n_q, int n_kv, int G,
-                                                                       int items_per_split, float* __restrict__ part,
-                                                                       unsigned int* __restrict__ ticket, void* out,
+                                                                       int items_per_split, float* part,
+                                                                       unsigned int* ticket, void* out,
                                                                        float* lse) {
   phase_mark(K_ATTEND, 0);
   __shared__ __align__(16) float sm_x[AT_WARPS][AT_BATCH * GMAX];
@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(AT_WARPS * 32) attend_partial_kernel(AttendArg
   if (threadIdx.x == 0) ticket[b * n_kv + g] = 0u;  // re-arm for the next launch / graph replay
 }
 
-__global__ void __launch_bounds__(D) attend_combine_kernel(const float* __restrict__ parts, int nsplits, int P,
+__global__ void __launch_bounds__(D) attend_combine_kernel(const float* parts, int nsplits, int P,
                                                             int64_t rank_stride, int n_q, void* out, float* lse) {
   const int h = blockIdx.x, b = blockIdx.y, d = threadIdx.x;
   const int64_t bhq = (int64_t)b * n_q + h;

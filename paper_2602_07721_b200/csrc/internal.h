@@ -125,9 +125,10 @@ cudaError_t launch_export(const pkv_index* ix, int64_t start, int64_t count, uin
 struct HotArgs {
   const void* K_hot;
   const void* V_hot;
-  int n_hot;
+  int n_hot;     // rows attended per (sequence, KV head)
   float scale;
   float* part;
+  int hot_rows;  // row capacity per (sequence, KV head): element (b, h, t, d) at K_hot + ((b*n_kv + h)*hot_rows + t)*D + d
 };
 cudaError_t launch_qprep(const pkv_index* ix, const void* q, int T, float* dbg_q_rot, const HotArgs& ha,
                          cudaStream_t stream);

@@ -52,7 +52,10 @@ const char* kNames[K_NUM_KINDS] = {"encode", "qprep", "scan", "select", "unused"
 
 }  // namespace
 
+thread_local int t_kind = -1;  // kind of the launch being bracketed (pdl_enabled's per-kernel mask)
+
 ProfScope::ProfScope(int kind, cudaStream_t s) : kind_(kind), s_(s) {
+  t_kind = kind;
   if (g_on) {
     std::lock_guard<std::mutex> l(g_mu);
     a_ = get_event();
@@ -104,7 +107,12 @@ bool pdl_enabled() {
     const char* e = std::getenv("PKV_NO_PDL");
     return !(e && e[0] == '1');
   }();
-  return on;
+  // PKV_NO_PDL_MASK: bit k disables programmatic launch for kernel kind k (KernelKind) — a diagnostic switch
+  static const unsigned mask = [] {
+    const char* e = std::getenv("PKV_NO_PDL_MASK");
+    return e ? (unsigned)std::strtoul(e, nullptr, 0) : 0u;
+  }();
+  return on && !(t_kind >= 0 && ((mask >> t_kind) & 1u));
 }
 }  // namespace pkv
 

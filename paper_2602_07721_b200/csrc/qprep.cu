@@ -38,10 +38,10 @@ __device__ __forceinline__ void ce(KV& mine, const KV& o, int p, int k, int j) {
 
 constexpr int HOT_RB = 8;  // hot rows per warp and round
 
-__global__ void __launch_bounds__(QP_THREADS) qprep_kernel(const uint16_t* __restrict__ q, int T, DevCfg cfg,
-                                                          uint32_t* __restrict__ lut, float* __restrict__ rtab,
-                                                          float* __restrict__ qnorm, float* __restrict__ qrot,
-                                                          float* __restrict__ dbg_q_rot, HotArgs ha) {
+__global__ void __launch_bounds__(QP_THREADS) qprep_kernel(const uint16_t* q, int T, DevCfg cfg,
+                                                          uint32_t* lut, float* rtab,
+                                                          float* qnorm, float* qrot,
+                                                          float* dbg_q_rot, HotArgs ha) {
   __shared__ unsigned long long sk[NC];
   __shared__ uint32_t si[NC];
   __shared__ float hm[4], hl[4], ho[4][D];
@@ -53,9 +53,12 @@ __global__ void __launch_bounds__(QP_THREADS) qprep_kernel(const uint16_t* __res
   // The rows do not depend on this decode step, so their loads are issued before waiting on the previous kernel.
   const int hper = (ha.n_hot + NB - 1) / NB;
   const int h0 = sb * hper, h1 = min(ha.n_hot, h0 + hper);
-  const uint16_t* Khb = static_cast<const uint16_t*>(ha.K_hot) + ((int64_t)b * cfg.n_kv + g) * ha.n_hot * D + 4 * lane;
-  const uint16_t* Vhb = static_cast<const uint16_t*>(ha.V_hot) + ((int64_t)b * cfg.n_kv + g) * ha.n_hot * D + 4 * lane;
+  const uint16_t* Khb = static_cast<const uint16_t*>(ha.K_hot) + ((int64_t)b * cfg.n_kv + g) * ha.hot_rows * D + 4 * lane;
+  const uint16_t* Vhb = static_cast<const uint16_t*>(ha.V_hot) + ((int64_t)b * cfg.n_kv + g) * ha.hot_rows * D + 4 * lane;
   uint2 hk[HOT_RB], hv[HOT_RB];
+#ifdef PKV_DBG_QPREP_LATE
+  pdl_wait();
+#endif
 #pragma unroll
   for (int u = 0; u < HOT_RB; ++u) {
     const int r = h0 + warp + 4 * u;

@@ -11,6 +11,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -27,12 +28,11 @@ constexpr int RR_THREADS = 256;
 // nibble address, so a lookup is SHF + LOP3 + LDS [reg + imm] + FADD.
 constexpr int RT_ROWS = D;
 
-__global__ void __launch_bounds__(RR_THREADS) rerank_kernel(const uint8_t* __restrict__ rec, const int32_t* __restrict__ cand,
-                                                             const int32_t* __restrict__ sel,
-                                                             const float* __restrict__ rtab,
-                                                             const float* __restrict__ qnorm, int64_t cap, int n_q,
+__global__ void __launch_bounds__(RR_THREADS) rerank_kernel(const uint8_t* __restrict__ rec, const int32_t* cand,
+                                                             const int32_t* sel, const float* rtab,
+                                                             const float* qnorm, int64_t cap, int n_q,
                                                              int n_kv, int G, int64_t cand_stride, int64_t id_offset,
-                                                             float* __restrict__ est_out) {
+                                                             float* est_out) {
   phase_mark(K_RERANK, 0);
   cta_mark(K_RERANK, 1);
   __shared__ __align__(16) float T[RT_ROWS * 16];
@@ -265,7 +265,7 @@ __device__ __forceinline__ unsigned long long ckey(float e, int id) {
 }
 
 // Top-k of the `count` (estimate, id) pairs at es / ids, written in order to oi / oe (k entries, -1 padded).
-__device__ __forceinline__ void topk_select(const float* __restrict__ es, const int32_t* __restrict__ ids, int count,
+__device__ __forceinline__ void topk_select(const float* es, const int32_t* ids, int count,
                                             int k, int32_t* oi, float* oe) {
   extern __shared__ float ecache[];  // [BS_CACHE] estimates, then [BS_CACHE] ids
   int32_t* icache = reinterpret_cast<int32_t*>(ecache + BS_CACHE);
@@ -443,8 +443,8 @@ struct AttendEpi {  // gather + attention over the selected rows, merged with pr
 // nseg > 1 (very long lists, e.g. 1M-token contexts): CTA z takes candidates [z*BS_CACHE, (z+1)*BS_CACHE) and
 // writes its local top-k to slot z of out (slot stride seg_stride), to be merged by merge_kernel.
 template <bool ATTEND, bool SELECT = true>
-__global__ void __launch_bounds__(BS_THREADS) topk_kernel(const float* __restrict__ est, const int32_t* __restrict__ cand,
-                                                           const int32_t* __restrict__ sel, int n_q,
+__global__ void __launch_bounds__(BS_THREADS) topk_kernel(const float* est, const int32_t* cand,
+                                                           const int32_t* sel, int n_q,
                                                            int64_t cand_stride, int k, int out_stride,
                                                            int32_t* out_idx, float* out_est, AttendEpi ep,
                                                            int64_t seg_stride) {
@@ -624,9 +624,8 @@ struct SmemCand {  // radix fallback source: the CTA's cached slice
 };
 
 template <bool ATTEND>
-__global__ void __launch_bounds__(BS_THREADS) topk_cl_kernel(const float* __restrict__ est,
-                                                              const int32_t* __restrict__ cand,
-                                                              const int32_t* __restrict__ sel, int n_q,
+__global__ void __launch_bounds__(BS_THREADS) topk_cl_kernel(const float* est, const int32_t* cand,
+                                                              const int32_t* sel, int n_q,
                                                               int64_t cand_stride, int k, int out_stride,
                                                               int32_t* out_idx, float* out_est, AttendEpi ep,
                                                               int slice_cap) {
@@ -1012,8 +1011,8 @@ __global__ void __launch_bounds__(BS_THREADS) topk_cl_kernel(const float* __rest
   phase_mark(K_TOPK, 11);
 }
 
-__global__ void __launch_bounds__(TK_THREADS) merge_kernel(const float* __restrict__ all_est,
-                                                            const int32_t* __restrict__ all_idx, int P, int batch,
+__global__ void __launch_bounds__(TK_THREADS) merge_kernel(const float* all_est,
+                                                            const int32_t* all_idx, int P, int batch,
                                                             int n_q, int k, int32_t* out_idx, float* out_est,
                                                             int out_stride) {
   const int h = blockIdx.x, b = blockIdx.y;
@@ -1079,6 +1078,14 @@ cudaError_t launch_rerank(const pkv_index* ix, int64_t C_cap, int64_t id_offset,
   // Grid covers the candidates (one per thread pair): more resident threads than a one-wave grid whose threads
   // loop over several candidates, because each candidate is a dependent id -> record load chain.
   int64_t tiles = (C_cap + RR_THREADS / 2 - 1) / (RR_THREADS / 2);
+  static const int wave = [] {
+    const char* e = getenv("PKV_RR_WAVE");
+    return e ? atoi(e) : 0;
+  }();
+  if (wave > 0) {  // experiment: at most `wave` resident CTAs per SM, threads loop over candidates
+    const int64_t cap = std::max<int64_t>(1, (int64_t)ix->num_sms * wave / ((int64_t)ix->cfg.n_q_heads * ix->batch));
+    tiles = std::min(tiles, cap);
+  }
   if (tiles < 1) tiles = 1;
   dim3 grid((unsigned)tiles, ix->cfg.n_q_heads, ix->batch);
   ProfScope p_(K_RERANK, stream);

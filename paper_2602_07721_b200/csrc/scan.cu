@@ -95,8 +95,7 @@ __device__ __forceinline__ void scan_loop(uint4 (&row)[SCAN_UNROLL], const uint8
 
 template <int RES>
 __global__ void __launch_bounds__(SCAN_THREADS, 1)
-    scan_kernel(const uint8_t* __restrict__ ids, const uint32_t* __restrict__ lut_g, uint32_t* __restrict__ scores,
-                uint32_t* __restrict__ chunk_hist, int64_t cap, int64_t n, int64_t chunk, int G) {
+    scan_kernel(const uint8_t* __restrict__ ids, const uint32_t* lut_g, uint32_t* scores, uint32_t* chunk_hist, int64_t cap, int64_t n, int64_t chunk, int G) {
   extern __shared__ __align__(16) uint32_t smem[];
   uint32_t* lut = smem;
   uint32_t* hist = smem + LUT_WORDS;
@@ -108,6 +107,9 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1)
   phase_mark(K_SCAN, 0);
   // the centroid ids do not depend on the query: start streaming them before qprep has finished
   uint4 row[SCAN_UNROLL];
+#ifdef PKV_DBG_SCAN_LATE
+  pdl_wait();
+#endif
   load_rows<true>(row, ids_bh, (uint32_t)t_begin + (threadIdx.x >> 5) * 32 + (threadIdx.x & 31), (uint32_t)t_end);
   for (int i = threadIdx.x; i < SCAN_WARPS * GMAX * HB; i += SCAN_THREADS) hist[i] = 0u;
   pdl_wait();  // lookup table comes from qprep
@@ -186,9 +188,9 @@ constexpr int SEL_SMEM = 32 * 8 * 32 * 8;  // per-warp compaction lists
 // and then writes its chunk's candidates: two passes over the packed scores (L2), warp-level ballots,
 // one block scan of the per-warp counts (no per-tile block synchronisation).
 __global__ void __launch_bounds__(SEL_THREADS) select_kernel(
-    const uint32_t* __restrict__ chunk_hist, const uint32_t* __restrict__ all_hist, int P, int rank, int batch,
-    const uint32_t* __restrict__ scores, int64_t cap, int64_t n, int64_t chunk, int nchunks, int n_q, int n_kv,
-    int G, int64_t C, int64_t id_offset, int64_t cand_stride, int32_t* __restrict__ cand, int32_t* __restrict__ sel) {
+    const uint32_t* chunk_hist, const uint32_t* all_hist, int P, int rank, int batch, const uint32_t* scores,
+    int64_t cap, int64_t n, int64_t chunk, int nchunks, int n_q, int n_kv, int G, int64_t C, int64_t id_offset,
+    int64_t cand_stride, int32_t* cand, int32_t* sel) {
   phase_mark(K_SELECT, 0);
   cta_mark(K_SELECT, 1);
   __shared__ uint32_t Hg[GMAX][HB];   // global cumulative counts
@@ -523,8 +525,8 @@ cudaError_t launch_dbg_scores(const pkv_index* ix, int64_t n, uint8_t* out, cuda
   return cudaGetLastError();
 }
 
-__global__ void head_hist_kernel(const uint32_t* __restrict__ chunk_hist, int nchunks, int n_q, int n_kv, int G,
-                                 uint32_t* __restrict__ out) {
+__global__ void head_hist_kernel(const uint32_t* chunk_hist, int nchunks, int n_q, int n_kv, int G,
+                                 uint32_t* out) {
   const int h = blockIdx.x, b = blockIdx.y, bin = threadIdx.x;
   const int g = h / G, hh = h % G;
   const uint32_t* ch = chunk_hist + ((int64_t)(b * n_kv + g) * MAX_CHUNKS) * GMAX * HB + hh * HB;

@@ -10,7 +10,7 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpariskv.so")
+LIB_PATH = os.path.join(_HERE, f"libpariskv_{os.environ['PKV_LIB']}.so" if os.environ.get("PKV_LIB") else "libpariskv.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"libpariskv.so not built ({LIB_PATH}); run `python -m paper_2602_07721_b200.build`")
@@ -34,6 +34,11 @@ class Config(ctypes.Structure):
                 ("rot_rounds", ctypes.c_int32)]
 
 
+class StreamConfig(ctypes.Structure):
+    _fields_ = [("sink", ctypes.c_int32), ("local_size", ctypes.c_int32), ("update_size", ctypes.c_int32),
+                ("offload_host", ctypes.c_int32)]
+
+
 class RetrieveParams(ctypes.Structure):
     _fields_ = [("probes_T", ctypes.c_int32), ("n_cand", ctypes.c_int64), ("top_k", ctypes.c_int32),
                 ("dbg_scores", ctypes.c_void_p), ("dbg_cand", ctypes.c_void_p), ("dbg_est", ctypes.c_void_p),
@@ -54,6 +59,14 @@ _sigs = {
     "sparse_attend": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _i32, _vp, _vp, _i32, _f32, _vp, _vp, _vp],
     "retrieve_and_attend": [_vp, _vp, ctypes.POINTER(RetrieveParams), _vp, _vp, _i64, _i64, _i64, _vp, _vp, _i32, _f32,
                             _vp, _vp, _vp, _vp, _vp],
+    "retrieve_and_attend_rows": [_vp, _vp, ctypes.POINTER(RetrieveParams), _vp, _vp, _i64, _i64, _i64, _vp, _vp,
+                                 _i32, _i32, _f32, _vp, _vp, _vp, _vp, _vp],
+    "pkv_stream_create": [_vp, ctypes.POINTER(StreamConfig), ctypes.POINTER(_vp)],
+    "pkv_stream_destroy": [_vp],
+    "pkv_stream_prefill": [_vp, _vp, _vp, _i64, _i64, _i64, _i64, _vp],
+    "pkv_stream_decode": [_vp, _vp, _vp, _vp, ctypes.POINTER(RetrieveParams), _f32, _vp, _vp, _vp, _vp, _vp],
+    "pkv_stream_state": [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i32), ctypes.POINTER(_i32),
+                         ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp)],
     "pkv_index_export": [_vp, _i64, _i64, _vp, _vp, _vp, _vp],
     "pkv_nccl_unique_id": [_vp],
     "pkv_comm_init": [_vp, _vp, _i32, _i32, _i64],
@@ -287,6 +300,94 @@ def retrieve_and_attend(index: Index, q: torch.Tensor, K, V, top_k: int, K_hot=N
                                     _ptr(K_hot), _ptr(V_hot), n_hot, scale, _ptr(out_idx), _ptr(out_est), _ptr(out),
                                     _ptr(lse), _stream(stream)))
     return out_idx, out_est, out, lse
+
+
+class Stream:
+    """Four-region streaming KV cache of one layer (PAPER §4.2.3; include/pariskv.h pkv_stream_*):
+    Sink + Local + Update buffer on the GPU, older tokens indexed in `index` with their K/V in a store owned by
+    the stream (HBM, or pinned host memory read through UVA when offload_host)."""
+
+    def __init__(self, index: Index, sink: int = 16, local_size: int = 256, update_size: int = 512,
+                 offload_host: bool = False):
+        self.index = index
+        self.cfg = StreamConfig(sink, local_size, update_size, int(offload_host))
+        h = _vp()
+        _check(_lib.pkv_stream_create(index.handle, ctypes.byref(self.cfg), ctypes.byref(h)))
+        self.handle = h
+
+    def close(self):
+        if getattr(self, "handle", None) is not None and self.handle.value:
+            _lib.pkv_stream_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def prefill(self, K: torch.Tensor, V: torch.Tensor, stream=None):
+        """K, V bf16 [batch, n_kv, tokens, 128] (unit last stride, same strides)."""
+        sb, sh, st = _kv_strides(K)
+        assert _kv_strides(V) == (sb, sh, st)
+        _check(_lib.pkv_stream_prefill(self.handle, _ptr(K), _ptr(V), sb, sh, st, K.shape[2], _stream(stream)))
+
+    def decode(self, q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor, top_k: int, scale=None,
+               probes_T: int = 0, n_cand: int = 0, out_idx=None, out_est=None, out=None, lse=None, debug=None,
+               stream=None):
+        """One decode step: q bf16 [batch, n_q, 128]; k_new, v_new bf16 [batch, n_kv, 128] (contiguous).
+        probes_T / n_cand = 0: the schedule for the current retrieval length. Returns (idx, est, out, lse);
+        idx are retrieval-store positions (token = sink + idx)."""
+        ix = self.index
+        dev = q.device
+        assert k_new.is_contiguous() and v_new.is_contiguous() and q.is_contiguous()
+        if out_idx is None:
+            out_idx = torch.empty(ix.batch, ix.n_q, top_k, dtype=torch.int32, device=dev)
+        if out_est is None:
+            out_est = torch.empty(ix.batch, ix.n_q, top_k, dtype=torch.float32, device=dev)
+        if out is None:
+            out = torch.empty(ix.batch, ix.n_q, D, dtype=torch.bfloat16, device=dev)
+        if lse is None:
+            lse = torch.empty(ix.batch, ix.n_q, dtype=torch.float32, device=dev)
+        scale = 1.0 / np.sqrt(D) if scale is None else scale
+        p = RetrieveParams(probes_T, n_cand, top_k, None, None, None, None)
+        if debug is not None:  # dict of preallocated tensors: scores [b,q,n_after], cand/est [b,q,C], q_rot
+            p.dbg_scores = debug["scores"].data_ptr() if "scores" in debug else None
+            p.dbg_cand = debug["cand"].data_ptr() if "cand" in debug else None
+            p.dbg_est = debug["est"].data_ptr() if "est" in debug else None
+            p.dbg_q_rot = debug["q_rot"].data_ptr() if "q_rot" in debug else None
+        _check(_lib.pkv_stream_decode(self.handle, _ptr(q), _ptr(k_new), _ptr(v_new), ctypes.byref(p), scale,
+                                      _ptr(out_idx), _ptr(out_est), _ptr(out), _ptr(lse), _stream(stream)))
+        return out_idx, out_est, out, lse
+
+    def state(self):
+        """(n_retrieval, n_local, n_buffer)."""
+        n = _i64(0)
+        nl, nb = _i32(0), _i32(0)
+        _check(_lib.pkv_stream_state(self.handle, ctypes.byref(n), ctypes.byref(nl), ctypes.byref(nb), None, None,
+                                     None, None))
+        return int(n.value), int(nl.value), int(nb.value)
+
+    def views(self):
+        """Torch views of the retrieval store (K, V [batch, n_kv, capacity, 128]) and of the hot buffer
+        (K, V [batch, n_kv, sink + local_size + update_size, 128]) — for tests and diagnostics."""
+        ptrs = [_vp() for _ in range(4)]
+        _check(_lib.pkv_stream_state(self.handle, None, None, None, *[ctypes.byref(p) for p in ptrs]))
+        ix = self.index
+        rows = self.cfg.sink + self.cfg.local_size + self.cfg.update_size
+        shapes = [(ix.batch, ix.n_kv, ix.capacity, D)] * 2 + [(ix.batch, ix.n_kv, rows, D)] * 2
+        return tuple(_wrap_bf16(p.value, shp, ix.device) for p, shp in zip(ptrs, shapes))
+
+
+def _wrap_bf16(ptr: int, shape, device: int) -> torch.Tensor:
+    """Non-owning torch view of library-owned bf16 device memory (valid while its owner lives)."""
+    n = int(np.prod(shape))
+
+    class _Cuda:
+        __cuda_array_interface__ = {"shape": (n,), "typestr": "<i2", "data": (ptr, False), "version": 3}
+
+    with torch.cuda.device(device):
+        return torch.as_tensor(_Cuda(), device=f"cuda:{device}").view(torch.bfloat16).view(*shape)
 
 
 def nccl_unique_id() -> bytes:

@@ -77,3 +77,40 @@ def test_index_create_fails_cleanly_without_gpu(pkv):
     with pytest.raises(pkv.PkvError) as e:
         pkv.Index(cfg, 1, 1024)
     assert e.value.status in (pkv.PKV_ERR_CUDA, pkv.PKV_ERR_INVALID_ARG)
+
+
+def test_no_predecessor_output_read_before_griddepcontrol_wait(pkv):
+    """Programmatic dependent launch contract, checked on the SASS of the built kernels: before
+    griddepcontrol.wait (ACQBULK) a kernel may only load data no kernel of the decode chain writes — the
+    index's centroid ids (scan prefetch), the caller's hot rows (qprep, attend_partial) and the query (fused
+    top-k) — and may not store. A predecessor output read there (e.g. a const __restrict__ load the compiler
+    hoisted onto the non-coherent path) is a race that returns stale candidates."""
+    import importlib.util
+    import shutil
+    if shutil.which("cuobjdump") is None:
+        pytest.skip("cuobjdump not available")
+    spec = importlib.util.spec_from_file_location("check_pdl_sass", os.path.join(ROOT, "scripts", "check_pdl_sass.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    build_dir = os.path.join(ROOT, "paper_2602_07721_b200", "build")
+    res = {}
+    for f in ("qprep.cu.o", "scan.cu.o", "rerank.cu.o", "attend.cu.o"):
+        res.update(mod.prewait_loads(os.path.join(build_dir, f)))
+    assert len(res) >= 10, sorted(res)
+
+    def ops(v):
+        return [x.split()[1] if x.startswith("@") else x.split()[0] for x in v]
+
+    for name, v in res.items():
+        kinds = ops(v)
+        assert all(k.startswith("LDG") for k in kinds), (name, v)  # no stores / atomics before the wait
+        if "scan_kernel" in name:
+            assert set(kinds) <= {"LDG.E.NA.128.CONSTANT"} and len(kinds) <= 4, (name, v)  # centroid-id rows
+        elif "qprep_kernel" in name:
+            assert set(kinds) <= {"LDG.E.64"} and len(kinds) <= 16, (name, v)  # hot K/V rows only
+        elif "attend_partial_kernel" in name:
+            assert set(kinds) <= {"LDG.E.64"}, (name, v)  # query + hot rows
+        elif "topk_cl_kernelILb1" in name:
+            assert kinds in ([], ["LDG.E.64"]), (name, v)  # the query
+        else:
+            assert kinds == [], (name, v)
