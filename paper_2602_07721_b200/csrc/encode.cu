@@ -39,28 +39,32 @@ __device__ __forceinline__ void fwht128(T v[8], int lane16) {
 #pragma unroll
   for (int x = 1; x < 16; x <<= 1) {
     const bool upper = (lane16 & x) != 0;
+    const T sgn = upper ? T(-1) : T(1);  // upper: o - v, lower: v + o — one multiply-add either way
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       T o = shfl_x(v[i], x);
-      v[i] = upper ? (o - v[i]) : (v[i] + o);
+      v[i] = v[i] * sgn + o;
     }
   }
 }
 
+// Grid (ceil(count / 16), batch * n_kv): no integer division on the key index.
 __global__ void __launch_bounds__(256) encode_kernel(const uint16_t* __restrict__ K, int64_t sb, int64_t sh,
                                                      int64_t st, int64_t t0, int64_t count, int n_kv,
-                                                     int64_t cap, int64_t total, DevCfg cfg,
-                                                     uint8_t* __restrict__ ids, uint8_t* __restrict__ rec) {
+                                                     int64_t cap, DevCfg cfg, uint8_t* __restrict__ ids,
+                                                     uint8_t* __restrict__ rec) {
+  __shared__ float sL[8];  // magnitude levels: per-lane indexed (a divergent constant-bank read would serialise)
   const int lane16 = threadIdx.x & 15;
-  int64_t kk = (int64_t)blockIdx.x * KEYS_PER_BLOCK + (threadIdx.x >> 4);
-  const bool live = kk < total;
-  if (!live) kk = total - 1;  // keep the half-warp shuffles full; results discarded
-  const int64_t tt = kk % count;
-  const int64_t bh = kk / count;
-  const int64_t b = bh / n_kv, h = bh % n_kv;
+  int64_t tt = (int64_t)blockIdx.x * KEYS_PER_BLOCK + (threadIdx.x >> 4);
+  const bool live = tt < count;
+  if (!live) tt = count - 1;  // keep the half-warp shuffles full; results discarded
+  const int bh = blockIdx.y;
+  const int b = bh / n_kv, h = bh - b * n_kv;
   const int64_t t = t0 + tt;
 
   const uint4 raw = ldg_nc_v4(K + b * sb + h * sh + tt * st + 8 * lane16);
+  if (threadIdx.x < 8) sL[threadIdx.x] = cfg.levels[threadIdx.x];
+  __syncthreads();  // sL (while the key is in flight)
   const uint32_t w4[4] = {raw.x, raw.y, raw.z, raw.w};
   uint32_t e[8], mant[8], sgn[8];
   int emax = 0;
@@ -123,12 +127,18 @@ __global__ void __launch_bounds__(256) encode_kernel(const uint16_t* __restrict_
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const bool pos = y[i] >= 0.0;
+#ifdef PKV_ENC_LINEAR
+    uint32_t idx = 0;
+#pragma unroll
+    for (int t2 = 0; t2 < 7; ++t2) idx += (uint32_t)(sq[i] >= th[t2]);
+#else
     const bool b2 = sq[i] >= th[3];
     const double t1 = b2 ? th[5] : th[1];
     const bool b1 = sq[i] >= t1;
     const double t0v = b2 ? (b1 ? th[6] : th[4]) : (b1 ? th[2] : th[0]);
     const bool b0 = sq[i] >= t0v;
     uint32_t idx = 4u * b2 + 2u * b1 + (uint32_t)b0;
+#endif
     uint32_t sbit = pos ? 1u : 0u;
     if (degenerate) {  // AMB-7: encode(e_1)
       idx = (i == 0) ? 7u : 0u;
@@ -136,7 +146,7 @@ __global__ void __launch_bounds__(256) encode_kernel(const uint16_t* __restrict_
     }
     id |= (pos ? 1u : 0u) << i;
     code |= ((sbit << 3) | idx) << (4 * i);
-    const float L = cfg.levels[idx];
+    const float L = sL[idx];
     const float yf = (float)(y[i] * scale);
     dot = fmaf(sbit ? L : -L, yf, dot);
     vn2 = fmaf(L, L, vn2);
@@ -185,13 +195,11 @@ __global__ void export_kernel(const uint8_t* __restrict__ ids_in, const uint8_t*
 
 cudaError_t launch_encode(const pkv_index* ix, const void* K, int64_t sb, int64_t sh, int64_t st, int64_t t0,
                           int64_t count, cudaStream_t stream) {
-  const int64_t total = (int64_t)ix->batch * ix->cfg.n_kv_heads * count;
-  if (total == 0) return cudaSuccess;
-  const int64_t blocks = (total + KEYS_PER_BLOCK - 1) / KEYS_PER_BLOCK;
+  if (count <= 0) return cudaSuccess;
+  const dim3 grid((unsigned)((count + KEYS_PER_BLOCK - 1) / KEYS_PER_BLOCK), ix->batch * ix->cfg.n_kv_heads);
   ProfScope p_(K_ENCODE, stream);
-  encode_kernel<<<(unsigned)blocks, 256, 0, stream>>>(static_cast<const uint16_t*>(K), sb, sh, st, t0, count,
-                                                      ix->cfg.n_kv_heads, ix->cap, total, ix->dcfg, ix->ids,
-                                                      ix->rec);
+  encode_kernel<<<grid, 256, 0, stream>>>(static_cast<const uint16_t*>(K), sb, sh, st, t0, count,
+                                          ix->cfg.n_kv_heads, ix->cap, ix->dcfg, ix->ids, ix->rec);
   return cudaGetLastError();
 }
 
