@@ -23,6 +23,16 @@ __device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
 }
 
 // Plain (coherent) 16-byte load: used for UVA host memory and data written by earlier kernels.
+// Same load as an ordered (volatile) asm statement: stays where it is written, e.g. ahead of a barrier, so a
+// batch of independent loads is really in flight together (the compiler otherwise sinks them to their use).
+__device__ __forceinline__ uint4 ldg_nc_v4_early(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
 __device__ __forceinline__ uint4 ldg_v4(const void* p) {
   uint4 r;
   asm("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));

@@ -107,6 +107,88 @@ __global__ void __launch_bounds__(RR_THREADS) rerank_kernel(const uint8_t* __res
   cta_mark(K_RERANK, 0);
 }
 
+// CPT candidates per thread pair (candidate tile of PER_CTA*CPT per CTA): the per-CTA work (table staging,
+// pointers) is amortised over CPT candidates and their record loads are all in flight before the lookups.
+template <int CPT>
+__global__ void __launch_bounds__(RR_THREADS) rerank_cpt_kernel(const uint8_t* __restrict__ rec, const int32_t* cand,
+                                                                 const int32_t* sel, const float* rtab,
+                                                                 const float* qnorm, int64_t cap, int n_q, int n_kv,
+                                                                 int G, int64_t cand_stride, int64_t id_offset,
+                                                                 float* est_out) {
+  __shared__ __align__(16) float T[RT_ROWS * 16];
+  pdl_trigger();
+  pdl_wait();
+  const int h = blockIdx.y, b = blockIdx.z;
+  const int g = h / G;
+  const int64_t bhq = (int64_t)b * n_q + h;
+  constexpr int PER_CTA = RR_THREADS / 2;
+  const int32_t* cd = cand + bhq * cand_stride;
+  const int pos0 = blockIdx.x * (PER_CTA * CPT) + (threadIdx.x >> 1);
+  const int C_local = sel[bhq * SEL_STRIDE + 2];
+  int32_t cid[CPT];
+#pragma unroll
+  for (int u = 0; u < CPT; ++u) {
+    const int pos = pos0 + u * PER_CTA;
+    cid[u] = pos < cand_stride ? cd[pos] : 0;  // speculative (inside the capacity); used only if pos < C_local
+  }
+  const float4* tsrc = reinterpret_cast<const float4*>(rtab + bhq * D * 16);
+  float4 tv[D * 4 / RR_THREADS];
+#pragma unroll
+  for (int u = 0; u < D * 4 / RR_THREADS; ++u) tv[u] = tsrc[threadIdx.x + u * RR_THREADS];
+  const float qn = qnorm[bhq];
+  if (blockIdx.x * (PER_CTA * CPT) >= C_local) return;
+#pragma unroll
+  for (int u = 0; u < D * 4 / RR_THREADS; ++u) {  // coordinate c -> physical row 2(c%64)+c/64
+    const int i = threadIdx.x + u * RR_THREADS;
+    const int c = i >> 2;
+    reinterpret_cast<float4*>(T)[(2 * (c & 63) + (c >> 6)) * 4 + (i & 3)] = tv[u];
+  }
+  const int half = threadIdx.x & 1;
+  const uint8_t* rec_bh = rec + ((int64_t)b * n_kv + g) * cap * REC + 32 * half;
+  uint4 cr[CPT][2], wr[CPT][2];
+#pragma unroll
+  for (int u = 0; u < CPT; ++u) {
+    cr[u][0] = cr[u][1] = wr[u][0] = wr[u][1] = make_uint4(0, 0, 0, 0);
+    if (pos0 + u * PER_CTA < C_local) {
+      const uint8_t* r = rec_bh + ((int64_t)cid[u] - id_offset) * REC;
+      cr[u][0] = ldg_nc_v4_early(r);
+      cr[u][1] = ldg_nc_v4_early(r + 16);
+      wr[u][0] = ldg_nc_v4_early(r + 64);
+      wr[u][1] = ldg_nc_v4_early(r + 80);
+    }
+  }
+  __syncthreads();
+  const char* Tb = reinterpret_cast<const char*>(T);
+  const uint32_t hoff = half ? 64u : 0u;
+  float est[CPT];
+#pragma unroll
+  for (int u = 0; u < CPT; ++u) {
+    const uint32_t cw[8] = {cr[u][0].x, cr[u][0].y, cr[u][0].z, cr[u][0].w,
+                            cr[u][1].x, cr[u][1].y, cr[u][1].z, cr[u][1].w};
+    const uint32_t ww[8] = {wr[u][0].x, wr[u][0].y, wr[u][0].z, wr[u][0].w,
+                            wr[u][1].x, wr[u][1].y, wr[u][1].z, wr[u][1].w};
+    float e = 0.f;
+#pragma unroll
+    for (int sb = 0; sb < 8; ++sb) {
+      float dot = *reinterpret_cast<const float*>(Tb + (8 * sb) * 128 + (((cw[sb] << 2) & 0x3cu) | hoff));
+#pragma unroll
+      for (int j = 1; j < 8; ++j) {
+        const uint32_t off = (cw[sb] >> (4 * j - 2)) & 0x3cu;
+        dot += *reinterpret_cast<const float*>(Tb + (8 * sb + j) * 128 + (off | hoff));
+      }
+      e = fmaf(__uint_as_float(ww[sb]), dot, e);
+    }
+    est[u] = e;
+  }
+  float* eo = est_out + bhq * cand_stride;
+#pragma unroll
+  for (int u = 0; u < CPT; ++u) {
+    const float e = est[u] + __shfl_xor_sync(0xffffffffu, est[u], 1);
+    const int pos = pos0 + u * PER_CTA;
+    if (!half && pos < C_local) eo[pos] = e * qn;
+  }
+}
+
 // ---------------------------------------------------------------- radix top-k
 constexpr int TK_THREADS = 1024;
 constexpr int TK_CACHE = 12288;  // composite keys cached in (dynamic) smem when the list is short enough
@@ -1075,6 +1157,19 @@ cudaError_t init_rerank_attrs() {
 
 cudaError_t launch_rerank(const pkv_index* ix, int64_t C_cap, int64_t id_offset, cudaStream_t stream) {
   const Workspace* ws = ix->ws;
+  static const int cpt = [] {  // candidates per thread pair: 2 measured best at 128K (PKV_RR_CPT=1|2|4 to compare)
+    const char* e = getenv("PKV_RR_CPT");
+    return e ? atoi(e) : 2;
+  }();
+  if (cpt == 2 || cpt == 4) {
+    const int64_t per = (int64_t)(RR_THREADS / 2) * cpt;
+    const dim3 grid((unsigned)std::max<int64_t>(1, (C_cap + per - 1) / per), ix->cfg.n_q_heads, ix->batch);
+    ProfScope p_(K_RERANK, stream);
+    auto kern = cpt == 2 ? rerank_cpt_kernel<2> : rerank_cpt_kernel<4>;
+    return pdl_launch(kern, grid, dim3(RR_THREADS), 0, stream, (const uint8_t*)ix->rec, (const int32_t*)ws->cand,
+                      (const int32_t*)ws->sel, (const float*)ws->rtab, (const float*)ws->qnorm, ix->cap,
+                      ix->cfg.n_q_heads, ix->cfg.n_kv_heads, ix->dcfg.G, ws->cap, id_offset, ws->est);
+  }
   // Grid covers the candidates (one per thread pair): more resident threads than a one-wave grid whose threads
   // loop over several candidates, because each candidate is a dependent id -> record load chain.
   int64_t tiles = (C_cap + RR_THREADS / 2 - 1) / (RR_THREADS / 2);
