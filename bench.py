@@ -140,6 +140,7 @@ def run_ours(args):
     n_loc = hi - lo
     T, C = pkv.schedule(n, TOP_K)
     cfg = pkv.config_init(N_Q, N_KV, synth.rotation_sign_bits())
+    cfg.w_fp16 = 1 if args.w16 else 0  # AMB-20 variant: 96-byte records with fp16 weights
     L = args.layers
 
     # ---- synthetic inputs, per layer distinct indices (> L2 touched per step) ----
@@ -333,7 +334,7 @@ def run_ours(args):
         "select": batch * N_KV * n_loc * 4 + batch * N_Q * min(C, n_loc) * 4,
         # fused RSQ-IP rerank: reads the candidate id and gathers its 128 B record, writes the estimate (4 B),
         # per (candidate, query head)
-        "rerank": batch * N_Q * min(C, n_loc) * (4 + 128 + 4),
+        "rerank": batch * N_Q * min(C, n_loc) * (4 + (96 if args.w16 else 128) + 4),
         # fused path: top-k over (est, id) pairs + gather of the k selected K/V rows (512 B per row and head);
         # two-call path: top-k only
         "topk": batch * N_Q * min(C, n_loc) * 8 + (batch * N_Q * TOP_K * 512 if fused else 0),
@@ -375,6 +376,7 @@ def run_ours(args):
                        "hot_rows": n_hot, "top_k": TOP_K, "probes_T": T, "n_cand": C, "layers": L,
                        "parallelism": f"seq-shard{world}" if world > 1 else "single",
                        "l2": "inputs > L2: 32 layer-distinct indices + K/V touched per step",
+                       "rerank_weights": "fp16 (96 B records)" if args.w16 else "fp32 (128 B records)",
                        "cuda_graph": use_graph},
             "roofline": roof,
             "scan_gbs": scan_gbs,
@@ -498,6 +500,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--w16", action="store_true", help="fp16 rerank weights (96-byte records, AMB-20 / SURVEY f2)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup) if args.impl == "ours" else args.warmup
     if args.impl == "reference":

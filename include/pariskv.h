@@ -74,6 +74,11 @@ typedef struct {
   double mag_mid_sq[7];              /* M_t = ((L_{t-1}+L_t)/2)^2 in fp64, exact from the fp32 levels     */
   uint8_t rot_sign[PKV_HEAD_DIM];    /* SRHT sign diagonal s_j: 0 -> +1, 1 -> -1 (AMB-1)          */
   int32_t rot_rounds;                /* 1 (only value supported)                                         */
+  int32_t w_fp16;                    /* rerank weight precision (AMB-20): 0 = fp32 w' in a */
+                                     /* 128-byte record (default); 1 = fp16 w' with a per-key power-of-two */
+                                     /* scale 2^E (E in [-126,126], kept in the 16 free sign bits) in a    */
+                                     /* 96-byte record. Estimates then carry an extra relative error of at */
+                                     /* most 2^-11 per subspace term (AMB-20)                */
 } pkv_config;
 
 /* Fill cfg with the paper defaults: D=128, B=16, m=8, 6 tiers {6..1}, Prop. 1 levels for m=8 computed on

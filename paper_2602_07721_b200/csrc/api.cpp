@@ -67,6 +67,7 @@ pkv_status validate_config(const pkv_config* c) {
   for (int i = 0; i < 8; ++i)
     if (!(c->mag_levels[i] > 0.f) || (i && !(c->mag_levels[i] > c->mag_levels[i - 1])) || !(c->mag_levels[i] < 1.f))
       return set_error(PKV_ERR_INVALID_ARG, "magnitude levels must be increasing in (0,1)");
+  if (c->w_fp16 != 0 && c->w_fp16 != 1) return set_error(PKV_ERR_INVALID_ARG, "w_fp16 must be 0 or 1");
   return PKV_OK;
 }
 
@@ -82,6 +83,8 @@ DevCfg make_devcfg(const pkv_config& c) {
   for (int i = 0; i < 7; ++i) d.mid_sq[i] = c.mag_mid_sq[i];
   for (int j = 0; j < PKV_HEAD_DIM; ++j)
     if (c.rot_sign[j]) d.sign_mask[j >> 5] |= 1u << (j & 31);
+  d.w16 = c.w_fp16;
+  d.rec_bytes = c.w_fp16 ? 96 : REC;
   return d;
 }
 
@@ -251,7 +254,7 @@ pkv_status pkv_index_create(const pkv_config* cfg, int32_t batch, int64_t capaci
   cudaDeviceGetAttribute(&ix->smem_reserved, cudaDevAttrReservedSharedMemoryPerBlock, device);
   const size_t units = (size_t)batch * cfg->n_kv_heads;
   cudaError_t e = cudaMalloc(&ix->ids, units * capacity * NB);
-  if (e == cudaSuccess) e = cudaMalloc(&ix->rec, units * capacity * REC);
+  if (e == cudaSuccess) e = cudaMalloc(&ix->rec, units * capacity * ix->dcfg.rec_bytes);
   if (e != cudaSuccess) {
     cudaFree(ix->ids);
     delete ix;

@@ -9,6 +9,8 @@
 //   midpoint rule y_j^2 >= M_t S_b on the Prop. 1 levels (AMB-5) — the fp64 op sequence of the oracle.
 //   w'_b = w_b / ||sign*L[idx]|| = S_b / (sqrt(128) <sign*L[idx], y_b>)  (Eq. 7, 9 with AMB-6; alpha clamp 1e-3)
 // Bytes per key: 256 in (bf16 K), 144 out (16 ids + 64 nibbles + 64 w'). HBM-bound.
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 
 namespace pkv {
@@ -168,18 +170,32 @@ __global__ void __launch_bounds__(256) encode_kernel(const uint16_t* __restrict_
     const uint32_t o = __shfl_sync(0xffffffffu, id, (int)((4 * q + j + t) & 15), 16);
     idw |= (o & 0xffu) << (8 * j);
   }
+  // fp16 weights (AMB-20 variant): w'_b = h_b * 2^E with one exponent per key, E = floor(log2 max_b w'_b) - 14
+  // so that every h_b < 2^15 is a normal fp16 down to max * 2^-28; bit (b mod 8) of E (8-bit two's
+  // complement) rides in the otherwise-zero sign bit of h_b, so each half of the record decodes E alone.
+  uint32_t hbits = 0;
+  if (cfg.w16) {
+    float m = wprime;
+#pragma unroll
+    for (int x = 1; x < 16; x <<= 1) m = fmaxf(m, shfl_x(m, x));
+    int E = (m > 0.f) ? ((__float_as_int(m) >> 23) & 0xff) - 127 - 14 : 0;
+    E = max(-126, min(126, E));
+    const float down = __int_as_float((127 - E) << 23);  // 2^-E, exact scaling
+    hbits = (uint32_t)__half_as_ushort(__float2half_rn(wprime * down)) | ((((uint32_t)E >> (lane16 & 7)) & 1u) << 15);
+  }
   if (live) {
     const int64_t row = (b * n_kv + h) * cap + t;
     if (lane16 < 4) reinterpret_cast<uint32_t*>(ids + row * NB)[lane16] = idw;
-    uint8_t* r = rec + row * REC;
+    uint8_t* r = rec + row * cfg.rec_bytes;
     reinterpret_cast<uint32_t*>(r)[lane16] = code;
-    reinterpret_cast<float*>(r + 64)[lane16] = wprime;
+    if (cfg.w16) reinterpret_cast<uint16_t*>(r + 64)[lane16] = (uint16_t)hbits;
+    else reinterpret_cast<float*>(r + 64)[lane16] = wprime;
   }
 }
 
 __global__ void export_kernel(const uint8_t* __restrict__ ids_in, const uint8_t* __restrict__ rec_in, int64_t start,
-                              int64_t count, int n_kv, int64_t cap, int64_t total, uint8_t* ids, uint8_t* codes,
-                              float* w) {
+                              int64_t count, int n_kv, int64_t cap, int64_t total, int w16, int rec_bytes,
+                              uint8_t* ids, uint8_t* codes, float* w) {
   const int64_t kk = (int64_t)blockIdx.x * 16 + (threadIdx.x >> 4);
   const int s = threadIdx.x & 15;
   if (kk >= total) return;
@@ -187,8 +203,20 @@ __global__ void export_kernel(const uint8_t* __restrict__ ids_in, const uint8_t*
   const int64_t t = start + i;
   const int64_t row = bh * cap + t;
   if (ids) ids[kk * NB + s] = ids_in[row * NB + ((s - t) & 15)];
-  if (codes) reinterpret_cast<uint32_t*>(codes + kk * 64)[s] = reinterpret_cast<const uint32_t*>(rec_in + row * REC)[s];
-  if (w) w[kk * NB + s] = reinterpret_cast<const float*>(rec_in + row * REC + 64)[s];
+  const uint8_t* r = rec_in + row * rec_bytes;
+  if (codes) reinterpret_cast<uint32_t*>(codes + kk * 64)[s] = reinterpret_cast<const uint32_t*>(r)[s];
+  if (w) {
+    if (w16) {  // h_b * 2^E, E from the sign bits of the 8 halves of this half of the record
+      const uint16_t* hw = reinterpret_cast<const uint16_t*>(r + 64) + (s & 8);
+      uint32_t e8 = 0;
+      for (int i = 0; i < 8; ++i) e8 |= (uint32_t)(hw[i] >> 15) << i;
+      const int E = (int)(int8_t)e8;
+      const float hv = __half2float(__ushort_as_half((unsigned short)(hw[s & 7] & 0x7fffu)));
+      w[kk * NB + s] = hv * __int_as_float((127 + E) << 23);
+    } else {
+      w[kk * NB + s] = reinterpret_cast<const float*>(r + 64)[s];
+    }
+  }
 }
 
 }  // namespace
@@ -209,8 +237,8 @@ cudaError_t launch_export(const pkv_index* ix, int64_t start, int64_t count, uin
   if (total == 0) return cudaSuccess;
   ProfScope p_(K_EXPORT, stream);
   export_kernel<<<(unsigned)((total + 15) / 16), 256, 0, stream>>>(ix->ids, ix->rec, start, count,
-                                                                   ix->cfg.n_kv_heads, ix->cap, total, ids,
-                                                                   codes, w);
+                                                                   ix->cfg.n_kv_heads, ix->cap, total,
+                                                                   ix->dcfg.w16, ix->dcfg.rec_bytes, ids, codes, w);
   return cudaGetLastError();
 }
 

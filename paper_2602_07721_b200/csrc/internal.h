@@ -32,6 +32,8 @@ struct DevCfg {
   float levels[8];
   double mid_sq[7];
   unsigned int sign_mask[4];  // bit d of word d/32 = rot_sign[d]
+  int w16;                    // 1: fp16 weights + per-key exponent (96-byte records), 0: fp32 (128-byte)
+  int rec_bytes;              // record stride: 96 or 128
 };
 
 struct Workspace {
@@ -76,7 +78,7 @@ struct pkv_index {
   int64_t cap = 0;
   int64_t n = 0;
   uint8_t* ids = nullptr;   // [batch][n_kv][cap][16]; row of key t rotated left by (t mod 16) bytes
-  uint8_t* rec = nullptr;   // [batch][n_kv][cap][128]
+  uint8_t* rec = nullptr;   // [batch][n_kv][cap][rec_bytes]: 64 B nibbles + 16 x fp32 w' (or 16 x fp16 w')
   pkv::Workspace* ws = nullptr;
   pkv::Comm* comm = nullptr;
   int rank = 0, world = 1;

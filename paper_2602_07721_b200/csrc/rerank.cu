@@ -9,6 +9,7 @@
 //                the k winners are then bitonic-sorted descending. Also used to merge the ranks' local top-k
 //                lists when sequence-sharded.
 #include <cooperative_groups.h>
+#include <cuda_fp16.h>
 
 #include <algorithm>
 #include <cstdlib>
@@ -28,93 +29,17 @@ constexpr int RR_THREADS = 256;
 // nibble address, so a lookup is SHF + LOP3 + LDS [reg + imm] + FADD.
 constexpr int RT_ROWS = D;
 
-__global__ void __launch_bounds__(RR_THREADS) rerank_kernel(const uint8_t* __restrict__ rec, const int32_t* cand,
-                                                             const int32_t* sel, const float* rtab,
-                                                             const float* qnorm, int64_t cap, int n_q,
-                                                             int n_kv, int G, int64_t cand_stride, int64_t id_offset,
-                                                             float* est_out) {
-  phase_mark(K_RERANK, 0);
-  cta_mark(K_RERANK, 1);
-  __shared__ __align__(16) float T[RT_ROWS * 16];
-  pdl_trigger();
-  pdl_wait();
-  phase_mark(K_RERANK, 1);
-  const int h = blockIdx.y, b = blockIdx.z;
-  const int g = h / G;
-  const int64_t bhq = (int64_t)b * n_q + h;
-  constexpr int PER_CTA = RR_THREADS / 2;
-  const int32_t* cd = cand + bhq * cand_stride;
-  int pos = blockIdx.x * PER_CTA + (threadIdx.x >> 1);
-  // one round of independent loads: candidate count, this thread's candidate id (speculative: pos < capacity),
-  // its share of the query table, ||q||
-  const int C_local = sel[bhq * SEL_STRIDE + 2];
-  const int32_t cid0 = pos < cand_stride ? cd[pos] : 0;
-  const float4* tsrc = reinterpret_cast<const float4*>(rtab + bhq * D * 16);
-  float4 tv[D * 4 / RR_THREADS];
-#pragma unroll
-  for (int u = 0; u < D * 4 / RR_THREADS; ++u) tv[u] = tsrc[threadIdx.x + u * RR_THREADS];
-  const float qn = qnorm[bhq];
-  if ((int64_t)blockIdx.x * PER_CTA >= C_local) return;
-#pragma unroll
-  for (int u = 0; u < D * 4 / RR_THREADS; ++u) {  // 4 float4 per row; coordinate c -> physical row 2(c%64)+c/64
-    const int i = threadIdx.x + u * RR_THREADS;
-    const int c = i >> 2;
-    reinterpret_cast<float4*>(T)[(2 * (c & 63) + (c >> 6)) * 4 + (i & 3)] = tv[u];
-  }
-  const uint8_t* rec_bh = rec + ((int64_t)b * n_kv + g) * cap * REC;
-  float* eo = est_out + bhq * cand_stride;
-  const int half = threadIdx.x & 1;
-  const char* Tb = reinterpret_cast<const char*>(T);
-  const uint32_t hoff = half ? 64u : 0u;
-  const unsigned pair_mask = 3u << ((threadIdx.x & 31) & ~1);
-  // the first candidate's record loads are issued before the table is published (__syncthreads)
-  uint4 c0, c1, w0, w1;
-  if (pos < C_local) {
-    const uint8_t* r = rec_bh + ((int64_t)cid0 - id_offset) * REC + 32 * half;
-    c0 = ldg_nc_v4(r);
-    c1 = ldg_nc_v4(r + 16);
-    w0 = ldg_nc_v4(r + 64);
-    w1 = ldg_nc_v4(r + 80);
-  }
-  __syncthreads();
-  for (; pos < C_local; pos += gridDim.x * PER_CTA) {
-  phase_mark(K_RERANK, 2);
-    const uint32_t cw[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
-    const uint32_t ww[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-    const int nxt = pos + gridDim.x * PER_CTA;
-    if (nxt < C_local) {  // prefetch the next candidate of this thread (rare: grids cover C in one pass)
-      const uint8_t* r = rec_bh + ((int64_t)cd[nxt] - id_offset) * REC + 32 * half;
-      c0 = ldg_nc_v4(r);
-      c1 = ldg_nc_v4(r + 16);
-      w0 = ldg_nc_v4(r + 64);
-      w1 = ldg_nc_v4(r + 80);
-    }
-    float est = 0.f;
-#pragma unroll
-    for (int sb = 0; sb < 8; ++sb) {
-      float dot = 0.f;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const uint32_t off = (j == 0 ? (cw[sb] << 2) : (cw[sb] >> (4 * j - 2))) & 0x3cu;
-        dot += *reinterpret_cast<const float*>(Tb + (8 * sb + j) * 128 + (off | hoff));
-      }
-      est = fmaf(__uint_as_float(ww[sb]), dot, est);
-    }
-    est += __shfl_xor_sync(pair_mask, est, 1);
-    if (!half) eo[pos] = est * qn;
-  }
-  phase_mark(K_RERANK, 3);
-  cta_mark(K_RERANK, 0);
-}
-
 // CPT candidates per thread pair (candidate tile of PER_CTA*CPT per CTA): the per-CTA work (table staging,
 // pointers) is amortised over CPT candidates and their record loads are all in flight before the lookups.
-template <int CPT>
+// W16: records of 96 bytes with fp16 weights h_b and a per-key exponent E in their sign bits (encode.cu):
+// each thread of the pair reads its 32 B of nibbles + 16 B of halves and decodes E from its own 8 halves.
+template <int CPT, bool W16>
 __global__ void __launch_bounds__(RR_THREADS) rerank_cpt_kernel(const uint8_t* __restrict__ rec, const int32_t* cand,
                                                                  const int32_t* sel, const float* rtab,
                                                                  const float* qnorm, int64_t cap, int n_q, int n_kv,
                                                                  int G, int64_t cand_stride, int64_t id_offset,
                                                                  float* est_out) {
+  constexpr int RB = W16 ? 96 : REC;  // record stride
   __shared__ __align__(16) float T[RT_ROWS * 16];
   pdl_trigger();
   pdl_wait();
@@ -144,17 +69,21 @@ __global__ void __launch_bounds__(RR_THREADS) rerank_cpt_kernel(const uint8_t* _
     reinterpret_cast<float4*>(T)[(2 * (c & 63) + (c >> 6)) * 4 + (i & 3)] = tv[u];
   }
   const int half = threadIdx.x & 1;
-  const uint8_t* rec_bh = rec + ((int64_t)b * n_kv + g) * cap * REC + 32 * half;
+  const uint8_t* rec_bh = rec + ((int64_t)b * n_kv + g) * cap * RB + 32 * half;
   uint4 cr[CPT][2], wr[CPT][2];
 #pragma unroll
   for (int u = 0; u < CPT; ++u) {
     cr[u][0] = cr[u][1] = wr[u][0] = wr[u][1] = make_uint4(0, 0, 0, 0);
     if (pos0 + u * PER_CTA < C_local) {
-      const uint8_t* r = rec_bh + ((int64_t)cid[u] - id_offset) * REC;
+      const uint8_t* r = rec_bh + ((int64_t)cid[u] - id_offset) * RB;
       cr[u][0] = ldg_nc_v4_early(r);
       cr[u][1] = ldg_nc_v4_early(r + 16);
-      wr[u][0] = ldg_nc_v4_early(r + 64);
-      wr[u][1] = ldg_nc_v4_early(r + 80);
+      if (W16) {
+        wr[u][0] = ldg_nc_v4_early(r + 64 - 16 * half);  // halves of subspaces 8*half .. 8*half+7
+      } else {
+        wr[u][0] = ldg_nc_v4_early(r + 64);
+        wr[u][1] = ldg_nc_v4_early(r + 80);
+      }
     }
   }
   __syncthreads();
@@ -165,8 +94,22 @@ __global__ void __launch_bounds__(RR_THREADS) rerank_cpt_kernel(const uint8_t* _
   for (int u = 0; u < CPT; ++u) {
     const uint32_t cw[8] = {cr[u][0].x, cr[u][0].y, cr[u][0].z, cr[u][0].w,
                             cr[u][1].x, cr[u][1].y, cr[u][1].z, cr[u][1].w};
-    const uint32_t ww[8] = {wr[u][0].x, wr[u][0].y, wr[u][0].z, wr[u][0].w,
-                            wr[u][1].x, wr[u][1].y, wr[u][1].z, wr[u][1].w};
+    uint32_t ww[8] = {wr[u][0].x, wr[u][0].y, wr[u][0].z, wr[u][0].w,
+                      wr[u][1].x, wr[u][1].y, wr[u][1].z, wr[u][1].w};
+    float escale = 1.f;
+    if (W16) {
+      const uint32_t h4[4] = {wr[u][0].x, wr[u][0].y, wr[u][0].z, wr[u][0].w};
+      uint32_t e8 = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) e8 |= (((h4[i] >> 15) & 1u) << (2 * i)) | (((h4[i] >> 31) & 1u) << (2 * i + 1));
+      escale = __int_as_float((127 + (int)(int8_t)e8) << 23);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&h4[i]));
+        ww[2 * i] = __float_as_uint(fabsf(f.x));
+        ww[2 * i + 1] = __float_as_uint(fabsf(f.y));
+      }
+    }
     float e = 0.f;
 #pragma unroll
     for (int sb = 0; sb < 8; ++sb) {
@@ -178,7 +121,7 @@ __global__ void __launch_bounds__(RR_THREADS) rerank_cpt_kernel(const uint8_t* _
       }
       e = fmaf(__uint_as_float(ww[sb]), dot, e);
     }
-    est[u] = e;
+    est[u] = W16 ? e * escale : e;
   }
   float* eo = est_out + bhq * cand_stride;
 #pragma unroll
@@ -1157,37 +1100,21 @@ cudaError_t init_rerank_attrs() {
 
 cudaError_t launch_rerank(const pkv_index* ix, int64_t C_cap, int64_t id_offset, cudaStream_t stream) {
   const Workspace* ws = ix->ws;
-  static const int cpt = [] {  // candidates per thread pair: 2 measured best at 128K (PKV_RR_CPT=1|2|4 to compare)
+  static const int cpt_env = [] {  // candidates per thread pair: 2 measured best at 128K (PKV_RR_CPT=1|2|4)
     const char* e = getenv("PKV_RR_CPT");
     return e ? atoi(e) : 2;
   }();
-  if (cpt == 2 || cpt == 4) {
-    const int64_t per = (int64_t)(RR_THREADS / 2) * cpt;
-    const dim3 grid((unsigned)std::max<int64_t>(1, (C_cap + per - 1) / per), ix->cfg.n_q_heads, ix->batch);
-    ProfScope p_(K_RERANK, stream);
-    auto kern = cpt == 2 ? rerank_cpt_kernel<2> : rerank_cpt_kernel<4>;
-    return pdl_launch(kern, grid, dim3(RR_THREADS), 0, stream, (const uint8_t*)ix->rec, (const int32_t*)ws->cand,
-                      (const int32_t*)ws->sel, (const float*)ws->rtab, (const float*)ws->qnorm, ix->cap,
-                      ix->cfg.n_q_heads, ix->cfg.n_kv_heads, ix->dcfg.G, ws->cap, id_offset, ws->est);
-  }
-  // Grid covers the candidates (one per thread pair): more resident threads than a one-wave grid whose threads
-  // loop over several candidates, because each candidate is a dependent id -> record load chain.
-  int64_t tiles = (C_cap + RR_THREADS / 2 - 1) / (RR_THREADS / 2);
-  static const int wave = [] {
-    const char* e = getenv("PKV_RR_WAVE");
-    return e ? atoi(e) : 0;
-  }();
-  if (wave > 0) {  // experiment: at most `wave` resident CTAs per SM, threads loop over candidates
-    const int64_t cap = std::max<int64_t>(1, (int64_t)ix->num_sms * wave / ((int64_t)ix->cfg.n_q_heads * ix->batch));
-    tiles = std::min(tiles, cap);
-  }
-  if (tiles < 1) tiles = 1;
-  dim3 grid((unsigned)tiles, ix->cfg.n_q_heads, ix->batch);
+  const int cpt = (cpt_env == 1 || cpt_env == 4) ? cpt_env : 2;
+  const int64_t per = (int64_t)(RR_THREADS / 2) * cpt;
+  const dim3 grid((unsigned)std::max<int64_t>(1, (C_cap + per - 1) / per), ix->cfg.n_q_heads, ix->batch);
   ProfScope p_(K_RERANK, stream);
-  return pdl_launch(rerank_kernel, grid, dim3(RR_THREADS), 0, stream, (const uint8_t*)ix->rec,
-                    (const int32_t*)ws->cand, (const int32_t*)ws->sel, (const float*)ws->rtab,
-                    (const float*)ws->qnorm, ix->cap, ix->cfg.n_q_heads, ix->cfg.n_kv_heads, ix->dcfg.G, ws->cap,
-                    id_offset, ws->est);
+  auto kern = ix->dcfg.w16 ? (cpt == 1 ? rerank_cpt_kernel<1, true> : cpt == 2 ? rerank_cpt_kernel<2, true>
+                                                                              : rerank_cpt_kernel<4, true>)
+                           : (cpt == 1 ? rerank_cpt_kernel<1, false> : cpt == 2 ? rerank_cpt_kernel<2, false>
+                                                                               : rerank_cpt_kernel<4, false>);
+  return pdl_launch(kern, grid, dim3(RR_THREADS), 0, stream, (const uint8_t*)ix->rec, (const int32_t*)ws->cand,
+                    (const int32_t*)ws->sel, (const float*)ws->rtab, (const float*)ws->qnorm, ix->cap,
+                    ix->cfg.n_q_heads, ix->cfg.n_kv_heads, ix->dcfg.G, ws->cap, id_offset, ws->est);
 }
 
 cudaError_t launch_topk(const pkv_index* ix, int64_t C_cap, int k, int32_t* out_idx, float* out_est,

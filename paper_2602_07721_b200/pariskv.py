@@ -31,7 +31,7 @@ class Config(ctypes.Structure):
                 ("n_q_heads", ctypes.c_int32), ("n_kv_heads", ctypes.c_int32), ("n_tiers", ctypes.c_int32),
                 ("tier_bonus", ctypes.c_int32 * 8), ("mag_levels", ctypes.c_float * 8),
                 ("mag_mid_sq", ctypes.c_double * 7), ("rot_sign", ctypes.c_uint8 * 128),
-                ("rot_rounds", ctypes.c_int32)]
+                ("rot_rounds", ctypes.c_int32), ("w_fp16", ctypes.c_int32)]
 
 
 class StreamConfig(ctypes.Structure):

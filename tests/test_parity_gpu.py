@@ -11,7 +11,8 @@ import torch
 
 import synth
 from oracle import attention, coarse, pipeline, sharded
-from tests.gpu_helpers import (ATT_ABS, SB, bf16_f64, check_encode, check_topk, oracle_meta, oracle_retrieval)
+from tests.gpu_helpers import (ATT_ABS, SB, bf16_f64, check_encode, check_topk, oracle_meta, oracle_retrieval,
+                               w16_bound)
 
 pytestmark = pytest.mark.gpu
 
@@ -52,11 +53,12 @@ def run_and_check(pkv, K, q, V, k, T=None, C=None, n_hot=0, check_all_heads=True
     ids_g, codes_g, w_g = [t.cpu().numpy() for t in ix.export()]
     torch.cuda.synchronize()
     Tn, Cn = dbg["T"], dbg["C"]
+    w16 = bool(cfg.w_fp16)
     for b in range(batch):
         for g in range(n_kv):
             Kf = bf16_f64(K[b, g])
             meta = oracle_meta(Kf)
-            check_encode(ids_g[b, g], codes_g[b, g], w_g[b, g], meta)
+            check_encode(ids_g[b, g], codes_g[b, g], w_g[b, g], meta, w16=w16)
             for hh in range(G):
                 h = g * G + hh
                 if not check_all_heads and hh > 0:
@@ -72,10 +74,15 @@ def run_and_check(pkv, K, q, V, k, T=None, C=None, n_hot=0, check_all_heads=True
                 eo = r["est"]
                 kn = meta["knorm"][r["cand"]]
                 tol = 1e-3 * np.maximum(np.abs(eo), 1e-2 * kn * r["qnorm"])
+                extra = None
+                if w16:
+                    xb = w16_bound(meta, r["cand"], r["qt"], r["qnorm"])
+                    tol = tol + xb
+                    extra = dict(zip(r["cand"].tolist(), xb.tolist()))
                 egv = np.array([eg[int(i)] for i in r["cand"]])
                 assert np.all(np.abs(egv - eo) <= tol), f"est max err {np.max(np.abs(egv - eo) / tol)} x tol"
                 check_topk(idx[b, h].cpu().numpy(), est[b, h].cpu().numpy(), r["cand"], eo,
-                           dict(zip(range(n), meta["knorm"].tolist())), r["qnorm"], k)
+                           dict(zip(range(n), meta["knorm"].tolist())), r["qnorm"], k, extra_by_id=extra)
                 # attention on the GPU's own index set (AMB-17)
                 ig = idx[b, h].cpu().numpy()
                 o, l = pipeline.attend(qf, Kf, bf16_f64(V[b, g]), ig,
@@ -359,3 +366,33 @@ def test_topk_massive_estimate_ties(pkv):
     Vh = synth.isotropic(98, (1, 1, 16, 128), device="cuda")
     i1, e1, o1, l1 = pkv.retrieve_and_attend(ix, q, K, V, 100, Kh, Vh, n_cand=4500)
     assert torch.equal(i1, idx) and torch.equal(e1, est)
+
+
+def w16_cfg(pkv, n_q, n_kv):
+    cfg = pkv.config_init(n_q, n_kv, SB)
+    cfg.w_fp16 = 1
+    return cfg
+
+
+@pytest.mark.parametrize("case", ["config1", "gqa", "llama", "degenerate"])
+def test_fp16_weights(pkv, case):
+    """96-byte records with fp16 weights and a per-key exponent. Codes and candidate
+    sets stay bit-exact; estimates within AMB-15 + the fp16 rounding bound; top-k equal up to those ties."""
+    if case == "config1":
+        K, q, V = make_problem(1, 1, 1, 1, 4096, plant=False)
+        synth.plant(K, q, 1, n_plant=25)
+        run_and_check(pkv, K, q, V, k=64, cfg=w16_cfg(pkv, 1, 1))
+    elif case == "gqa":
+        K, q, V = make_problem(2, 2, 8, 2, 5003)
+        run_and_check(pkv, K, q, V, k=100, n_hot=37, cfg=w16_cfg(pkv, 8, 2))
+    elif case == "llama":
+        K, q, V = make_problem(3, 1, 32, 8, 3001)
+        run_and_check(pkv, K, q, V, k=100, n_hot=272, check_all_heads=False, cfg=w16_cfg(pkv, 32, 8))
+    else:
+        K, q, V = make_problem(9, 1, 4, 1, 2048, plant=False)
+        K[0, 0, 5] = 0
+        K[0, 0, 6, 16:24] = 0
+        K[0, 0, 10:40, 3] = 1e-9
+        K[0, 0, 40:60, 100] = 3e-30
+        K[0, 0, 60:70, :] = torch.randn(10, 128, device="cuda").to(torch.bfloat16) * 1e-20
+        run_and_check(pkv, K, q, V, k=64, cfg=w16_cfg(pkv, 4, 1))
