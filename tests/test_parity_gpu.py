@@ -306,6 +306,80 @@ def test_full_size_128k_sampled_head(pkv):
         assert np.all(np.abs(og - o) <= ATT_ABS + 2.0 ** -8 * np.abs(o))
 
 
+def check_group_fused(pkv, K, q, V, Kh, Vh, idx, est, out, lse, b, g, T, C, k, dbg=None):
+    """One (sequence, KV head) group of a fused retrieve_and_attend call against the oracle: retrieval of its
+    query heads (AMB-15/16) and attention over hot rows U retrieved rows (AMB-17, GPU's own index set)."""
+    G = q.shape[1] // K.shape[1]
+    n = K.shape[2]
+    Kf = bf16_f64(K[b, g])
+    Vf = bf16_f64(V[b, g])
+    meta = oracle_meta(Kf)
+    for hh in range(G):
+        h = G * g + hh
+        qf = bf16_f64(q[b, h])
+        r = oracle_retrieval(meta, qf, T, C, k)
+        if dbg is not None:
+            assert np.array_equal(dbg["scores"][b, h].cpu().numpy().astype(np.int64), r["score"])
+            cg = dbg["cand"][b, h].cpu().numpy()
+            assert np.array_equal(np.sort(cg), r["cand"])
+        check_topk(idx[b, h].cpu().numpy(), est[b, h].cpu().numpy(), r["cand"], r["est"],
+                   dict(zip(range(n), meta["knorm"].tolist())), r["qnorm"], k)
+        o, l = pipeline.attend(qf, Kf, Vf, idx[b, h].cpu().numpy(), bf16_f64(Kh[b, g]), bf16_f64(Vh[b, g]))
+        og = out[b, h].float().cpu().numpy()
+        assert np.all(np.abs(og - o) <= ATT_ABS + 2.0 ** -8 * np.abs(o)), f"attn err {np.max(np.abs(og - o))}"
+        assert abs(float(lse[b, h]) - l) <= 1e-3 * max(1.0, abs(l))
+
+
+def test_full_size_32k_bs8_fused(pkv):
+    """BASELINE config 3 (bs 8, 32K context = 32,496 retrieval + 272 hot rows per sequence, 32 q / 8 KV heads)
+    through retrieve_and_attend, the call bench.py times: two (sequence, KV head) groups in full against the
+    oracle, sampled key summaries of every sequence."""
+    n, n_hot, k = 32768 - 272, 272, 100
+    K, q, V = make_problem(41, 8, 32, 8, n)
+    Kh = synth.isotropic(42, (8, 8, n_hot, 128), device="cuda")
+    Vh = synth.isotropic(43, (8, 8, n_hot, 128), device="cuda")
+    cfg = pkv.config_init(32, 8, SB)
+    ix = pkv.Index(cfg, 8, n)
+    pkv.encode_keys(ix, K)
+    T, C = pkv.schedule(n, k)
+    idx, est, out, lse = pkv.retrieve_and_attend(ix, q, K, V, k, Kh, Vh)
+    ids_g, codes_g, w_g = [t.cpu().numpy() for t in ix.export()]
+    rng = np.random.default_rng(1)
+    for b in range(8):
+        pos = rng.choice(n, 256, replace=False)
+        meta = oracle_meta(bf16_f64(K[b, b % 8, torch.as_tensor(pos, device="cuda")]))
+        check_encode(ids_g[b, b % 8, pos], codes_g[b, b % 8, pos], w_g[b, b % 8, pos], meta)
+    for b, g in ((0, 3), (7, 6)):
+        check_group_fused(pkv, K, q, V, Kh, Vh, idx, est, out, lse, b, g, T, C, k)
+
+
+@pytest.mark.slow
+def test_full_size_1m_uva_fused(pkv):
+    """BASELINE config 5 on one GPU: 1,048,304 retrieval keys x 8 KV heads, K/V in pinned host memory read
+    through UVA, the long-list (C = 52,416) cluster top-k; one KV group checked in full against the oracle."""
+    n, n_hot, k = 1048576 - 272, 272, 100
+    K, q, V = make_problem(51, 1, 32, 8, n)
+    cfg = pkv.config_init(32, 8, SB)
+    ix = pkv.Index(cfg, 1, n)
+    pkv.encode_keys(ix, K)
+    Kh = synth.isotropic(52, (1, 8, n_hot, 128), device="cuda")
+    Vh = synth.isotropic(53, (1, 8, n_hot, 128), device="cuda")
+    g = 2
+    Kg, Vg = K[:, g:g + 1].contiguous(), V[:, g:g + 1].contiguous()
+    Kc, Vc = K.cpu().pin_memory(), V.cpu().pin_memory()
+    del K, V
+    torch.cuda.empty_cache()
+    T, C = pkv.schedule(n, k)
+    sb, sh, st = Kc.stride(0), Kc.stride(1), Kc.stride(2)
+    idx, est, out, lse = pkv.retrieve_and_attend(ix, q, None, None, k, Kh, Vh, K_ptr=Kc.data_ptr(),
+                                                 V_ptr=Vc.data_ptr(), strides=(sb, sh, st))
+    torch.cuda.synchronize()
+    # the oracle sees the same group: KV head g as a 1-KV-head problem (its query heads are 4g .. 4g+3)
+    check_group_fused(pkv, Kg, q[:, 4 * g:4 * g + 4].contiguous(), Vg, Kh[:, g:g + 1], Vh[:, g:g + 1],
+                      idx[:, 4 * g:4 * g + 4], est[:, 4 * g:4 * g + 4], out[:, 4 * g:4 * g + 4],
+                      lse[:, 4 * g:4 * g + 4], 0, 0, T, C, k)
+
+
 @pytest.mark.parametrize("n,n_hot,k", [(4096, 272, 100), (777, 0, 64), (50, 16, 64), (20000, 300, 100)])
 def test_retrieve_and_attend_matches_two_calls(pkv, n, n_hot, k):
     """The fused schedule (hot attention on a forked stream, top-k fused with gather+attention) returns the
