@@ -101,7 +101,7 @@ pkv_status alloc_workspace(Workspace* ws, int batch, int n_q, int n_kv, int64_t 
       bq * D * 16 * 4,                                   // rtab
       bq * 4,                                            // qnorm
       bq * D * 4,                                        // qrot
-      bk * (size_t)cap * 4,                              // scores
+      bk * (size_t)((cap + 3) & ~3LL) * 4 + 16,          // scores (rows 16-byte aligned for vector loads)
       bk * MAX_CHUNKS * GMAX * HB * 4,                   // chunk_hist
       (size_t)MAX_RANKS * bq * HB * 4,                   // head_hist
       bq * SEL_STRIDE * 4,                               // sel

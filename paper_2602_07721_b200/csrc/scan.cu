@@ -95,7 +95,8 @@ __device__ __forceinline__ void scan_loop(uint4 (&row)[SCAN_UNROLL], const uint8
 
 template <int RES>
 __global__ void __launch_bounds__(SCAN_THREADS, 1)
-    scan_kernel(const uint8_t* __restrict__ ids, const uint32_t* lut_g, uint32_t* scores, uint32_t* chunk_hist, int64_t cap, int64_t n, int64_t chunk, int G) {
+    scan_kernel(const uint8_t* __restrict__ ids, const uint32_t* lut_g, uint32_t* scores, uint32_t* chunk_hist,
+                int64_t cap, int64_t sstride, int64_t n, int64_t chunk, int G) {
   extern __shared__ __align__(16) uint32_t smem[];
   uint32_t* lut = smem;
   uint32_t* hist = smem + LUT_WORDS;
@@ -129,7 +130,7 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1)
   __syncthreads();
   const uint32_t lut_base = (uint32_t)__cvta_generic_to_shared(lut);
   phase_mark(K_SCAN, 2);
-  uint32_t* scores_bh = scores + (int64_t)bh * cap;
+  uint32_t* scores_bh = scores + (int64_t)bh * sstride;
   uint32_t* hist_w = hist + (threadIdx.x >> 5) * GMAX * HB;
   const uint32_t tb = (uint32_t)t_begin, te = (uint32_t)t_end;
   if (lut_base == (uint32_t)RES) {
@@ -178,7 +179,7 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1)
 // sel layout per (b, q head): [0] s*, [1] gt_local, [2] C_local, [3] take_local (written by chunk 0's CTA)
 constexpr int SEL_STRIDE = 4 + 4 * MAX_CHUNKS;
 constexpr int SEL_THREADS = 1024;
-constexpr int SEL_SMEM = 32 * 8 * 32 * 8;  // per-warp compaction lists
+constexpr int SEL_SMEM = 32 * 4 * 128 * 8;  // per-warp compaction lists: up to 4 groups of 128 keys x uint2
 
 // Fused threshold + compaction (bucket_topk). Chunk histograms are CUMULATIVE:
 // cum_j[h][s] = #(score >= s) in chunk j. Every CTA of a (sequence, KV head) recomputes, for its query heads,
@@ -187,6 +188,7 @@ constexpr int SEL_SMEM = 32 * 8 * 32 * 8;  // per-warp compaction lists
 //   offsets : gt_off = sum_{j' < j} #(> s*) in j',  tie quota/offset from the suffix of newer chunks
 // and then writes its chunk's candidates: two passes over the packed scores (L2), warp-level ballots,
 // one block scan of the per-warp counts (no per-tile block synchronisation).
+template <int VB>  // 128-key groups per lane batch (VB * 4 keys per lane in flight)
 __global__ void __launch_bounds__(SEL_THREADS) select_kernel(
     const uint32_t* chunk_hist, const uint32_t* all_hist, int P, int rank, int batch, const uint32_t* scores,
     int64_t cap, int64_t n, int64_t chunk, int nchunks, int n_q, int n_kv, int G, int64_t C, int64_t id_offset,
@@ -198,7 +200,7 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(
   __shared__ int s_star[GMAX], gt_local[GMAX], take_local[GMAX];
   __shared__ int p_gt_off[GMAX], p_tie_off[GMAX], p_take[GMAX], p_eq[GMAX], p_gt_cnt[GMAX];
   __shared__ uint32_t wcnt[32][2 * GMAX];
-  extern __shared__ uint2 sel_list[];  // per-warp compaction lists (VB * 32 entries each), SEL_SMEM bytes
+  extern __shared__ uint2 sel_list[];  // per-warp compaction lists (VB * 128 entries each), SEL_SMEM bytes
   pdl_trigger();
   pdl_wait();
   phase_mark(K_SELECT, 1);
@@ -323,7 +325,8 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(
   const uint32_t t_begin = (uint32_t)j * (uint32_t)chunk;
   const uint32_t t_end = (uint32_t)min(n, (int64_t)t_begin + chunk);
   const uint32_t len = t_end - t_begin;
-  const uint32_t seg = ((len + 32 * 32 - 1) / (32 * 32)) * 32;
+  // warp segments are whole multiples of 128 keys: a lane reads 4 consecutive keys as one 16-byte vector
+  const uint32_t seg = ((len + 32 * 128 - 1) / (32 * 128)) * 128;
   const uint32_t seg0 = t_begin + warp * seg;
   const uint32_t seg1 = min(t_end, seg0 + seg);
   const uint32_t* sc = scores + (int64_t)bh * cap;
@@ -334,27 +337,30 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(
     kgt |= (0x7fu - st) << (8 * hh);
     kge |= (0x80u - st) << (8 * hh);
   }
-  // pass 1: per-head counts of this warp's segment; the lane's scores are loaded 8 at a time (all in flight)
-  // and kept in registers for pass 2 when the segment is short enough (the 128K case)
-  constexpr int VB = 8;
-  uint32_t vreg[VB];
-  const uint32_t nper = (seg1 > seg0) ? (seg1 - seg0 + 31) / 32 : 0;  // keys per lane (upper bound)
+  // pass 1: per-head counts of this warp's segment; lane l reads keys 4l..4l+3 of each 128-key group, VB groups
+  // (16 keys per lane) in flight, kept in registers for pass 2 when the segment is short enough (the 128K case)
+  uint4 vreg[VB];
+  const uint32_t ngrp = (seg1 > seg0) ? (seg1 - seg0 + 127) / 128 : 0;  // 128-key groups of this warp
   uint32_t tot_gt[GMAX] = {0, 0, 0, 0}, tot_eq[GMAX] = {0, 0, 0, 0};
-  for (uint32_t i0 = 0; i0 < nper; i0 += VB) {
+  for (uint32_t g0 = 0; g0 < ngrp; g0 += VB) {
 #pragma unroll
     for (int k2 = 0; k2 < VB; ++k2) {
-      const uint32_t t = seg0 + lane + 32u * (i0 + k2);
-      vreg[k2] = (t < seg1) ? sc[t] : 0u;
+      const uint32_t t = seg0 + 128u * (g0 + k2) + 4u * lane;
+      vreg[k2] = (t < seg1) ? *reinterpret_cast<const uint4*>(sc + t) : make_uint4(0, 0, 0, 0);
     }
-    uint32_t cgt = 0, ceq = 0;
+    uint32_t cgt = 0, ceq = 0;  // per-byte counts (<= 16 per batch: no carries)
 #pragma unroll
     for (int k2 = 0; k2 < VB; ++k2) {
-      const uint32_t t = seg0 + lane + 32u * (i0 + k2);
-      const uint32_t gtb = (vreg[k2] + kgt) & 0x80808080u;
-      const uint32_t geb = (vreg[k2] + kge) & 0x80808080u;
-      if (t < seg1) {
-        cgt += gtb >> 7;
-        ceq += (geb & ~gtb) >> 7;
+      const uint32_t t = seg0 + 128u * (g0 + k2) + 4u * lane;
+      const uint32_t vv[4] = {vreg[k2].x, vreg[k2].y, vreg[k2].z, vreg[k2].w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint32_t gtb = (vv[e] + kgt) & 0x80808080u;
+        const uint32_t geb = (vv[e] + kge) & 0x80808080u;
+        if (t + e < seg1) {
+          cgt += gtb >> 7;
+          ceq += (geb & ~gtb) >> 7;
+        }
       }
     }
 #pragma unroll
@@ -404,26 +410,42 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(
   const uint32_t lt = (1u << lane) - 1u;
   phase_mark(K_SELECT, 4);
   // pass 2: keys with score >= s* for at least one head (~4 x beta of them) are first compacted, in key
-  // order, into a per-warp list; the per-head ballots then run over that list only.
-  uint2* wl = sel_list + warp * (VB * 32);
-  for (uint32_t i0 = 0; i0 < nper; i0 += VB) {
-    if (nper > VB) {
+  // order, into a per-warp list; the per-head ballots then run over that list only. Key (lane l, element e)
+  // of a group precedes (l', e') iff l < l' or (l == l' and e < e'): its list slot is the number of kept keys
+  // of lower lanes (one ballot per element position) plus its own earlier kept elements.
+  uint2* wl = sel_list + warp * (VB * 128);
+  for (uint32_t g0 = 0; g0 < ngrp; g0 += VB) {
+    if (ngrp > VB) {
 #pragma unroll
       for (int k2 = 0; k2 < VB; ++k2) {
-        const uint32_t t = seg0 + lane + 32u * (i0 + k2);
-        vreg[k2] = (t < seg1) ? sc[t] : 0u;
+        const uint32_t t = seg0 + 128u * (g0 + k2) + 4u * lane;
+        vreg[k2] = (t < seg1) ? *reinterpret_cast<const uint4*>(sc + t) : make_uint4(0, 0, 0, 0);
       }
     }
     uint32_t nl = 0;
 #pragma unroll
     for (int k2 = 0; k2 < VB; ++k2) {
-      const uint32_t t = seg0 + lane + 32u * (i0 + k2);
-      const uint32_t gtb = (vreg[k2] + kgt) & 0x80808080u;
-      const uint32_t geb = (vreg[k2] + kge) & 0x80808080u;
-      const bool keep = (t < seg1) && geb != 0u;
-      const uint32_t m = __ballot_sync(0xffffffffu, keep);
-      if (keep) wl[nl + __popc(m & lt)] = make_uint2(t, gtb | ((geb & ~gtb) >> 1));  // bit7: >, bit6: ==
-      nl += __popc(m);
+      const uint32_t t = seg0 + 128u * (g0 + k2) + 4u * lane;
+      const uint32_t vv[4] = {vreg[k2].x, vreg[k2].y, vreg[k2].z, vreg[k2].w};
+      uint32_t fl[4];
+      bool keep[4];
+      uint32_t below = 0, total = 0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint32_t gtb = (vv[e] + kgt) & 0x80808080u;
+        const uint32_t geb = (vv[e] + kge) & 0x80808080u;
+        keep[e] = (t + e < seg1) && geb != 0u;
+        fl[e] = gtb | ((geb & ~gtb) >> 1);  // bit 7: >, bit 6: ==
+        const uint32_t m = __ballot_sync(0xffffffffu, keep[e]);
+        below += __popc(m & lt);
+        total += __popc(m);
+      }
+      uint32_t slot = nl + below;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if (keep[e]) wl[slot++] = make_uint2(t + e, fl[e]);
+      }
+      nl += total;
     }
     __syncwarp();
     for (uint32_t l0 = 0; l0 < nl; l0 += 32) {
@@ -466,10 +488,16 @@ __global__ void dbg_scores_kernel(const uint32_t* __restrict__ scores, int64_t c
 cudaError_t init_scan_attrs() {
   cudaError_t e = cudaFuncSetAttribute(scan_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, SCAN_SMEM);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SEL_SMEM);
+  e = cudaFuncSetAttribute(select_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, SEL_SMEM);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(select_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SEL_SMEM / 2);
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(scan_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, SCAN_SMEM);
 }
+
+// packed-score row stride: the capacity rounded to 4 keys, so every row is 16-byte aligned for the select's
+// vector loads
+static int64_t score_stride(const pkv_index* ix) { return (ix->cap + 3) & ~(int64_t)3; }
 
 ScanPlan plan_scan(const pkv_index* ix, int64_t n) {
   // One 1024-thread CTA per SM (~114 KB smem): never more CTAs than SMs, so there is no second wave.
@@ -498,11 +526,13 @@ cudaError_t launch_scan(const pkv_index* ix, int64_t n, const ScanPlan& plan, cu
   if (ix->smem_reserved == 1024) {
     ProfScope p_(K_SCAN, stream);
     e = pdl_launch(scan_kernel<1024>, grid, dim3(SCAN_THREADS), SCAN_SMEM, stream, (const uint8_t*)ix->ids,
-                   (const uint32_t*)ws->lut, ws->scores, ws->chunk_hist, ix->cap, n, plan.chunk, ix->dcfg.G);
+                   (const uint32_t*)ws->lut, ws->scores, ws->chunk_hist, ix->cap, score_stride(ix), n, plan.chunk,
+                   ix->dcfg.G);
   } else {
     ProfScope p_(K_SCAN, stream);
     e = pdl_launch(scan_kernel<0>, grid, dim3(SCAN_THREADS), SCAN_SMEM, stream, (const uint8_t*)ix->ids,
-                   (const uint32_t*)ws->lut, ws->scores, ws->chunk_hist, ix->cap, n, plan.chunk, ix->dcfg.G);
+                   (const uint32_t*)ws->lut, ws->scores, ws->chunk_hist, ix->cap, score_stride(ix), n, plan.chunk,
+                   ix->dcfg.G);
   }
   return e;
 }
@@ -512,15 +542,19 @@ cudaError_t launch_select(const pkv_index* ix, int64_t n, const ScanPlan& plan, 
   const Workspace* ws = ix->ws;
   dim3 grid(plan.nchunks, ix->batch * ix->cfg.n_kv_heads);
   ProfScope p_(K_SELECT, stream);
-  return pdl_launch(select_kernel, grid, dim3(SEL_THREADS), SEL_SMEM, stream, (const uint32_t*)ws->chunk_hist, all_hist, P,
-                    rank, ix->batch, (const uint32_t*)ws->scores, ix->cap, n, plan.chunk, plan.nchunks,
+  // 128-key groups per warp: ceil(chunk / (32 * 128)); two of them fit one batch (the 128K case), longer chunks
+  // stream four groups per batch
+  const bool small = (plan.chunk + 32 * 128 - 1) / (32 * 128) <= 2;
+  return pdl_launch(small ? select_kernel<2> : select_kernel<4>, grid, dim3(SEL_THREADS),
+                    small ? SEL_SMEM / 2 : SEL_SMEM, stream, (const uint32_t*)ws->chunk_hist, all_hist, P,
+                    rank, ix->batch, (const uint32_t*)ws->scores, score_stride(ix), n, plan.chunk, plan.nchunks,
                     ix->cfg.n_q_heads, ix->cfg.n_kv_heads, ix->dcfg.G, C, id_offset, ws->cap, ws->cand, ws->sel);
 }
 
 cudaError_t launch_dbg_scores(const pkv_index* ix, int64_t n, uint8_t* out, cudaStream_t stream) {
   dim3 grid((unsigned)((n + 255) / 256), ix->batch * ix->cfg.n_kv_heads);
   ProfScope p_(K_DEBUG, stream);
-  dbg_scores_kernel<<<grid, 256, 0, stream>>>(ix->ws->scores, ix->cap, n, ix->cfg.n_q_heads, ix->cfg.n_kv_heads,
+  dbg_scores_kernel<<<grid, 256, 0, stream>>>(ix->ws->scores, score_stride(ix), n, ix->cfg.n_q_heads, ix->cfg.n_kv_heads,
                                               ix->dcfg.G, out);
   return cudaGetLastError();
 }
