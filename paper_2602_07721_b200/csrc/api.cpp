@@ -454,23 +454,27 @@ pkv_status retrieve_and_attend_rows(pkv_index* ix, const void* q, const pkv_retr
   if (n_hot > 16 * 64) return set_error(PKV_ERR_UNSUPPORTED, "retrieve_and_attend: n_hot must be <= 1024");
   DeviceGuard g(ix->device);
   ScanPlan plan;
-  // the hot-row attention rides in the query-prep kernel (16 partials per head, merged by the last kernel)
-  if (hot_rows < n_hot) return set_error(PKV_ERR_INVALID_ARG, "retrieve_and_attend: hot_rows < n_hot");
-  const HotArgs ha{K_hot, V_hot, n_hot, scale, n_hot > 0 ? ix->ws->hot_part : nullptr, hot_rows};
+  const int64_t C_cap = std::min<int64_t>(p->n_cand, ix->n);
+  const bool clustered = topk_segments(C_cap) == 1;
+  // Hot-row attention: in the cluster top-k kernel before its dependency wait (it overlaps the rerank
+  // kernel's drain), or for very long candidate lists in the query-prep kernel (16 partials per head).
+  const bool hot_in_qprep = n_hot > 0 && !clustered;
+  const HotArgs ha{K_hot, V_hot, hot_in_qprep ? n_hot : 0, scale, hot_in_qprep ? ix->ws->hot_part : nullptr,
+                   hot_rows};
   st0 = phase_scan(ix, q, p, plan, stream, &ha);
   if (st0 != PKV_OK) return st0;
   st0 = phase_select_rerank(ix, p, plan, nullptr, 1, 0, stream);
   if (st0 != PKV_OK) return st0;
-  const int hsplits = n_hot > 0 ? NB : 0;
-  if (topk_segments(std::min<int64_t>(p->n_cand, ix->n)) > 1) {
-    // long candidate lists (1M-token contexts): segmented top-k + merge, then the attention kernel
+  if (!clustered) {
+    // long candidate lists (beyond 8 x 16384): segmented top-k + merge, then the attention kernel
+    const int hsplits = n_hot > 0 ? NB : 0;
     PKV_CUDA(launch_topk(ix, p->n_cand, p->top_k, out_idx, out_est, p->top_k, stream), "topk");
     PKV_CUDA(launch_topk_attend_rows(ix, p->top_k, out_idx, q, K, V, sb, sh, st, scale, ix->ws->hot_part, hsplits,
                                      out, lse, stream),
              "attend rows");
-  } else {  // top-k selection fused with the gather + attention of hot U selected rows, one CTA per head
-    PKV_CUDA(launch_topk_attend(ix, std::min<int64_t>(p->n_cand, ix->n), p->top_k, out_idx, out_est, q, K, V, sb, sh, st, scale, ix->ws->hot_part, hsplits,
-                                out, lse, stream),
+  } else {  // top-k fused with the gather + attention of hot U selected rows, one cluster per head
+    PKV_CUDA(launch_topk_attend(ix, C_cap, p->top_k, out_idx, out_est, q, K, V, sb, sh, st, scale, nullptr, 0, K_hot,
+                                V_hot, n_hot, hot_rows, out, lse, stream),
              "topk+attend");
   }
   if (p->dbg_cand || p->dbg_est) PKV_CUDA(launch_dbg_cand(ix, p->n_cand, p->dbg_cand, p->dbg_est, stream), "dbg cand");

@@ -155,9 +155,11 @@ cudaError_t launch_topk(const pkv_index* ix, int64_t C_cap, int k, int32_t* out_
                         int out_stride, cudaStream_t stream);
 // Final top-k fused with the gather + attention of the selected rows and the merge with hot-row partials
 // (hot_part: [batch][n_q][MAX_SPLITS][PART], hsplits entries per head).
-cudaError_t launch_topk_attend(const pkv_index* ix, int64_t C_cap, int k, int32_t* out_idx, float* out_est, const void* q,
-                               const void* K, const void* V, int64_t sb, int64_t sh, int64_t st, float scale,
-                               const float* hot_part, int hsplits, void* out, float* lse, cudaStream_t stream);
+cudaError_t launch_topk_attend(const pkv_index* ix, int64_t C_cap, int k, int32_t* out_idx, float* out_est,
+                               const void* q, const void* K, const void* V, int64_t sb, int64_t sh, int64_t st,
+                               float scale, const float* hot_part, int hsplits, const void* K_hot,
+                               const void* V_hot, int n_hot, int hot_rows, void* out, float* lse,
+                               cudaStream_t stream);
 int topk_segments(int64_t C_cap);
 // Attention over the given top-k rows (no selection) merged with hot partials.
 cudaError_t launch_topk_attend_rows(const pkv_index* ix, int k, const int32_t* idx, const void* q, const void* K,

@@ -456,9 +456,10 @@ struct AttendEpi {  // gather + attention over the selected rows, merged with pr
   float scale;
   const float* hot_part;  // [batch][n_q][MAX_SPLITS][PART], hsplits valid entries per head (may be 0)
   int hsplits;
-  const void* K_hot;      // [batch][n_kv][n_hot][D] hot rows attended in this kernel (may be null)
-  const void* V_hot;
+  const void* K_hot;      // hot rows attended in this kernel (may be null): row t of (b, h) at
+  const void* V_hot;      //   K_hot + ((b*n_kv + h)*hot_rows + t)*D
   int n_hot;
+  int hot_rows;
   void* out;
   float* lse;
   int G;
@@ -677,6 +678,8 @@ __global__ void __launch_bounds__(BS_THREADS) topk_cl_kernel(const float* est, c
   phase_mark(K_TOPK, 0);
   pdl_trigger();
   float q0 = 0.f, q1 = 0.f, q2 = 0.f, q3 = 0.f;
+  // online-softmax state of this warp (log2 domain); seeded with hot rows before the wait
+  float am = -INFINITY, al = 0.f, ao0 = 0.f, ao1 = 0.f, ao2 = 0.f, ao3 = 0.f;
   if constexpr (ATTEND) {  // the query is an input of the layer, complete before the retrieval chain started
     const float qscale = ep.scale * 1.4426950408889634f;
     const uint2 qraw = ldg_v2(static_cast<const uint16_t*>(ep.q) + bhq * D + 4 * lane);
@@ -684,6 +687,60 @@ __global__ void __launch_bounds__(BS_THREADS) topk_cl_kernel(const float* est, c
     q1 = bf16_hi(qraw.x) * qscale;
     q2 = bf16_lo(qraw.y) * qscale;
     q3 = bf16_hi(qraw.y) * qscale;
+    // Hot rows (sink + local + buffer) do not depend on the retrieval: CTA r of the cluster attends
+    // rows [r*per, (r+1)*per) of its head's KV group while the rerank kernel is still draining.
+    if (ep.n_hot > 0) {
+      const int Rr = (int)cl.num_blocks(), rr = (int)cl.block_rank();
+      const int per = (ep.n_hot + Rr - 1) / Rr;
+      const int r0 = rr * per, r1 = min(ep.n_hot, r0 + per);
+      const int64_t hb = ((int64_t)b * (n_q / ep.G) + h / ep.G) * ep.hot_rows * D + 4 * lane;
+      const uint16_t* Kh = static_cast<const uint16_t*>(ep.K_hot) + hb;
+      const uint16_t* Vh = static_cast<const uint16_t*>(ep.V_hot) + hb;
+      constexpr int HB2 = 4;
+      for (int j0 = r0 + warp; j0 < r1; j0 += NW * HB2) {
+        uint2 kr[HB2], vr[HB2];
+#pragma unroll
+        for (int u = 0; u < HB2; ++u) {
+          const int r = j0 + u * NW;
+          kr[u] = vr[u] = make_uint2(0, 0);
+          if (r < r1) {
+            kr[u] = ldg_v2(Kh + (int64_t)r * D);
+            vr[u] = ldg_v2(Vh + (int64_t)r * D);
+          }
+        }
+        float x[HB2];
+#pragma unroll
+        for (int u = 0; u < HB2; ++u)
+          x[u] = bf16_lo(kr[u].x) * q0 + bf16_hi(kr[u].x) * q1 + bf16_lo(kr[u].y) * q2 + bf16_hi(kr[u].y) * q3;
+#pragma unroll
+        for (int xm = 16; xm > 0; xm >>= 1) {
+#pragma unroll
+          for (int u = 0; u < HB2; ++u) x[u] += __shfl_xor_sync(0xffffffffu, x[u], xm);
+        }
+        float mxx = am;
+#pragma unroll
+        for (int u = 0; u < HB2; ++u)
+          if (j0 + u * NW < r1) mxx = fmaxf(mxx, x[u]);
+        const float c = exp2f(am - mxx);
+        al *= c;
+        ao0 *= c;
+        ao1 *= c;
+        ao2 *= c;
+        ao3 *= c;
+#pragma unroll
+        for (int u = 0; u < HB2; ++u) {
+          if (j0 + u * NW < r1) {
+            const float pu = exp2f(x[u] - mxx);
+            al += pu;
+            ao0 = fmaf(pu, bf16_lo(vr[u].x), ao0);
+            ao1 = fmaf(pu, bf16_hi(vr[u].x), ao1);
+            ao2 = fmaf(pu, bf16_lo(vr[u].y), ao2);
+            ao3 = fmaf(pu, bf16_hi(vr[u].y), ao3);
+          }
+        }
+        am = mxx;
+      }
+    }
   }
   pdl_wait();
   phase_mark(K_TOPK, 1);
@@ -908,7 +965,7 @@ __global__ void __launch_bounds__(BS_THREADS) topk_cl_kernel(const float* est, c
     const int g = h / ep.G;
     const uint16_t* Kb = static_cast<const uint16_t*>(ep.K) + (int64_t)b * ep.sb + (int64_t)g * ep.sh + 4 * lane;
     const uint16_t* Vb = static_cast<const uint16_t*>(ep.V) + (int64_t)b * ep.sb + (int64_t)g * ep.sh + 4 * lane;
-    float m = -INFINITY, l = 0.f, o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f;
+    float m = am, l = al, o0 = ao0, o1 = ao1, o2 = ao2, o3 = ao3;  // continues the hot-row state
     constexpr int RB = 4;
     for (int j0 = warp; j0 < nwin; j0 += NW * RB) {
       int id[RB];
@@ -1148,11 +1205,12 @@ cudaError_t launch_topk(const pkv_index* ix, int64_t C_cap, int k, int32_t* out_
 
 cudaError_t launch_topk_attend(const pkv_index* ix, int64_t C_cap, int k, int32_t* out_idx, float* out_est, const void* q,
                                const void* K, const void* V, int64_t sb, int64_t sh, int64_t st, float scale,
-                               const float* hot_part, int hsplits, void* out, float* lse, cudaStream_t stream) {
+                               const float* hot_part, int hsplits, const void* K_hot, const void* V_hot, int n_hot,
+                               int hot_rows, void* out, float* lse, cudaStream_t stream) {
   const Workspace* ws = ix->ws;
   dim3 grid(ix->cfg.n_q_heads, ix->batch);
   ProfScope p_(K_TOPK, stream);
-  AttendEpi ep{q, K, V, sb, sh, st, scale, hot_part, hsplits, nullptr, nullptr, 0, out, lse, ix->dcfg.G};
+  AttendEpi ep{q, K, V, sb, sh, st, scale, hot_part, hsplits, K_hot, V_hot, n_hot, hot_rows, out, lse, ix->dcfg.G};
   int slice = 0;
   const int R = topk_cluster(ix, C_cap, &slice);
   if (R > 0)
@@ -1180,7 +1238,7 @@ cudaError_t launch_topk_attend_rows(const pkv_index* ix, int k, const int32_t* i
   const Workspace* ws = ix->ws;
   dim3 grid(ix->cfg.n_q_heads, ix->batch);
   ProfScope p_(K_ATTEND, stream);
-  AttendEpi ep{q, K, V, sb, sh, st, scale, hot_part, hsplits, nullptr, nullptr, 0, out, lse, ix->dcfg.G};
+  AttendEpi ep{q, K, V, sb, sh, st, scale, hot_part, hsplits, nullptr, nullptr, 0, 0, out, lse, ix->dcfg.G};
   return pdl_launch(topk_kernel<true, false>, grid, dim3(BS_THREADS), TK_SMEM, stream, (const float*)ws->est,
                     (const int32_t*)ws->cand, (const int32_t*)ws->sel, ix->cfg.n_q_heads, ws->cap, k, k,
                     const_cast<int32_t*>(idx), (float*)nullptr, ep, (int64_t)0);
