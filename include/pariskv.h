@@ -162,10 +162,9 @@ pkv_status sparse_attend(pkv_index* index, const void* q, const void* K, const v
 
 /* (3)+(4) retrieve_and_attend — one decode step of one layer: exactly retrieve_topk followed by sparse_attend
  * with the same arguments (K/V rows strided as above, HBM or UVA), scheduled as one unit on the caller's
- * stream (CUDA-graph capturable, no host sync): the hot-row attention (sink + local + buffer) runs
- * inside the query-prep kernel, 16 partial softmax states per query head, and the final top-k selection is
- * fused with the gather and attention of the selected rows and the merge with the hot partials (one
- * thread-block cluster per query head). out_idx/out_est are identical to retrieve_topk's; out/lse equal
+ * stream (CUDA-graph capturable, no host sync): the final top-k selection is fused with the gather and
+ * attention of the selected rows and of the hot rows (sink + local + buffer), one thread-block
+ * cluster per query head; the hot rows are attended before that kernel waits on the rerank kernel. out_idx/out_est are identical to retrieve_topk's; out/lse equal
  * sparse_attend's up to fp32 summation order. n_hot <= 1024. When sequence-sharded it calls the two entry
  * points. Ordering: K_hot/V_hot are read before the kernels wait on their stream predecessor's completion
  * (programmatic dependent launch), so a producer kernel that itself triggers early must not write them. */

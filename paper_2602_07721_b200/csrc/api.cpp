@@ -96,7 +96,7 @@ pkv_status alloc_workspace(Workspace* ws, int batch, int n_q, int n_kv, int64_t 
   ws->n_kv = n_kv;
   ws->cap = cap;
   const size_t bq = (size_t)batch * n_q, bk = (size_t)batch * n_kv;
-  size_t sizes[17] = {
+  size_t sizes[16] = {
       bk * NC * NB * 4,                                  // lut
       bq * D * 16 * 4,                                   // rtab
       bq * 4,                                            // qnorm
@@ -111,7 +111,6 @@ pkv_status alloc_workspace(Workspace* ws, int batch, int n_q, int n_kv, int64_t 
       (size_t)MAX_RANKS * bq * MAX_TOPK * 4,             // topk_idx
       (size_t)MAX_RANKS * bq * MAX_SPLITS * PART * 4,    // part
       bk * 4,                                            // ticket
-      bq * MAX_SPLITS * PART * 4,                        // hot_part
       (size_t)MAX_RANKS * bq * MAX_TOPK * 4,             // seg_est
       (size_t)MAX_RANKS * bq * MAX_TOPK * 4};            // seg_idx
   size_t total = 0;
@@ -139,17 +138,12 @@ pkv_status alloc_workspace(Workspace* ws, int batch, int n_q, int n_kv, int64_t 
   ws->topk_idx = reinterpret_cast<int32_t*>(take(11));
   ws->part = reinterpret_cast<float*>(take(12));
   ws->ticket = reinterpret_cast<unsigned int*>(take(13));
-  ws->hot_part = reinterpret_cast<float*>(take(14));
-  ws->seg_est = reinterpret_cast<float*>(take(15));
-  ws->seg_idx = reinterpret_cast<int32_t*>(take(16));
+  ws->seg_est = reinterpret_cast<float*>(take(14));
+  ws->seg_idx = reinterpret_cast<int32_t*>(take(15));
   ws->base = base;
   ws->bytes = total;
   e = cudaMemset(base, 0, total);
   if (e != cudaSuccess) return cuda_status(e, "workspace memset");
-  e = cudaStreamCreateWithFlags(&ws->side, cudaStreamNonBlocking);
-  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ws->ev_fork, cudaEventDisableTiming);
-  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ws->ev_join, cudaEventDisableTiming);
-  if (e != cudaSuccess) return cuda_status(e, "workspace stream/events");
   return PKV_OK;
 }
 
@@ -157,9 +151,6 @@ void release_workspace(Workspace* ws) {
   if (!ws) return;
   if (--ws->refs == 0) {
     if (ws->base) cudaFree(ws->base);
-    if (ws->ev_fork) cudaEventDestroy(ws->ev_fork);
-    if (ws->ev_join) cudaEventDestroy(ws->ev_join);
-    if (ws->side) cudaStreamDestroy(ws->side);
     delete ws;
   }
 }
@@ -175,11 +166,9 @@ pkv_status check_kv_layout(const void* K, int64_t sb, int64_t sh, int64_t st, co
 }
 
 // -------------------------------------------------------------- retrieval phases (shared by all modes)
-pkv_status phase_scan(pkv_index* ix, const void* q, const pkv_retrieve_params* p, ScanPlan& plan, cudaStream_t s,
-                      const HotArgs* ha = nullptr) {
+pkv_status phase_scan(pkv_index* ix, const void* q, const pkv_retrieve_params* p, ScanPlan& plan, cudaStream_t s) {
   const int64_t n = ix->n;
-  const HotArgs none{nullptr, nullptr, 0, 0.f, nullptr, 0};
-  PKV_CUDA(launch_qprep(ix, q, p->probes_T, p->dbg_q_rot, ha ? *ha : none, s), "qprep");
+  PKV_CUDA(launch_qprep(ix, q, p->probes_T, p->dbg_q_rot, s), "qprep");
   plan = plan_scan(ix, n > 0 ? n : 1);
   if (n > 0) {
     PKV_CUDA(launch_scan(ix, n, plan, s), "scan");
@@ -456,25 +445,20 @@ pkv_status retrieve_and_attend_rows(pkv_index* ix, const void* q, const pkv_retr
   ScanPlan plan;
   const int64_t C_cap = std::min<int64_t>(p->n_cand, ix->n);
   const bool clustered = topk_segments(C_cap) == 1;
-  // Hot-row attention: in the cluster top-k kernel before its dependency wait (it overlaps the rerank
-  // kernel's drain), or for very long candidate lists in the query-prep kernel (16 partials per head).
-  const bool hot_in_qprep = n_hot > 0 && !clustered;
-  const HotArgs ha{K_hot, V_hot, hot_in_qprep ? n_hot : 0, scale, hot_in_qprep ? ix->ws->hot_part : nullptr,
-                   hot_rows};
-  st0 = phase_scan(ix, q, p, plan, stream, &ha);
+  st0 = phase_scan(ix, q, p, plan, stream);
   if (st0 != PKV_OK) return st0;
   st0 = phase_select_rerank(ix, p, plan, nullptr, 1, 0, stream);
   if (st0 != PKV_OK) return st0;
+  // The hot rows (sink + local + buffer) are attended by the last kernel: in the cluster top-k kernel ahead of
+  // its dependency wait (overlapping the rerank kernel's drain); after the segmented top-k for very long lists.
   if (!clustered) {
-    // long candidate lists (beyond 8 x 16384): segmented top-k + merge, then the attention kernel
-    const int hsplits = n_hot > 0 ? NB : 0;
     PKV_CUDA(launch_topk(ix, p->n_cand, p->top_k, out_idx, out_est, p->top_k, stream), "topk");
-    PKV_CUDA(launch_topk_attend_rows(ix, p->top_k, out_idx, q, K, V, sb, sh, st, scale, ix->ws->hot_part, hsplits,
+    PKV_CUDA(launch_topk_attend_rows(ix, p->top_k, out_idx, q, K, V, sb, sh, st, scale, K_hot, V_hot, n_hot, hot_rows,
                                      out, lse, stream),
              "attend rows");
-  } else {  // top-k fused with the gather + attention of hot U selected rows, one cluster per head
-    PKV_CUDA(launch_topk_attend(ix, C_cap, p->top_k, out_idx, out_est, q, K, V, sb, sh, st, scale, nullptr, 0, K_hot,
-                                V_hot, n_hot, hot_rows, out, lse, stream),
+  } else {
+    PKV_CUDA(launch_topk_attend(ix, C_cap, p->top_k, out_idx, out_est, q, K, V, sb, sh, st, scale, K_hot, V_hot, n_hot,
+                                hot_rows, out, lse, stream),
              "topk+attend");
   }
   if (p->dbg_cand || p->dbg_est) PKV_CUDA(launch_dbg_cand(ix, p->n_cand, p->dbg_cand, p->dbg_est, stream), "dbg cand");

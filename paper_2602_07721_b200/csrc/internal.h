@@ -54,11 +54,8 @@ struct Workspace {
   int32_t* topk_idx = nullptr;    // [MAX_RANKS][batch][n_q][MAX_TOPK]
   float* part = nullptr;          // [MAX_RANKS][batch][n_q][MAX_SPLITS][PART] (exchange A)
   unsigned int* ticket = nullptr; // [batch][n_kv] split-completion counters of the fused attention merge
-  float* hot_part = nullptr;      // [batch][n_q][MAX_SPLITS][PART] hot-row partials of retrieve_and_attend
   float* seg_est = nullptr;       // [MAX_RANKS][batch][n_q][MAX_TOPK] segmented top-k of long candidate lists
   int32_t* seg_idx = nullptr;
-  cudaStream_t side = nullptr;    // forked stream for the hot-row attention
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   void* base = nullptr;
   size_t bytes = 0;
   int refs = 1;
@@ -122,18 +119,7 @@ cudaError_t launch_encode(const pkv_index* ix, const void* K, int64_t sb, int64_
                           int64_t count, cudaStream_t stream);
 cudaError_t launch_export(const pkv_index* ix, int64_t start, int64_t count, uint8_t* ids, uint8_t* codes,
                           float* w, cudaStream_t stream);
-// Optional hot-row attention done by qprep: CTA (subspace sb, head h) attends rows [sb*ceil(n/16), ...) of the
-// hot segment and writes its partial (m, l, o) to part[b][h][sb] (log2 domain). part == nullptr: skipped.
-struct HotArgs {
-  const void* K_hot;
-  const void* V_hot;
-  int n_hot;     // rows attended per (sequence, KV head)
-  float scale;
-  float* part;
-  int hot_rows;  // row capacity per (sequence, KV head): element (b, h, t, d) at K_hot + ((b*n_kv + h)*hot_rows + t)*D + d
-};
-cudaError_t launch_qprep(const pkv_index* ix, const void* q, int T, float* dbg_q_rot, const HotArgs& ha,
-                         cudaStream_t stream);
+cudaError_t launch_qprep(const pkv_index* ix, const void* q, int T, float* dbg_q_rot, cudaStream_t stream);
 
 struct ScanPlan {
   int nchunks;
@@ -153,18 +139,19 @@ cudaError_t launch_rerank(const pkv_index* ix, int64_t C_cap, int64_t id_offset,
 cudaError_t launch_dbg_scores(const pkv_index* ix, int64_t n, uint8_t* out, cudaStream_t stream);
 cudaError_t launch_topk(const pkv_index* ix, int64_t C_cap, int k, int32_t* out_idx, float* out_est,
                         int out_stride, cudaStream_t stream);
-// Final top-k fused with the gather + attention of the selected rows and the merge with hot-row partials
-// (hot_part: [batch][n_q][MAX_SPLITS][PART], hsplits entries per head).
+// Final top-k fused with the gather + attention of the selected rows and of the hot rows (row t of (b, h) at
+// K_hot + ((b*n_kv + h)*hot_rows + t)*D), one thread-block cluster per query head.
 cudaError_t launch_topk_attend(const pkv_index* ix, int64_t C_cap, int k, int32_t* out_idx, float* out_est,
                                const void* q, const void* K, const void* V, int64_t sb, int64_t sh, int64_t st,
-                               float scale, const float* hot_part, int hsplits, const void* K_hot,
+                               float scale, const void* K_hot,
                                const void* V_hot, int n_hot, int hot_rows, void* out, float* lse,
                                cudaStream_t stream);
 int topk_segments(int64_t C_cap);
-// Attention over the given top-k rows (no selection) merged with hot partials.
+// Attention over the given top-k rows (no selection) and the hot rows (segmented top-k path).
 cudaError_t launch_topk_attend_rows(const pkv_index* ix, int k, const int32_t* idx, const void* q, const void* K,
                                     const void* V, int64_t sb, int64_t sh, int64_t st, float scale,
-                                    const float* hot_part, int hsplits, void* out, float* lse, cudaStream_t stream);  // > 1: long lists take the segmented top-k + merge (no fused attend)
+                                    const void* K_hot, const void* V_hot, int n_hot, int hot_rows, void* out,
+                                    float* lse, cudaStream_t stream);  // > 1: long lists take the segmented top-k + merge (no fused attend)
 cudaError_t launch_topk_merge_strided(const pkv_index* ix, int P, int k, const float* all_est, const int32_t* all_idx,
                                       int32_t* out_idx, float* out_est, int out_stride, cudaStream_t stream);
 cudaError_t launch_topk_merge(const pkv_index* ix, int P, int k, const float* all_est, const int32_t* all_idx,

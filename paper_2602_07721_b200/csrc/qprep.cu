@@ -36,39 +36,16 @@ __device__ __forceinline__ void ce(KV& mine, const KV& o, int p, int k, int j) {
   mine.id = take ? o.id : mine.id;
 }
 
-constexpr int HOT_RB = 8;  // hot rows per warp and round
-
 __global__ void __launch_bounds__(QP_THREADS) qprep_kernel(const uint16_t* q, int T, DevCfg cfg,
                                                           uint32_t* lut, float* rtab,
                                                           float* qnorm, float* qrot,
-                                                          float* dbg_q_rot, HotArgs ha) {
+                                                          float* dbg_q_rot) {
   __shared__ unsigned long long sk[NC];
   __shared__ uint32_t si[NC];
-  __shared__ float hm[4], hl[4], ho[4][D];
   phase_mark(K_QPREP, 0);
   const int sb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int g = h / cfg.G, hh = h % cfg.G;
-  // Hot-row attention (sink + local + buffer) of this head: CTA (sb, h) takes 1/16 of the hot rows.
-  // The rows do not depend on this decode step, so their loads are issued before waiting on the previous kernel.
-  const int hper = (ha.n_hot + NB - 1) / NB;
-  const int h0 = sb * hper, h1 = min(ha.n_hot, h0 + hper);
-  const uint16_t* Khb = static_cast<const uint16_t*>(ha.K_hot) + ((int64_t)b * cfg.n_kv + g) * ha.hot_rows * D + 4 * lane;
-  const uint16_t* Vhb = static_cast<const uint16_t*>(ha.V_hot) + ((int64_t)b * cfg.n_kv + g) * ha.hot_rows * D + 4 * lane;
-  uint2 hk[HOT_RB], hv[HOT_RB];
-#ifdef PKV_DBG_QPREP_LATE
-  pdl_wait();
-#endif
-#pragma unroll
-  for (int u = 0; u < HOT_RB; ++u) {
-    const int r = h0 + warp + 4 * u;
-    hk[u] = make_uint2(0, 0);
-    hv[u] = make_uint2(0, 0);
-    if (r < h1) {
-      hk[u] = ldg_v2(Khb + (int64_t)r * D);
-      hv[u] = ldg_v2(Vhb + (int64_t)r * D);
-    }
-  }
   pdl_wait();  // the query of this layer follows the previous layer's work
   pdl_trigger();
   phase_mark(K_QPREP, 1);
@@ -134,82 +111,6 @@ __global__ void __launch_bounds__(QP_THREADS) qprep_kernel(const uint16_t* q, in
     }
   }
   if (sb == 0 && t == 0) qnorm[(int64_t)b * cfg.n_q + h] = sqrtf(qn2);
-  if (ha.part != nullptr) {
-    const float qs = ha.scale * 1.4426950408889634f;
-    const float q0 = qf[0] * qs, q1 = qf[1] * qs, q2 = qf[2] * qs, q3 = qf[3] * qs;
-    float m = -INFINITY, l = 0.f, o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f;
-    for (int rbase = h0 + warp; rbase < h1; rbase += 4 * HOT_RB) {
-      if (rbase != h0 + warp) {  // more than 4 * HOT_RB rows per CTA: next round
-#pragma unroll
-        for (int u = 0; u < HOT_RB; ++u) {
-          const int r = rbase + 4 * u;
-          hk[u] = make_uint2(0, 0);
-          hv[u] = make_uint2(0, 0);
-          if (r < h1) {
-            hk[u] = ldg_v2(Khb + (int64_t)r * D);
-            hv[u] = ldg_v2(Vhb + (int64_t)r * D);
-          }
-        }
-      }
-      float x[HOT_RB];
-#pragma unroll
-      for (int u = 0; u < HOT_RB; ++u)
-        x[u] = bf16_lo(hk[u].x) * q0 + bf16_hi(hk[u].x) * q1 + bf16_lo(hk[u].y) * q2 + bf16_hi(hk[u].y) * q3;
-#pragma unroll
-      for (int xm = 16; xm > 0; xm >>= 1) {
-#pragma unroll
-        for (int u = 0; u < HOT_RB; ++u) x[u] += __shfl_xor_sync(0xffffffffu, x[u], xm);
-      }
-      float mx = m;
-#pragma unroll
-      for (int u = 0; u < HOT_RB; ++u)
-        if (rbase + 4 * u < h1) mx = fmaxf(mx, x[u]);
-      const float c = exp2f(m - mx);
-      l *= c;
-      o0 *= c;
-      o1 *= c;
-      o2 *= c;
-      o3 *= c;
-#pragma unroll
-      for (int u = 0; u < HOT_RB; ++u) {
-        if (rbase + 4 * u < h1) {
-          const float pu = exp2f(x[u] - mx);
-          l += pu;
-          o0 = fmaf(pu, bf16_lo(hv[u].x), o0);
-          o1 = fmaf(pu, bf16_hi(hv[u].x), o1);
-          o2 = fmaf(pu, bf16_lo(hv[u].y), o2);
-          o3 = fmaf(pu, bf16_hi(hv[u].y), o3);
-        }
-      }
-      m = mx;
-    }
-    ho[warp][4 * lane] = o0;
-    ho[warp][4 * lane + 1] = o1;
-    ho[warp][4 * lane + 2] = o2;
-    ho[warp][4 * lane + 3] = o3;
-    if (lane == 0) {
-      hm[warp] = m;
-      hl[warp] = l;
-    }
-    __syncthreads();
-    float M = fmaxf(fmaxf(hm[0], hm[1]), fmaxf(hm[2], hm[3]));
-    float L = 0.f, O = 0.f;
-    if (M != -INFINITY) {
-#pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        if (hm[w] == -INFINITY) continue;
-        const float c = exp2f(hm[w] - M);
-        L += c * hl[w];
-        O += c * ho[w][t];
-      }
-    }
-    float* pp = ha.part + (((int64_t)b * cfg.n_q + h) * MAX_SPLITS + sb) * PART;
-    if (t == 0) {
-      pp[0] = M;
-      pp[1] = L;
-    }
-    pp[2 + t] = O;
-  }
   phase_mark(K_QPREP, 2);
   // scores of the two centroids at positions 2t, 2t+1 (ids = positions before sorting)
   KV e[2];
@@ -264,13 +165,12 @@ __global__ void __launch_bounds__(QP_THREADS) qprep_kernel(const uint16_t* q, in
 
 }  // namespace
 
-cudaError_t launch_qprep(const pkv_index* ix, const void* q, int T, float* dbg_q_rot, const HotArgs& ha,
-                         cudaStream_t stream) {
+cudaError_t launch_qprep(const pkv_index* ix, const void* q, int T, float* dbg_q_rot, cudaStream_t stream) {
   const Workspace* ws = ix->ws;
   dim3 grid(NB, ix->cfg.n_q_heads, ix->batch);
   ProfScope p_(K_QPREP, stream);
   return pdl_launch(qprep_kernel, grid, dim3(QP_THREADS), 0, stream, static_cast<const uint16_t*>(q), T, ix->dcfg,
-                    ws->lut, ws->rtab, ws->qnorm, ws->qrot, dbg_q_rot, ha);
+                    ws->lut, ws->rtab, ws->qnorm, ws->qrot, dbg_q_rot);
 }
 
 cudaError_t set_phase_qprep(unsigned long long* p) { return set_phase_ptr_tu(p); }

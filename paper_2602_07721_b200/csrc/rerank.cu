@@ -1,13 +1,16 @@
 // Stage II on the GPU: RSQ-IP rerank (a5) and final top-k (a6) — PAPER §4.1.3 Eq. 8-10, §4.2.2 (2),
 // P:409-425, P:482-486, P:526 ("fused reranking kernel (gather+unpack+score)").
 //
-// rerank_kernel  two threads per candidate gather its 128-byte record (64 B of 4-bit codes + 16 fp32
-//                w' = w/||sign*L[idx]||) and decode each nibble through a per-query table
-//                T[j][nibble] = sign*L[idx]*q~_j in shared memory: est = ||q|| sum_b w'_b sum_j T[8b+j][nib].
-// topk_kernel    per (sequence, query head): MSB-first radix select (8-bit digits) on the 64-bit composite key
-//                (order-preserving fp32 bits of est << 32 | id), so ties in est go to the larger id;
-//                the k winners are then bitonic-sorted descending. Also used to merge the ranks' local top-k
-//                lists when sequence-sharded.
+// rerank_cpt_kernel  a thread pair per candidate, CPT candidates per pair: each thread gathers half of the
+//                    candidate's record (32 B of 4-bit codes + its 8 weights: fp32 w' = w/||sign*L[idx]||, or fp16
+//                    with a per-key exponent) and decodes each nibble through a per-query table
+//                    T[j][nibble] = sign*L[idx]*q~_j in shared memory: est = ||q|| sum_b w'_b sum_j T[8b+j][nib].
+// topk_cl_kernel     per (sequence, query head) a thread-block cluster: local bucket-select top-k per CTA, sorted
+//                    lists exchanged over DSMEM, global ranks by binary search; with ATTEND the gather and
+//                    attention of the selected rows and of the hot rows (the latter before the dependency wait).
+// topk_kernel        single-CTA variant for segmented (> 8 x 16384) candidate lists; merge_kernel merges
+//                    per-segment / per-rank lists by MSB-first radix select on (ord(est) << 32 | id), so ties in
+//                    est go to the larger id.
 #include <cooperative_groups.h>
 #include <cuda_fp16.h>
 
@@ -448,14 +451,12 @@ __device__ __forceinline__ void topk_select(const float* es, const int32_t* ids,
 }
 
 
-struct AttendEpi {  // gather + attention over the selected rows, merged with precomputed hot-row partials
+struct AttendEpi {  // gather + attention over the selected rows and the hot rows
   const void* q;
   const void* K;
   const void* V;
   int64_t sb, sh, st;
   float scale;
-  const float* hot_part;  // [batch][n_q][MAX_SPLITS][PART], hsplits valid entries per head (may be 0)
-  int hsplits;
   const void* K_hot;      // hot rows attended in this kernel (may be null): row t of (b, h) at
   const void* V_hot;      //   K_hot + ((b*n_kv + h)*hot_rows + t)*D
   int n_hot;
@@ -508,8 +509,8 @@ __global__ void __launch_bounds__(BS_THREADS) topk_kernel(const float* est, cons
     float m = -INFINITY, l = 0.f, o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f;
     constexpr int RB = 8;
     // rows of this head: the n_hot hot rows (sink + local + buffer) then the k retrieved rows
-    const uint16_t* Khb = static_cast<const uint16_t*>(ep.K_hot) + ((int64_t)b * n_kv + g) * ep.n_hot * D + 4 * lane;
-    const uint16_t* Vhb = static_cast<const uint16_t*>(ep.V_hot) + ((int64_t)b * n_kv + g) * ep.n_hot * D + 4 * lane;
+    const uint16_t* Khb = static_cast<const uint16_t*>(ep.K_hot) + ((int64_t)b * n_kv + g) * ep.hot_rows * D + 4 * lane;
+    const uint16_t* Vhb = static_cast<const uint16_t*>(ep.V_hot) + ((int64_t)b * n_kv + g) * ep.hot_rows * D + 4 * lane;
     const int nrows = ep.n_hot + k;
     for (int r0 = warp; r0 < nrows; r0 += NW * RB) {
       int id[RB];
@@ -589,37 +590,6 @@ __global__ void __launch_bounds__(BS_THREADS) topk_kernel(const float* est, cons
           O += cw * sm_o[w * D + d];
         }
       }
-      // hot-row partials written by qprep (one per subspace CTA): all loads issued together, then one rescale
-      for (int s0 = 0; s0 < ep.hsplits; s0 += 16) {
-        const float* hp = ep.hot_part + (bhq * MAX_SPLITS + s0) * PART;
-        float ms[16], ls[16], os[16];
-#pragma unroll
-        for (int s2 = 0; s2 < 16; ++s2) {
-          ms[s2] = -INFINITY;
-          ls[s2] = os[s2] = 0.f;
-          if (s0 + s2 < ep.hsplits) {
-            ms[s2] = __ldcg(hp + s2 * PART);
-            ls[s2] = __ldcg(hp + s2 * PART + 1);
-            os[s2] = __ldcg(hp + s2 * PART + 2 + d);
-          }
-        }
-        float Mn = M;
-#pragma unroll
-        for (int s2 = 0; s2 < 16; ++s2) Mn = fmaxf(Mn, ms[s2]);
-        if (Mn != -INFINITY) {
-          const float c0 = (M == -INFINITY) ? 0.f : exp2f(M - Mn);
-          L *= c0;
-          O *= c0;
-#pragma unroll
-          for (int s2 = 0; s2 < 16; ++s2) {
-            if (ms[s2] == -INFINITY) continue;
-            const float cs = exp2f(ms[s2] - Mn);
-            L = fmaf(cs, ls[s2], L);
-            O = fmaf(cs, os[s2], O);
-          }
-          M = Mn;
-        }
-      }
       static_cast<__nv_bfloat16*>(ep.out)[bhq * D + d] = __float2bfloat16_rn(L > 0.f ? O / L : 0.f);
       if (ep.lse && d == 0) ep.lse[bhq] = L > 0.f ? (M + log2f(L)) * 0.6931471805599453f : -INFINITY;
     }
@@ -636,12 +606,12 @@ __global__ void __launch_bounds__(BS_THREADS) topk_kernel(const float* est, cons
 // distributed shared memory — DSMEM bandwidth is ~20 B/clk per SM, so only these short lists cross it) and
 // ranks its own entries by binary search in them: global rank = local index + #peer entries greater. Entries
 // with rank < k are a prefix of the local list; the CTA writes them to out[rank] and, when ATTEND, gathers and
-// attends those rows (plus hot partials r, r+R, ...), sending one (m, l, o) partial to CTA 0, which merges the
+// attends those rows (the hot rows r*per .. (r+1)*per were attended before the dependency wait, seeding the
+// online-softmax state), sending one (m, l, o) partial to CTA 0, which merges the
 // R partials (log2 domain) after the second and last cluster barrier.
 constexpr int CL_MAX = 8;
 constexpr int CL_SLICE = 16384;  // candidates per CTA (est + id cached: 8 B each)
 constexpr int CL_PARTS = 8;      // threads counting one local winner's rank
-constexpr int CL_HOT = 4;        // hot partials per CTA prefetched into registers
 
 struct SmemCand {  // radix fallback source: the CTA's cached slice
   const float* est;
@@ -753,23 +723,6 @@ __global__ void __launch_bounds__(BS_THREADS) topk_cl_kernel(const float* est, c
   const int32_t* ids = cand + bhq * cand_stride;
   int32_t* oi = out_idx + bhq * out_stride;
   float* oe = out_est + bhq * out_stride;
-  // hot-row partials owned by this CTA (written by qprep, complete once pdl_wait returned): prefetched
-  float hpm[CL_HOT], hpl[CL_HOT], hpo[CL_HOT];
-  if constexpr (ATTEND) {
-#pragma unroll
-    for (int u = 0; u < CL_HOT; ++u) {
-      const int s2 = r + u * R;
-      hpm[u] = -INFINITY;
-      hpl[u] = hpo[u] = 0.f;
-      if (s2 < ep.hsplits && tid < D) {
-        const float* pp = ep.hot_part + (bhq * MAX_SPLITS + s2) * PART;
-        hpm[u] = __ldcg(pp);
-        hpl[u] = __ldcg(pp + 1);
-        hpo[u] = __ldcg(pp + 2 + tid);
-      }
-    }
-  }
-
   // ---- 1. cache the slice, min / max
   float mn = INFINITY, mx = -INFINITY;
   for (int i0 = 0; i0 < n_loc; i0 += 8 * BS_THREADS) {
@@ -960,7 +913,7 @@ __global__ void __launch_bounds__(BS_THREADS) topk_cl_kernel(const float* est, c
   phase_mark(K_TOPK, 7);
 
   if constexpr (ATTEND) {
-    // ---- 6. attention over the local winners lst[0..nwin), merged with the owned hot partials
+    // ---- 6. attention over the local winners lst[0..nwin), continuing the hot-row state
     const int nwin = s_nwin;
     const int g = h / ep.G;
     const uint16_t* Kb = static_cast<const uint16_t*>(ep.K) + (int64_t)b * ep.sb + (int64_t)g * ep.sh + 4 * lane;
@@ -1032,10 +985,6 @@ __global__ void __launch_bounds__(BS_THREADS) topk_cl_kernel(const float* est, c
       const int d = tid;
       float M = -INFINITY;
       for (int w = 0; w < NW; ++w) M = fmaxf(M, sm_ml[2 * w]);
-#pragma unroll
-      for (int u = 0; u < CL_HOT; ++u) M = fmaxf(M, hpm[u]);
-      for (int s2 = r + CL_HOT * R; s2 < ep.hsplits; s2 += R)
-        M = fmaxf(M, __ldcg(ep.hot_part + (bhq * MAX_SPLITS + s2) * PART));
       float L = 0.f, O = 0.f;
       if (M != -INFINITY) {
         for (int w = 0; w < NW; ++w) {
@@ -1044,21 +993,6 @@ __global__ void __launch_bounds__(BS_THREADS) topk_cl_kernel(const float* est, c
           const float cw = exp2f(mw - M);
           L = fmaf(cw, sm_ml[2 * w + 1], L);
           O = fmaf(cw, sm_o[w * D + d], O);
-        }
-#pragma unroll
-        for (int u = 0; u < CL_HOT; ++u) {
-          if (hpm[u] == -INFINITY) continue;
-          const float cs = exp2f(hpm[u] - M);
-          L = fmaf(cs, hpl[u], L);
-          O = fmaf(cs, hpo[u], O);
-        }
-        for (int s2 = r + CL_HOT * R; s2 < ep.hsplits; s2 += R) {
-          const float* pp = ep.hot_part + (bhq * MAX_SPLITS + s2) * PART;
-          const float ms = __ldcg(pp);
-          if (ms == -INFINITY) continue;
-          const float cs = exp2f(ms - M);
-          L = fmaf(cs, __ldcg(pp + 1), L);
-          O = fmaf(cs, __ldcg(pp + 2 + d), O);
         }
       }
       float* cp = cl.map_shared_rank(&cpart[r][0], 0);
@@ -1205,12 +1139,12 @@ cudaError_t launch_topk(const pkv_index* ix, int64_t C_cap, int k, int32_t* out_
 
 cudaError_t launch_topk_attend(const pkv_index* ix, int64_t C_cap, int k, int32_t* out_idx, float* out_est, const void* q,
                                const void* K, const void* V, int64_t sb, int64_t sh, int64_t st, float scale,
-                               const float* hot_part, int hsplits, const void* K_hot, const void* V_hot, int n_hot,
+                               const void* K_hot, const void* V_hot, int n_hot,
                                int hot_rows, void* out, float* lse, cudaStream_t stream) {
   const Workspace* ws = ix->ws;
   dim3 grid(ix->cfg.n_q_heads, ix->batch);
   ProfScope p_(K_TOPK, stream);
-  AttendEpi ep{q, K, V, sb, sh, st, scale, hot_part, hsplits, K_hot, V_hot, n_hot, hot_rows, out, lse, ix->dcfg.G};
+  AttendEpi ep{q, K, V, sb, sh, st, scale, K_hot, V_hot, n_hot, hot_rows, out, lse, ix->dcfg.G};
   int slice = 0;
   const int R = topk_cluster(ix, C_cap, &slice);
   if (R > 0)
@@ -1234,11 +1168,12 @@ cudaError_t launch_topk_merge(const pkv_index* ix, int P, int k, const float* al
 
 cudaError_t launch_topk_attend_rows(const pkv_index* ix, int k, const int32_t* idx, const void* q, const void* K,
                                     const void* V, int64_t sb, int64_t sh, int64_t st, float scale,
-                                    const float* hot_part, int hsplits, void* out, float* lse, cudaStream_t stream) {
+                                    const void* K_hot, const void* V_hot, int n_hot, int hot_rows, void* out,
+                                    float* lse, cudaStream_t stream) {
   const Workspace* ws = ix->ws;
   dim3 grid(ix->cfg.n_q_heads, ix->batch);
   ProfScope p_(K_ATTEND, stream);
-  AttendEpi ep{q, K, V, sb, sh, st, scale, hot_part, hsplits, nullptr, nullptr, 0, 0, out, lse, ix->dcfg.G};
+  AttendEpi ep{q, K, V, sb, sh, st, scale, K_hot, V_hot, n_hot, hot_rows, out, lse, ix->dcfg.G};
   return pdl_launch(topk_kernel<true, false>, grid, dim3(BS_THREADS), TK_SMEM, stream, (const float*)ws->est,
                     (const int32_t*)ws->cand, (const int32_t*)ws->sel, ix->cfg.n_q_heads, ws->cap, k, k,
                     const_cast<int32_t*>(idx), (float*)nullptr, ep, (int64_t)0);
