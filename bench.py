@@ -335,9 +335,10 @@ def run_ours(args):
         # fused RSQ-IP rerank: reads the candidate id and gathers its 128 B record, writes the estimate (4 B),
         # per (candidate, query head)
         "rerank": batch * N_Q * min(C, n_loc) * (4 + (96 if args.w16 else 128) + 4),
-        # fused path: top-k over (est, id) pairs + gather of the k selected K/V rows (512 B per row and head);
-        # two-call path: top-k only
-        "topk": batch * N_Q * min(C, n_loc) * 8 + (batch * N_Q * TOP_K * 512 if fused else 0),
+        # fused path: top-k over (est, id) pairs + gather of the k selected K/V rows (512 B per row and head)
+        # + the hot rows (512 B per row and KV head, attended in the same kernel); two-call path: top-k only
+        "topk": batch * N_Q * min(C, n_loc) * 8 + (batch * N_Q * TOP_K * 512 if fused else 0)
+        + (batch * N_KV * n_hot * 512 if fused and rank == world - 1 else 0),  # fused: hot rows too
         # fused path: hot rows only (read once per KV head); two-call path: hot + retrieved rows
         "attend": batch * ((0 if fused else N_Q * TOP_K * 512) + (N_KV * n_hot * 512 if rank == world - 1 else 0)),
     }
