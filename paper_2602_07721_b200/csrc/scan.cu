@@ -10,6 +10,8 @@
 //                  in shared memory; per-chunk totals to global (deterministic, no global atomics).
 // select_kernel    threshold s* = max{s : #(score >= s) >= C} per query head from cumulative chunk histograms,
 //                  ties in the s* bucket handed out newest first (AMB-12), then the chunk's candidate ids.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace pkv {
@@ -192,7 +194,7 @@ template <int VB>  // 128-key groups per lane batch (VB * 4 keys per lane in fli
 __global__ void __launch_bounds__(SEL_THREADS) select_kernel(
     const uint32_t* chunk_hist, const uint32_t* all_hist, int P, int rank, int batch, const uint32_t* scores,
     int64_t cap, int64_t n, int64_t chunk, int nchunks, int n_q, int n_kv, int G, int64_t C, int64_t id_offset,
-    int64_t cand_stride, int32_t* cand, int32_t* sel) {
+    int64_t cand_stride, int32_t* cand, int32_t* sel, const uint8_t* rec, int64_t rec_head_bytes, int rec_bytes) {
   phase_mark(K_SELECT, 0);
   cta_mark(K_SELECT, 1);
   __shared__ uint32_t Hg[GMAX][HB];   // global cumulative counts
@@ -451,6 +453,11 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(
     for (uint32_t l0 = 0; l0 < nl; l0 += 32) {
       const bool valid = l0 + lane < nl;
       const uint2 ent = valid ? wl[l0 + lane] : make_uint2(0u, 0u);
+      if (valid && rec != nullptr) {  // warm L2 with the record the rerank kernel will gather for this key
+        const uint8_t* r = rec + (int64_t)bh * rec_head_bytes + (int64_t)ent.x * rec_bytes;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(r));
+        if (rec_bytes != 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(r + rec_bytes - 1));
+      }
 #pragma unroll
       for (int hh = 0; hh < GMAX; ++hh) {
         const bool fg = (ent.y >> (8 * hh + 7)) & 1u;
@@ -537,6 +544,15 @@ cudaError_t launch_scan(const pkv_index* ix, int64_t n, const ScanPlan& plan, cu
   return e;
 }
 
+// L2 prefetch of the rerank records by the select kernel (PKV_SELECT_PREFETCH=0 disables it, for A/B)
+static bool prefetch_rec() {
+  static const bool on = [] {
+    const char* e = getenv("PKV_SELECT_PREFETCH");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 cudaError_t launch_select(const pkv_index* ix, int64_t n, const ScanPlan& plan, const uint32_t* all_hist, int P,
                           int rank, int64_t C, int64_t id_offset, cudaStream_t stream) {
   const Workspace* ws = ix->ws;
@@ -548,7 +564,13 @@ cudaError_t launch_select(const pkv_index* ix, int64_t n, const ScanPlan& plan, 
   return pdl_launch(small ? select_kernel<2> : select_kernel<4>, grid, dim3(SEL_THREADS),
                     small ? SEL_SMEM / 2 : SEL_SMEM, stream, (const uint32_t*)ws->chunk_hist, all_hist, P,
                     rank, ix->batch, (const uint32_t*)ws->scores, score_stride(ix), n, plan.chunk, plan.nchunks,
-                    ix->cfg.n_q_heads, ix->cfg.n_kv_heads, ix->dcfg.G, C, id_offset, ws->cap, ws->cand, ws->sel);
+                    ix->cfg.n_q_heads, ix->cfg.n_kv_heads, ix->dcfg.G, C, id_offset, ws->cap, ws->cand, ws->sel,
+                    // only when the candidates' records fit the L2 comfortably (128K: 32 MB); at 1M (214 MB) the
+                    // prefetches evict each other and measured slower
+                    prefetch_rec() && (int64_t)ix->batch * ix->cfg.n_q_heads * C * ix->dcfg.rec_bytes <= (48ll << 20)
+                        ? (const uint8_t*)ix->rec
+                        : (const uint8_t*)nullptr,
+                    ix->cap * ix->dcfg.rec_bytes, ix->dcfg.rec_bytes);
 }
 
 cudaError_t launch_dbg_scores(const pkv_index* ix, int64_t n, uint8_t* out, cudaStream_t stream) {
