@@ -110,9 +110,6 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1)
   phase_mark(K_SCAN, 0);
   // the centroid ids do not depend on the query: start streaming them before qprep has finished
   uint4 row[SCAN_UNROLL];
-#ifdef PKV_DBG_SCAN_LATE
-  pdl_wait();
-#endif
   load_rows<true>(row, ids_bh, (uint32_t)t_begin + (threadIdx.x >> 5) * 32 + (threadIdx.x & 31), (uint32_t)t_end);
   for (int i = threadIdx.x; i < SCAN_WARPS * GMAX * HB; i += SCAN_THREADS) hist[i] = 0u;
   pdl_wait();  // lookup table comes from qprep

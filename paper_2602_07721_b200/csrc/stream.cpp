@@ -218,9 +218,6 @@ pkv_status pkv_stream_decode(pkv_stream* s, const void* q, const void* k_new, co
     s->n_buf = 0;
   }
   // (4) retrieval over the updated index + attention over Sink U Local U Update and the retrieved rows
-#ifdef PKV_DBG_STREAM_SYNC
-  if (flush) cudaStreamSynchronize(stream);
-#endif
   pkv_retrieve_params p = *params;
   if (p.probes_T <= 0 || p.n_cand <= 0) {
     int32_t T = 0;
