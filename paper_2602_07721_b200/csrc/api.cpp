@@ -107,8 +107,8 @@ pkv_status alloc_workspace(Workspace* ws, int batch, int n_q, int n_kv, int64_t 
       bq * SEL_STRIDE * 4,                               // sel
       bq * (size_t)cap * 4,                              // cand
       bq * (size_t)cap * 4,                              // est
-      (size_t)MAX_RANKS * bq * MAX_TOPK * 4,             // topk_est
-      (size_t)MAX_RANKS * bq * MAX_TOPK * 4,             // topk_idx
+      (size_t)MAX_RANKS * bq * MAX_TOPK * 8,             // topk exchange: per rank [idx | est] (one all-gather)
+      0,                                                 // (unused)
       (size_t)MAX_RANKS * bq * MAX_SPLITS * PART * 4,    // part
       bk * 4,                                            // ticket
       (size_t)MAX_RANKS * bq * MAX_TOPK * 4,             // seg_est
@@ -134,8 +134,9 @@ pkv_status alloc_workspace(Workspace* ws, int batch, int n_q, int n_kv, int64_t 
   ws->sel = reinterpret_cast<int32_t*>(take(7));
   ws->cand = reinterpret_cast<int32_t*>(take(8));
   ws->est = reinterpret_cast<float*>(take(9));
-  ws->topk_est = reinterpret_cast<float*>(take(10));
-  ws->topk_idx = reinterpret_cast<int32_t*>(take(11));
+  ws->topk_idx = reinterpret_cast<int32_t*>(take(10));
+  ws->topk_est = reinterpret_cast<float*>(ws->topk_idx + bq * MAX_TOPK);  // rank r: idx at 2r*slot, est after
+  take(11);
   ws->part = reinterpret_cast<float*>(take(12));
   ws->ticket = reinterpret_cast<unsigned int*>(take(13));
   ws->seg_est = reinterpret_cast<float*>(take(14));
@@ -358,13 +359,14 @@ pkv_status retrieve_topk(pkv_index* ix, const void* q, const pkv_retrieve_params
     if (st != PKV_OK) return st;
     st = phase_select_rerank(ix, p, plan, ws->head_hist, ix->world, ix->rank, stream);
     if (st != PKV_OK) return st;
-    PKV_CUDA(launch_topk(ix, p->n_cand, p->top_k, ws->topk_idx + ix->rank * topk_slot,
-                         ws->topk_est + ix->rank * topk_slot, MAX_TOPK, stream),
+    // (T) local top-k lists, ids and estimates of a rank adjacent: one all-gather of 2*slot words per rank
+    PKV_CUDA(launch_topk(ix, p->n_cand, p->top_k, ws->topk_idx + ix->rank * 2 * topk_slot,
+                         ws->topk_est + ix->rank * 2 * topk_slot, MAX_TOPK, stream),
              "topk");
-    st = comm_allgather_u32(ix, reinterpret_cast<uint32_t*>(ws->topk_idx), topk_slot, stream);
-    if (st == PKV_OK) st = comm_allgather_u32(ix, reinterpret_cast<uint32_t*>(ws->topk_est), topk_slot, stream);
+    st = comm_allgather_u32(ix, reinterpret_cast<uint32_t*>(ws->topk_idx), 2 * topk_slot, stream);
     if (st != PKV_OK) return st;
-    PKV_CUDA(launch_topk_merge(ix, ix->world, p->top_k, ws->topk_est, ws->topk_idx, out_idx, out_est, stream),
+    PKV_CUDA(launch_topk_merge(ix, ix->world, p->top_k, ws->topk_est, ws->topk_idx, 2 * topk_slot, out_idx, out_est,
+                               stream),
              "topk merge");
   } else {
     st = phase_select_rerank(ix, p, plan, nullptr, 1, 0, stream);
@@ -500,11 +502,13 @@ pkv_status pkv_retrieve_topk_sharded_local(pkv_index* const* shards, const int64
   for (int r = 0; r < P; ++r) {
     st = phase_select_rerank(shards[r], p, plans[r], w0->head_hist, P, r, stream);
     if (st != PKV_OK) return st;
-    PKV_CUDA(launch_topk(shards[r], p->n_cand, p->top_k, w0->topk_idx + r * topk_slot, w0->topk_est + r * topk_slot,
-                         MAX_TOPK, stream),
+    PKV_CUDA(launch_topk(shards[r], p->n_cand, p->top_k, w0->topk_idx + r * 2 * topk_slot,
+                         w0->topk_est + r * 2 * topk_slot, MAX_TOPK, stream),
              "topk");
   }
-  PKV_CUDA(launch_topk_merge(shards[0], P, p->top_k, w0->topk_est, w0->topk_idx, out_idx, out_est, stream), "merge");
+  PKV_CUDA(launch_topk_merge(shards[0], P, p->top_k, w0->topk_est, w0->topk_idx, 2 * topk_slot, out_idx, out_est,
+                             stream),
+           "merge");
   for (int r = 0; r < P; ++r) shards[r]->shard_offset = 0;
   return PKV_OK;
 }

@@ -50,8 +50,8 @@ struct Workspace {
   int32_t* sel = nullptr;         // [batch][n_q][4 + 4*MAX_CHUNKS] threshold + per-chunk offsets
   int32_t* cand = nullptr;        // [batch][n_q][cap]
   float* est = nullptr;           // [batch][n_q][cap]
-  float* topk_est = nullptr;      // [MAX_RANKS][batch][n_q][MAX_TOPK] (sharded exchange T)
-  int32_t* topk_idx = nullptr;    // [MAX_RANKS][batch][n_q][MAX_TOPK]
+  int32_t* topk_idx = nullptr;    // sharded exchange T: rank r's ids at topk_idx + 2r*slot,
+  float* topk_est = nullptr;      //   its estimates at topk_est + 2r*slot (= ids + slot); slot = batch*n_q*MAX_TOPK
   float* part = nullptr;          // [MAX_RANKS][batch][n_q][MAX_SPLITS][PART] (exchange A)
   unsigned int* ticket = nullptr; // [batch][n_kv] split-completion counters of the fused attention merge
   float* seg_est = nullptr;       // [MAX_RANKS][batch][n_q][MAX_TOPK] segmented top-k of long candidate lists
@@ -155,7 +155,7 @@ cudaError_t launch_topk_attend_rows(const pkv_index* ix, int k, const int32_t* i
 cudaError_t launch_topk_merge_strided(const pkv_index* ix, int P, int k, const float* all_est, const int32_t* all_idx,
                                       int32_t* out_idx, float* out_est, int out_stride, cudaStream_t stream);
 cudaError_t launch_topk_merge(const pkv_index* ix, int P, int k, const float* all_est, const int32_t* all_idx,
-                              int32_t* out_idx, float* out_est, cudaStream_t stream);
+                              int64_t rank_stride, int32_t* out_idx, float* out_est, cudaStream_t stream);
 cudaError_t launch_dbg_cand(const pkv_index* ix, int64_t C, int32_t* dbg_cand, float* dbg_est,
                             cudaStream_t stream);
 

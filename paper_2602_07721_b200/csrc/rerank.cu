@@ -1028,12 +1028,12 @@ __global__ void __launch_bounds__(BS_THREADS) topk_cl_kernel(const float* est, c
 }
 
 __global__ void __launch_bounds__(TK_THREADS) merge_kernel(const float* all_est,
-                                                            const int32_t* all_idx, int P, int batch,
+                                                            const int32_t* all_idx, int P, int64_t rank_stride,
                                                             int n_q, int k, int32_t* out_idx, float* out_est,
                                                             int out_stride) {
   const int h = blockIdx.x, b = blockIdx.y;
   const int64_t bhq = (int64_t)b * n_q + h;
-  MergeSrc src{all_est + bhq * MAX_TOPK, all_idx + bhq * MAX_TOPK, k, (int64_t)batch * n_q * MAX_TOPK};
+  MergeSrc src{all_est + bhq * MAX_TOPK, all_idx + bhq * MAX_TOPK, k, rank_stride};
   radix_topk(src, P * k, k, out_idx + bhq * out_stride, out_est + bhq * out_stride);
 }
 
@@ -1158,11 +1158,11 @@ cudaError_t launch_topk_attend(const pkv_index* ix, int64_t C_cap, int k, int32_
 }
 
 cudaError_t launch_topk_merge(const pkv_index* ix, int P, int k, const float* all_est, const int32_t* all_idx,
-                              int32_t* out_idx, float* out_est, cudaStream_t stream) {
+                              int64_t rank_stride, int32_t* out_idx, float* out_est, cudaStream_t stream) {
   dim3 grid(ix->cfg.n_q_heads, ix->batch);
   ProfScope p_(K_MERGE, stream);
-  merge_kernel<<<grid, TK_THREADS, TK_SMEM, stream>>>(all_est, all_idx, P, ix->batch, ix->cfg.n_q_heads, k, out_idx,
-                                                out_est, k);
+  merge_kernel<<<grid, TK_THREADS, TK_SMEM, stream>>>(all_est, all_idx, P, rank_stride, ix->cfg.n_q_heads, k,
+                                                out_idx, out_est, k);
   return cudaGetLastError();
 }
 
@@ -1183,8 +1183,9 @@ cudaError_t launch_topk_merge_strided(const pkv_index* ix, int P, int k, const f
                                       int32_t* out_idx, float* out_est, int out_stride, cudaStream_t stream) {
   dim3 grid(ix->cfg.n_q_heads, ix->batch);
   ProfScope p_(K_MERGE, stream);
-  merge_kernel<<<grid, TK_THREADS, TK_SMEM, stream>>>(all_est, all_idx, P, ix->batch, ix->cfg.n_q_heads, k, out_idx,
-                                                out_est, out_stride);
+  merge_kernel<<<grid, TK_THREADS, TK_SMEM, stream>>>(all_est, all_idx, P,
+                                                (int64_t)ix->batch * ix->cfg.n_q_heads * MAX_TOPK,
+                                                ix->cfg.n_q_heads, k, out_idx, out_est, out_stride);
   return cudaGetLastError();
 }
 
