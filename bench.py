@@ -200,7 +200,8 @@ def run_ours(args):
             ly["Kd"] = None
         torch.cuda.empty_cache()
 
-    fused = world == 1 and not args.two_calls
+    # one call per layer; when sharded the library runs the fused T+A exchange (two collectives per layer)
+    fused = not args.two_calls
 
     def layer_call(ly):
         if fused:  # one decode step of one layer: retrieval + attention scheduled as one unit

@@ -182,6 +182,18 @@ pkv_status retrieve_and_attend_rows(pkv_index* index, const void* q, const pkv_r
                                     float scale, int32_t* out_idx, float* out_est, void* out, float* lse,
                                     cudaStream_t stream);
 
+/* Same for retrieve_and_attend (top_k <= 256): the fused exchange of SURVEY §8(f3) — per query head every
+ * shard contributes its local top-k entries with their attention logits and value rows (and shard P-1 its
+ * hot-row partial) to ONE exchange buffer; a replicated merge selects the global top-k exactly as
+ * retrieve_topk does and attends the selected entries. A communicator-attached index takes the same path in
+ * retrieve_and_attend (two collectives per layer: score histograms, then this exchange). */
+pkv_status pkv_retrieve_and_attend_sharded_local(pkv_index* const* shards, const int64_t* offsets, int32_t P,
+                                                const void* q, const void* const* Ks, const void* const* Vs,
+                                                int64_t sb, int64_t sh, int64_t st,
+                                                const pkv_retrieve_params* params, const void* K_hot,
+                                                const void* V_hot, int32_t n_hot, float scale, int32_t* out_idx,
+                                                float* out_est, void* out, float* lse, cudaStream_t stream);
+
 /* ---------------------------------------------------------------------------------------------------
  * Streaming decode: the four-region KV cache of PAPER §4.2.3 "Buffer Update".
  *   Sink      the first `sink` tokens, kept on the GPU (full precision, always attended)

@@ -152,11 +152,24 @@ void release_workspace(Workspace* ws) {
   if (!ws) return;
   if (--ws->refs == 0) {
     if (ws->base) cudaFree(ws->base);
+    if (ws->ta_msg) cudaFree(ws->ta_msg);
     delete ws;
   }
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// Fused T+A exchange buffer, allocated on first use (an eager call precedes any graph capture).
+pkv_status ensure_ta_msg(Workspace* ws) {
+  if (ws->ta_msg) return PKV_OK;
+  const size_t words = (size_t)MAX_RANKS * ws->batch * ws->n_q * ta_slot(TA_MAXK);
+  cudaError_t e = cudaMalloc(&ws->ta_msg, words * 4);
+  if (e != cudaSuccess) {
+    ws->ta_msg = nullptr;
+    return cuda_status(e, "exchange buffer cudaMalloc");
+  }
+  return PKV_OK;
+}
 
 pkv_status check_kv_layout(const void* K, int64_t sb, int64_t sh, int64_t st, const char* who) {
   if (!K) return set_error(PKV_ERR_INVALID_ARG, std::string(who) + ": null K/V pointer");
@@ -203,6 +216,45 @@ pkv_status check_retrieve(const pkv_index* ix, const void* q, const pkv_retrieve
   if (n_global < 1) return set_error(PKV_ERR_INVALID_ARG, "retrieve_topk: empty retrieval zone");
   if (p->n_cand < std::min<int64_t>(p->top_k, n_global) || p->n_cand > n_global)
     return set_error(PKV_ERR_INVALID_ARG, "retrieve_topk: n_cand must be in [min(top_k, n), n]");
+  return PKV_OK;
+}
+
+// Sequence-sharded retrieve_and_attend with the fused T+A exchange: H all-gather, local
+// candidates and top-k, then ONE all-gather of (est, id, logit, v row) + hot partial per head, and a replicated
+// merge + attention. Two collectives per layer instead of three.
+pkv_status retrieve_and_attend_sharded(pkv_index* ix, const void* q, const pkv_retrieve_params* p, const void* K,
+                                       const void* V, int64_t sb, int64_t sh, int64_t st, const void* K_hot,
+                                       const void* V_hot, int32_t n_hot, float scale, int32_t* out_idx,
+                                       float* out_est, void* out, float* lse, cudaStream_t stream) {
+  const int64_t n_global = comm_global_n(ix);
+  pkv_status st0 = check_retrieve(ix, q, p, n_global, out_idx, out_est);
+  if (st0 != PKV_OK) return st0;
+  if (n_hot < 0 || (n_hot > 0 && (!K_hot || !V_hot))) return set_error(PKV_ERR_INVALID_ARG, "bad hot rows");
+  st0 = check_kv_layout(K, sb, sh, st, "retrieve_and_attend(K)");
+  if (st0 == PKV_OK) st0 = check_kv_layout(V, sb, sh, st, "retrieve_and_attend(V)");
+  if (st0 != PKV_OK) return st0;
+  DeviceGuard g(ix->device);
+  Workspace* ws = ix->ws;
+  st0 = ensure_ta_msg(ws);
+  if (st0 != PKV_OK) return st0;
+  ScanPlan plan;
+  st0 = phase_scan(ix, q, p, plan, stream);
+  if (st0 != PKV_OK) return st0;
+  const size_t hist_slot = (size_t)ix->batch * ix->cfg.n_q_heads * HB;
+  PKV_CUDA(launch_head_hist(ix, plan, ws->head_hist + ix->rank * hist_slot, stream), "head hist");
+  st0 = comm_allgather_u32(ix, ws->head_hist, hist_slot, stream);
+  if (st0 != PKV_OK) return st0;
+  st0 = phase_select_rerank(ix, p, plan, ws->head_hist, ix->world, ix->rank, stream);
+  if (st0 != PKV_OK) return st0;
+  PKV_CUDA(launch_topk(ix, p->n_cand, p->top_k, ws->topk_idx, ws->topk_est, MAX_TOPK, stream), "topk");
+  const size_t rank_words = (size_t)ix->batch * ix->cfg.n_q_heads * ta_slot(p->top_k);
+  const bool last = ix->rank == ix->world - 1;
+  PKV_CUDA(launch_ta_pack(ix, ws->topk_idx, ws->topk_est, p->top_k, q, K, V, sb, sh, st, scale, ix->shard_offset,
+                          K_hot, V_hot, last ? n_hot : 0, ws->ta_msg + ix->rank * rank_words, stream),
+           "exchange pack");
+  st0 = comm_allgather_u32(ix, ws->ta_msg, rank_words, stream);
+  if (st0 != PKV_OK) return st0;
+  PKV_CUDA(launch_ta_merge(ix, ws->ta_msg, ix->world, p->top_k, out_idx, out_est, out, lse, stream), "exchange merge");
   return PKV_OK;
 }
 
@@ -428,8 +480,11 @@ pkv_status retrieve_and_attend_rows(pkv_index* ix, const void* q, const pkv_retr
                                     const void* V_hot, int32_t n_hot, int32_t hot_rows, float scale, int32_t* out_idx,
                                     float* out_est, void* out, float* lse, cudaStream_t stream) {
   if (!ix) return set_error(PKV_ERR_INVALID_ARG, "retrieve_and_attend: null index");
-  if (ix->comm) {
-    if (hot_rows != n_hot) return set_error(PKV_ERR_UNSUPPORTED, "retrieve_and_attend: strided hot rows when sharded");  // sequence-sharded: the exchanges sit between the phases; use the two calls
+  if (ix->comm) {  // sequence-sharded: one fused T+A exchange when k fits its slots, else the two calls
+    if (hot_rows != n_hot) return set_error(PKV_ERR_UNSUPPORTED, "retrieve_and_attend: strided hot rows when sharded");
+    if (p && p->top_k <= TA_MAXK && out)
+      return retrieve_and_attend_sharded(ix, q, p, K, V, sb, sh, st, K_hot, V_hot, n_hot, scale, out_idx, out_est, out,
+                                         lse, stream);
     pkv_status st1 = retrieve_topk(ix, q, p, out_idx, out_est, stream);
     if (st1 != PKV_OK) return st1;
     return sparse_attend(ix, q, K, V, sb, sh, st, out_idx, p->top_k, K_hot, V_hot, n_hot, scale, out, lse, stream);
@@ -542,6 +597,61 @@ pkv_status pkv_sparse_attend_sharded_local(pkv_index* const* shards, const int64
              "attend");
   }
   PKV_CUDA(launch_attend_combine(shards[0], w0->part, splits, P, out, lse, stream), "combine");
+  return PKV_OK;
+}
+
+pkv_status pkv_retrieve_and_attend_sharded_local(pkv_index* const* shards, const int64_t* offsets, int32_t P,
+                                                const void* q, const void* const* Ks, const void* const* Vs,
+                                                int64_t sb, int64_t sh, int64_t st, const pkv_retrieve_params* p,
+                                                const void* K_hot, const void* V_hot, int32_t n_hot, float scale,
+                                                int32_t* out_idx, float* out_est, void* out, float* lse,
+                                                cudaStream_t stream) {
+  if (!shards || !offsets || !Ks || !Vs || P < 1 || P > MAX_RANKS || !q || !p || !out)
+    return set_error(PKV_ERR_INVALID_ARG, "retrieve_and_attend_sharded_local: bad arguments");
+  if (p->top_k > TA_MAXK) return set_error(PKV_ERR_UNSUPPORTED, "retrieve_and_attend_sharded_local: top_k > 256");
+  if (n_hot < 0 || (n_hot > 0 && (!K_hot || !V_hot))) return set_error(PKV_ERR_INVALID_ARG, "bad hot rows");
+  int64_t n_global = 0;
+  for (int r = 0; r < P; ++r) {
+    if (!shards[r] || shards[r]->device != shards[0]->device || shards[r]->batch != shards[0]->batch ||
+        shards[r]->comm || (r && shards[r]->ws == shards[0]->ws))
+      return set_error(PKV_ERR_INVALID_ARG, "sharded_local: shards must be distinct, same device/batch, own workspace");
+    if (offsets[r] != n_global) return set_error(PKV_ERR_INVALID_ARG, "sharded_local: offsets must be contiguous");
+    pkv_status s1 = check_kv_layout(Ks[r], sb, sh, st, "sharded_local(K)");
+    if (s1 == PKV_OK) s1 = check_kv_layout(Vs[r], sb, sh, st, "sharded_local(V)");
+    if (s1 != PKV_OK) return s1;
+    n_global += shards[r]->n;
+  }
+  pkv_status st0 = check_retrieve(shards[0], q, p, n_global, out_idx, out_est);
+  if (st0 != PKV_OK) return st0;
+  DeviceGuard g(shards[0]->device);
+  Workspace* w0 = shards[0]->ws;
+  st0 = ensure_ta_msg(w0);
+  if (st0 != PKV_OK) return st0;
+  const size_t hist_slot = (size_t)shards[0]->batch * shards[0]->cfg.n_q_heads * HB;
+  const size_t rank_words = (size_t)shards[0]->batch * shards[0]->cfg.n_q_heads * ta_slot(p->top_k);
+  ScanPlan plans[MAX_RANKS];
+  pkv_retrieve_params pr = *p;
+  pr.dbg_scores = nullptr;
+  pr.dbg_cand = nullptr;
+  pr.dbg_est = nullptr;
+  pr.dbg_q_rot = nullptr;
+  for (int r = 0; r < P; ++r) {
+    shards[r]->shard_offset = offsets[r];
+    st0 = phase_scan(shards[r], q, &pr, plans[r], stream);
+    if (st0 != PKV_OK) return st0;
+    PKV_CUDA(launch_head_hist(shards[r], plans[r], w0->head_hist + r * hist_slot, stream), "head hist");
+  }
+  for (int r = 0; r < P; ++r) {  // each shard's local top-k in its own workspace, packed into slot r
+    st0 = phase_select_rerank(shards[r], &pr, plans[r], w0->head_hist, P, r, stream);
+    if (st0 != PKV_OK) return st0;
+    Workspace* wr = shards[r]->ws;
+    PKV_CUDA(launch_topk(shards[r], pr.n_cand, pr.top_k, wr->topk_idx, wr->topk_est, MAX_TOPK, stream), "topk");
+    PKV_CUDA(launch_ta_pack(shards[r], wr->topk_idx, wr->topk_est, pr.top_k, q, Ks[r], Vs[r], sb, sh, st, scale,
+                            offsets[r], K_hot, V_hot, r == P - 1 ? n_hot : 0, w0->ta_msg + r * rank_words, stream),
+             "exchange pack");
+  }
+  PKV_CUDA(launch_ta_merge(shards[0], w0->ta_msg, P, pr.top_k, out_idx, out_est, out, lse, stream), "exchange merge");
+  for (int r = 0; r < P; ++r) shards[r]->shard_offset = 0;
   return PKV_OK;
 }
 

@@ -50,6 +50,7 @@ struct Workspace {
   int32_t* sel = nullptr;         // [batch][n_q][4 + 4*MAX_CHUNKS] threshold + per-chunk offsets
   int32_t* cand = nullptr;        // [batch][n_q][cap]
   float* est = nullptr;           // [batch][n_q][cap]
+  uint32_t* ta_msg = nullptr;     // fused T+A exchange: [MAX_RANKS][batch][n_q][ta_slot(TA_MAXK)] words
   int32_t* topk_idx = nullptr;    // sharded exchange T: rank r's ids at topk_idx + 2r*slot,
   float* topk_est = nullptr;      //   its estimates at topk_est + 2r*slot (= ids + slot); slot = batch*n_q*MAX_TOPK
   float* part = nullptr;          // [MAX_RANKS][batch][n_q][MAX_SPLITS][PART] (exchange A)
@@ -154,6 +155,16 @@ cudaError_t launch_topk_attend_rows(const pkv_index* ix, int k, const int32_t* i
                                     float* lse, cudaStream_t stream);  // > 1: long lists take the segmented top-k + merge (no fused attend)
 cudaError_t launch_topk_merge_strided(const pkv_index* ix, int P, int k, const float* all_est, const int32_t* all_idx,
                                       int32_t* out_idx, float* out_est, int out_stride, cudaStream_t stream);
+// Sharded fused exchange (T+A): per (rank, sequence, head) a slot of ta_slot(k) words holding the rank's local
+// top-k entries (est, id, logit), their value rows and the rank's hot-row partial; one all-gather, then a
+// replicated merge + attention.
+constexpr int TA_MAXK = 256;
+int64_t ta_slot(int k);
+cudaError_t launch_ta_pack(const pkv_index* ix, const int32_t* lidx, const float* lest, int k, const void* q,
+                           const void* K, const void* V, int64_t sb, int64_t sh, int64_t st, float scale, int64_t off,
+                           const void* K_hot, const void* V_hot, int n_hot, uint32_t* msg, cudaStream_t stream);
+cudaError_t launch_ta_merge(const pkv_index* ix, const uint32_t* msg, int P, int k, int32_t* out_idx, float* out_est,
+                            void* out, float* lse, cudaStream_t stream);
 cudaError_t launch_topk_merge(const pkv_index* ix, int P, int k, const float* all_est, const int32_t* all_idx,
                               int64_t rank_stride, int32_t* out_idx, float* out_est, cudaStream_t stream);
 cudaError_t launch_dbg_cand(const pkv_index* ix, int64_t C, int32_t* dbg_cand, float* dbg_est,

@@ -1037,6 +1037,186 @@ __global__ void __launch_bounds__(TK_THREADS) merge_kernel(const float* all_est,
   radix_topk(src, P * k, k, out_idx + bhq * out_stride, out_est + bhq * out_stride);
 }
 
+// ---------------------------------------------------------------- sharded: fused top-k + attention exchange
+// SURVEY §8(f3) "fusing T+A": instead of all-gathering the local top-k lists, merging, then computing and
+// all-gathering attention partials over the owned winners (two exchanges), every rank ships, per query head,
+// its local top-k entries together with what the attention needs from them — the logit x_j = <q, k_j>/sqrt(D)
+// (log2 domain) and the value row v_j — plus its hot-row partial (last rank). After ONE all-gather every rank
+// merges the P*k entries (same radix select on (est, id) as the unfused merge: identical top-k) and attends the
+// selected entries' (x, v) directly, merging the hot partials: replicated output, one collective less.
+// Slot of one (rank, sequence, head), in 32-bit words: [k x (est, id, x, 0)] [k x 64 words of bf16 v] [m, l, o[128]].
+struct TASrc {  // merge source: P ranks x k entries, entries 4 words apart
+  const uint32_t* base;
+  int k;
+  int64_t rank_stride;
+  __device__ __forceinline__ unsigned long long key(int i) const {
+    const int r = i / k, j = i % k;
+    const uint32_t* e = base + r * rank_stride + 4 * j;
+    if ((int32_t)e[1] < 0) return 0ull;  // padding: never selected
+    return ((unsigned long long)ord_f32(__uint_as_float(e[0])) << 32) | e[1];
+  }
+};
+
+__host__ __device__ constexpr int64_t ta_slot_words(int k) { return ((int64_t)68 * k + PART + 3) / 4 * 4; }
+
+// Grid (n_q, batch), 256 threads: pack this rank's local top-k (lidx/lest, stride MAX_TOPK) into its slots.
+__global__ void __launch_bounds__(256) ta_pack_kernel(const int32_t* lidx, const float* lest, int k, int n_q, int G,
+                                                      const uint16_t* q, const uint16_t* K, const uint16_t* V,
+                                                      int64_t sb, int64_t sh, int64_t st, float scale, int64_t off,
+                                                      const uint16_t* K_hot, const uint16_t* V_hot, int n_hot,
+                                                      uint32_t* msg, int64_t SW) {
+  __shared__ float sm_o[8][D], sm_ml[8][2];
+  pdl_trigger();
+  pdl_wait();
+  const int h = blockIdx.x, b = blockIdx.y, g = h / G, n_kv = n_q / G;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t bhq = (int64_t)b * n_q + h;
+  uint32_t* slot = msg + bhq * SW;
+  const float qs = scale * 1.4426950408889634f;
+  const uint2 qr = ldg_v2(q + bhq * D + 4 * lane);
+  const float q0 = bf16_lo(qr.x) * qs, q1 = bf16_hi(qr.x) * qs, q2 = bf16_lo(qr.y) * qs, q3 = bf16_hi(qr.y) * qs;
+  const uint16_t* Kb = K + (int64_t)b * sb + (int64_t)g * sh + 4 * lane;
+  const uint16_t* Vb = V + (int64_t)b * sb + (int64_t)g * sh + 4 * lane;
+  for (int j = warp; j < k; j += 8) {
+    const int32_t id = lidx[bhq * MAX_TOPK + j];
+    float x = 0.f;
+    if (id >= 0) {
+      const uint2 kr = ldg_v2(Kb + (id - off) * st);
+      const uint2 vr = ldg_v2(Vb + (id - off) * st);
+      x = bf16_lo(kr.x) * q0 + bf16_hi(kr.x) * q1 + bf16_lo(kr.y) * q2 + bf16_hi(kr.y) * q3;
+#pragma unroll
+      for (int xm = 16; xm > 0; xm >>= 1) x += __shfl_xor_sync(0xffffffffu, x, xm);
+      reinterpret_cast<uint2*>(slot + 4 * k + 64 * j)[lane] = vr;
+    }
+    if (lane == 0) {
+      slot[4 * j] = __float_as_uint(id >= 0 ? lest[bhq * MAX_TOPK + j] : -INFINITY);
+      slot[4 * j + 1] = (uint32_t)id;
+      slot[4 * j + 2] = __float_as_uint(x);
+      slot[4 * j + 3] = 0u;
+    }
+  }
+  // hot-row partial of this head (n_hot = 0 except on the last rank)
+  float m = -INFINITY, l = 0.f, o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f;
+  const uint16_t* Kh = K_hot + ((int64_t)b * n_kv + g) * n_hot * D + 4 * lane;
+  const uint16_t* Vh = V_hot + ((int64_t)b * n_kv + g) * n_hot * D + 4 * lane;
+  for (int r = warp; r < n_hot; r += 8) {
+    const uint2 kr = ldg_v2(Kh + (int64_t)r * D), vr = ldg_v2(Vh + (int64_t)r * D);
+    float x = bf16_lo(kr.x) * q0 + bf16_hi(kr.x) * q1 + bf16_lo(kr.y) * q2 + bf16_hi(kr.y) * q3;
+#pragma unroll
+    for (int xm = 16; xm > 0; xm >>= 1) x += __shfl_xor_sync(0xffffffffu, x, xm);
+    const float mx = fmaxf(m, x), c = exp2f(m - mx), p = exp2f(x - mx);
+    l = l * c + p;
+    o0 = fmaf(p, bf16_lo(vr.x), o0 * c);
+    o1 = fmaf(p, bf16_hi(vr.x), o1 * c);
+    o2 = fmaf(p, bf16_lo(vr.y), o2 * c);
+    o3 = fmaf(p, bf16_hi(vr.y), o3 * c);
+    m = mx;
+  }
+  sm_o[warp][4 * lane] = o0;
+  sm_o[warp][4 * lane + 1] = o1;
+  sm_o[warp][4 * lane + 2] = o2;
+  sm_o[warp][4 * lane + 3] = o3;
+  if (lane == 0) {
+    sm_ml[warp][0] = m;
+    sm_ml[warp][1] = l;
+  }
+  __syncthreads();
+  if (threadIdx.x < D) {
+    const int d = threadIdx.x;
+    float M = -INFINITY;
+    for (int w = 0; w < 8; ++w) M = fmaxf(M, sm_ml[w][0]);
+    float L = 0.f, O = 0.f;
+    if (M != -INFINITY)
+      for (int w = 0; w < 8; ++w) {
+        if (sm_ml[w][0] == -INFINITY) continue;
+        const float c = exp2f(sm_ml[w][0] - M);
+        L = fmaf(c, sm_ml[w][1], L);
+        O = fmaf(c, sm_o[w][d], O);
+      }
+    float* hp = reinterpret_cast<float*>(slot + 68 * k);
+    if (d == 0) {
+      hp[0] = M;
+      hp[1] = L;
+    }
+    hp[2 + d] = O;
+  }
+}
+
+// Grid (n_q, batch), TK_THREADS: merge the P ranks' entries into the global top-k (radix select on (est, id), as
+// merge_kernel) and attend the selected entries' (x, v) plus the P hot partials.
+__global__ void __launch_bounds__(TK_THREADS) ta_merge_kernel(const uint32_t* msg, int P, int64_t rank_stride,
+                                                              int64_t SW, int n_q, int k, int32_t* out_idx,
+                                                              float* out_est, void* out, float* lse) {
+  constexpr int NW = TK_THREADS / 32;
+  __shared__ float sm_o[NW][D], sm_ml[NW][2];
+  __shared__ unsigned long long s_kth;
+  const int h = blockIdx.x, b = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t bhq = (int64_t)b * n_q + h;
+  pdl_trigger();
+  pdl_wait();
+  int32_t* oi = out_idx + bhq * k;
+  float* oe = out_est + bhq * k;
+  radix_topk(TASrc{msg + bhq * SW, k, rank_stride}, P * k, k, oi, oe);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int kv = 0;
+    while (kv < k && oi[kv] >= 0) ++kv;
+    s_kth = kv > 0 ? ckey(oe[kv - 1], oi[kv - 1]) : ~0ull;  // the k-th largest composite key (none: select none)
+  }
+  __syncthreads();
+  const unsigned long long kth = s_kth;
+  float m = -INFINITY, l = 0.f, o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f;
+  for (int e = warp; e < P * k; e += NW) {
+    const int r = e / k, j = e - r * k;
+    const uint32_t* slot = msg + r * rank_stride + bhq * SW;
+    const int32_t id = (int32_t)slot[4 * j + 1];
+    if (id < 0 || ckey(__uint_as_float(slot[4 * j]), id) < kth) continue;  // warp-uniform
+    const float x = __uint_as_float(slot[4 * j + 2]);
+    const uint2 vr = reinterpret_cast<const uint2*>(slot + 4 * k + 64 * j)[lane];
+    const float mx = fmaxf(m, x), c = exp2f(m - mx), p = exp2f(x - mx);
+    l = l * c + p;
+    o0 = fmaf(p, bf16_lo(vr.x), o0 * c);
+    o1 = fmaf(p, bf16_hi(vr.x), o1 * c);
+    o2 = fmaf(p, bf16_lo(vr.y), o2 * c);
+    o3 = fmaf(p, bf16_hi(vr.y), o3 * c);
+    m = mx;
+  }
+  sm_o[warp][4 * lane] = o0;
+  sm_o[warp][4 * lane + 1] = o1;
+  sm_o[warp][4 * lane + 2] = o2;
+  sm_o[warp][4 * lane + 3] = o3;
+  if (lane == 0) {
+    sm_ml[warp][0] = m;
+    sm_ml[warp][1] = l;
+  }
+  __syncthreads();
+  if (threadIdx.x < D) {
+    const int d = threadIdx.x;
+    float M = -INFINITY;
+    for (int w = 0; w < NW; ++w) M = fmaxf(M, sm_ml[w][0]);
+    for (int r = 0; r < P; ++r) M = fmaxf(M, reinterpret_cast<const float*>(msg + r * rank_stride + bhq * SW + 68 * k)[0]);
+    float L = 0.f, O = 0.f;
+    if (M != -INFINITY) {
+      for (int w = 0; w < NW; ++w) {
+        if (sm_ml[w][0] == -INFINITY) continue;
+        const float c = exp2f(sm_ml[w][0] - M);
+        L = fmaf(c, sm_ml[w][1], L);
+        O = fmaf(c, sm_o[w][d], O);
+      }
+      for (int r = 0; r < P; ++r) {
+        const float* hp = reinterpret_cast<const float*>(msg + r * rank_stride + bhq * SW + 68 * k);
+        if (hp[0] == -INFINITY) continue;
+        const float c = exp2f(hp[0] - M);
+        L = fmaf(c, hp[1], L);
+        O = fmaf(c, hp[2 + d], O);
+      }
+    }
+    static_cast<__nv_bfloat16*>(out)[bhq * D + d] = __float2bfloat16_rn(L > 0.f ? O / L : 0.f);
+    if (lse && d == 0) lse[bhq] = L > 0.f ? (M + log2f(L)) * 0.6931471805599453f : -INFINITY;
+  }
+}
+
 __global__ void dbg_cand_kernel(const int32_t* __restrict__ cand, const float* __restrict__ est,
                                 const int32_t* __restrict__ sel, int n_q, int64_t cand_stride, int64_t C,
                                 int32_t* dbg_cand, float* dbg_est) {
@@ -1085,6 +1265,8 @@ cudaError_t init_rerank_attrs() {
   static_assert(CL_SLICE * 8 >= CL_MAX * MAX_TOPK * 8 + (BS_THREADS / 32) * (D + 2) * 4, "cluster top-k smem");
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(topk_cl_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, CL_SLICE * 8);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(ta_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TK_SMEM);
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TK_SMEM);
 }
@@ -1187,6 +1369,28 @@ cudaError_t launch_topk_merge_strided(const pkv_index* ix, int P, int k, const f
                                                 (int64_t)ix->batch * ix->cfg.n_q_heads * MAX_TOPK,
                                                 ix->cfg.n_q_heads, k, out_idx, out_est, out_stride);
   return cudaGetLastError();
+}
+
+int64_t ta_slot(int k) { return ta_slot_words(k); }
+
+cudaError_t launch_ta_pack(const pkv_index* ix, const int32_t* lidx, const float* lest, int k, const void* q,
+                           const void* K, const void* V, int64_t sb, int64_t sh, int64_t st, float scale, int64_t off,
+                           const void* K_hot, const void* V_hot, int n_hot, uint32_t* msg, cudaStream_t stream) {
+  dim3 grid(ix->cfg.n_q_heads, ix->batch);
+  ProfScope p_(K_ATTEND, stream);
+  return pdl_launch(ta_pack_kernel, grid, dim3(256), 0, stream, lidx, lest, k, ix->cfg.n_q_heads, ix->dcfg.G,
+                    static_cast<const uint16_t*>(q), static_cast<const uint16_t*>(K), static_cast<const uint16_t*>(V),
+                    sb, sh, st, scale, off, static_cast<const uint16_t*>(K_hot), static_cast<const uint16_t*>(V_hot),
+                    n_hot, msg, ta_slot_words(k));
+}
+
+cudaError_t launch_ta_merge(const pkv_index* ix, const uint32_t* msg, int P, int k, int32_t* out_idx, float* out_est,
+                            void* out, float* lse, cudaStream_t stream) {
+  dim3 grid(ix->cfg.n_q_heads, ix->batch);
+  ProfScope p_(K_MERGE, stream);
+  const int64_t SW = ta_slot_words(k);
+  return pdl_launch(ta_merge_kernel, grid, dim3(TK_THREADS), TK_SMEM, stream, msg, P,
+                    (int64_t)ix->batch * ix->cfg.n_q_heads * SW, SW, ix->cfg.n_q_heads, k, out_idx, out_est, out, lse);
 }
 
 cudaError_t launch_dbg_cand(const pkv_index* ix, int64_t C, int32_t* dbg_cand, float* dbg_est, cudaStream_t stream) {

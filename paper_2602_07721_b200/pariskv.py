@@ -74,6 +74,9 @@ _sigs = {
     "pkv_retrieve_topk_sharded_local": [_vp, _vp, _i32, _vp, ctypes.POINTER(RetrieveParams), _vp, _vp, _vp],
     "pkv_sparse_attend_sharded_local": [_vp, _vp, _i32, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _i32, _vp, _vp, _i32,
                                         _f32, _vp, _vp, _vp],
+    "pkv_retrieve_and_attend_sharded_local": [_vp, _vp, _i32, _vp, _vp, _vp, _i64, _i64, _i64,
+                                              ctypes.POINTER(RetrieveParams), _vp, _vp, _i32, _f32, _vp, _vp, _vp,
+                                              _vp, _vp],
     "pkv_launch_count": [ctypes.POINTER(ctypes.c_uint64)],
     "pkv_profile_enable": [_i32],
     "pkv_profile_read": [_i32, ctypes.POINTER(_i64), ctypes.POINTER(ctypes.c_double)],
@@ -416,6 +419,33 @@ def retrieve_topk_sharded_local(shards, offsets, q, top_k, n_global, stream=None
     _check(_lib.pkv_retrieve_topk_sharded_local(hs, offs, P, _ptr(q), ctypes.byref(p), _ptr(out_idx), _ptr(out_est),
                                                 _stream(stream)))
     return out_idx, out_est
+
+
+def retrieve_and_attend_sharded_local(shards, offsets, q, Ks, Vs, top_k, K_hot=None, V_hot=None, scale=None,
+                                      stream=None):
+    """Single-process emulation of the sequence-sharded retrieve_and_attend with the fused exchange (§8(f3)):
+    shard p owns global positions [offsets[p], offsets[p] + len(shards[p])); Ks[p], Vs[p] its K/V rows."""
+    P = len(shards)
+    n_global = sum(len(s) for s in shards)
+    T, C = schedule(n_global, top_k)
+    hs = (_vp * P)(*[s.handle.value for s in shards])
+    offs = (_i64 * P)(*offsets)
+    kp = (_vp * P)(*[k.data_ptr() for k in Ks])
+    vp = (_vp * P)(*[v.data_ptr() for v in Vs])
+    sb, sh, st = _kv_strides(Ks[0])
+    ix = shards[0]
+    dev = q.device
+    out_idx = torch.empty(ix.batch, ix.n_q, top_k, dtype=torch.int32, device=dev)
+    out_est = torch.empty(ix.batch, ix.n_q, top_k, dtype=torch.float32, device=dev)
+    out = torch.empty(ix.batch, ix.n_q, D, dtype=torch.bfloat16, device=dev)
+    lse = torch.empty(ix.batch, ix.n_q, dtype=torch.float32, device=dev)
+    n_hot = 0 if K_hot is None else K_hot.shape[2]
+    scale = 1.0 / np.sqrt(D) if scale is None else scale
+    p = RetrieveParams(T, C, top_k, None, None, None, None)
+    _check(_lib.pkv_retrieve_and_attend_sharded_local(hs, offs, P, _ptr(q), kp, vp, sb, sh, st, ctypes.byref(p),
+                                                      _ptr(K_hot), _ptr(V_hot), n_hot, scale, _ptr(out_idx),
+                                                      _ptr(out_est), _ptr(out), _ptr(lse), _stream(stream)))
+    return out_idx, out_est, out, lse
 
 
 def sparse_attend_sharded_local(shards, offsets, q, Ks, Vs, idx, K_hot=None, V_hot=None, scale=None, stream=None):

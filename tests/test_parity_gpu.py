@@ -273,6 +273,34 @@ def test_sequence_sharded_local_equals_unsharded(pkv, P):
 
 
 @pytest.mark.slow
+@pytest.mark.parametrize("P,n_hot", [(2, 272), (3, 0), (4, 40)])
+def test_fused_exchange_sharded_local(pkv, P, n_hot):
+    """the fused T+A exchange (one exchange per layer after the histogram one) gives the same
+    top-k as the unsharded retrieval (bit-identical ids and estimates) and the same attention output."""
+    batch, n_q, n_kv, n, k = 2, 8, 2, 9000, 100
+    K, q, V = make_problem(61 + P, batch, n_q, n_kv, n)
+    Kh = synth.isotropic(62, (batch, n_kv, max(n_hot, 1), 128), device="cuda")[:, :, :n_hot].contiguous()
+    Vh = synth.isotropic(63, (batch, n_kv, max(n_hot, 1), 128), device="cuda")[:, :, :n_hot].contiguous()
+    cfg = pkv.config_init(n_q, n_kv, SB)
+    full = pkv.Index(cfg, batch, n)
+    pkv.encode_keys(full, K)
+    i0, e0, o0, l0 = pkv.retrieve_and_attend(full, q, K, V, k, Kh if n_hot else None, Vh if n_hot else None)
+    bounds = [n * r // P for r in range(P + 1)]
+    shards, Ks, Vs = [], [], []
+    for r in range(P):
+        lo, hi = bounds[r], bounds[r + 1]
+        ix = pkv.Index(cfg, batch, hi - lo)
+        pkv.encode_keys(ix, K[:, :, lo:hi].contiguous())
+        shards.append(ix)
+        Ks.append(K[:, :, lo:hi].contiguous())
+        Vs.append(V[:, :, lo:hi].contiguous())
+    i1, e1, o1, l1 = pkv.retrieve_and_attend_sharded_local(shards, bounds[:P], q, Ks, Vs, k,
+                                                           Kh if n_hot else None, Vh if n_hot else None)
+    torch.cuda.synchronize()
+    assert torch.equal(i0, i1) and torch.equal(e0, e1)
+    assert torch.allclose(o0.float(), o1.float(), atol=4e-3) and torch.allclose(l0, l1, atol=1e-4)
+
+
 def test_full_size_128k_sampled_head(pkv):
     """BASELINE config 2 shape (32 q / 8 KV heads, n = 130,800) in the launch configuration bench.py times:
     one KV head (4 query heads) checked in full against the oracle, plus sampled keys of every head."""

@@ -1,7 +1,8 @@
 """-m "not gpu": the sequence-sharded exchange protocol over a real process group — world size 2,
 gloo backend on CPU. Each rank owns a contiguous half of the retrieval zone, exchanges (H) per-head score
-histograms, (T) local top-k lists and (A) partial softmax states with all_gather, and must reproduce the
-unsharded oracle exactly (candidate set, top-k) and to fp64 rounding (attention)."""
+histograms, (T) local top-k lists and (A) partial softmax states with all_gather — and, in the fused variant
+(SURVEY §8(f3)), T and A as one exchange of (id, est, logit, value row) entries plus the hot partial — and must
+reproduce the unsharded oracle exactly (candidate set, top-k) and to fp64 rounding (attention)."""
 from __future__ import annotations
 
 import os
@@ -94,7 +95,41 @@ def _worker(rank, world, port, q_out):
         dist.all_gather(ps, part)
         valid = [p.numpy() for p in ps if np.isfinite(p[0])]
         o, lse = attention.merge_partials([p[0] for p in valid], [p[1] for p in valid], [p[2:] for p in valid])
-        q_out.put((rank, gidx, o, lse, len(cand)))
+        # fused T+A exchange: the local top-k entries travel with their logits and value rows,
+        # the last rank adds its hot-row partial; one all_gather, then every rank merges and attends alone
+        ok = idx >= 0
+        x_loc = Kf[idx[ok]] @ qf / np.sqrt(128)
+        ent = np.zeros((k, 3 + 128))
+        ent[:, 0], ent[:, 1] = -1, -np.inf
+        ent[: ok.sum(), 0], ent[: ok.sum(), 1], ent[: ok.sum(), 2] = idx[ok], val[ok], x_loc
+        ent[: ok.sum(), 3:] = Vf[idx[ok]]
+        hot = np.full(130, 0.0)
+        hot[0] = -np.inf
+        if rank == world - 1:
+            lh = Kh @ qf / np.sqrt(128)
+            mh = lh.max()
+            eh = np.exp(lh - mh)
+            hot = np.concatenate([[mh, eh.sum()], (eh[:, None] * Vh).sum(0) / eh.sum()])
+        msg = torch.from_numpy(np.concatenate([ent.ravel(), hot]))
+        ms = [torch.zeros_like(msg) for _ in range(world)]
+        dist.all_gather(ms, msg)
+        ents = np.concatenate([m_[: k * 131].numpy().reshape(k, 131) for m_ in ms])
+        ents = ents[ents[:, 0] >= 0]
+        order = sorted(range(len(ents)), key=lambda i: (-ents[i, 1], -ents[i, 0]))[:k]
+        sel = ents[order]
+        gidx_f = sel[:, 0].astype(np.int64)
+        xs = sel[:, 2]
+        mx = xs.max()
+        ex = np.exp(xs - mx)
+        parts_m, parts_l, parts_o = [mx], [ex.sum()], [(ex[:, None] * sel[:, 3:]).sum(0) / ex.sum()]
+        for m_ in ms:
+            hp = m_[k * 131:].numpy()
+            if np.isfinite(hp[0]):
+                parts_m.append(hp[0])
+                parts_l.append(hp[1])
+                parts_o.append(hp[2:])
+        o_f, lse_f = attention.merge_partials(parts_m, parts_l, parts_o)
+        q_out.put((rank, gidx, o, lse, len(cand), gidx_f, o_f, lse_f))
     finally:
         dist.destroy_process_group()
 
@@ -117,9 +152,11 @@ def test_two_rank_gloo_exchange_equals_unsharded():
     r0 = pipeline.decode_step(meta, qf[None], SB, 64)[0]
     o0, l0 = pipeline.attend(qf, Kf, Vf, r0["idx"], Kh, Vh)
     assert sum(r[4] for r in res) == r0["C"]
-    for rank, gidx, o, lse, _ in res:
+    for rank, gidx, o, lse, _, gidx_f, o_f, lse_f in res:
         assert list(gidx) == list(r0["idx"])
         assert np.allclose(o, o0, atol=1e-12) and abs(lse - l0) < 1e-12
+        assert list(gidx_f) == list(r0["idx"])  # fused exchange: same top-k, same attention
+        assert np.allclose(o_f, o0, atol=1e-12) and abs(lse_f - l0) < 1e-12
 
 
 if __name__ == "__main__":
