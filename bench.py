@@ -193,6 +193,10 @@ def run_ours(args):
     e1.record()
     torch.cuda.synchronize()
     enc_ms_layer = e0.elapsed_time(e1) / L
+    if args.inverted:  # inverted-list collision scan (same results; builds the postings now)
+        for ly in layers:
+            ly["ix"].set_postings(True)
+        torch.cuda.synchronize()
     if uva:  # the device copies were only needed to build the summaries
         for d in data:
             d["Kd"] = None
@@ -379,6 +383,7 @@ def run_ours(args):
                        "parallelism": f"seq-shard{world}" if world > 1 else "single",
                        "l2": "inputs > L2: 32 layer-distinct indices + K/V touched per step",
                        "rerank_weights": "fp16 (96 B records)" if args.w16 else "fp32 (128 B records)",
+                       "collision_scan": "inverted lists" if args.inverted else "dense",
                        "cuda_graph": use_graph},
             "roofline": roof,
             "scan_gbs": scan_gbs,
@@ -503,6 +508,7 @@ def main():
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--w16", action="store_true", help="fp16 rerank weights (96-byte records, AMB-20 / SURVEY f2)")
+    ap.add_argument("--inverted", action="store_true", help="inverted-list collision scan (SURVEY f4)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup) if args.impl == "ours" else args.warmup
     if args.impl == "reference":

@@ -239,6 +239,14 @@ pkv_status pkv_stream_decode(pkv_stream* s, const void* q, const void* k_new, co
 pkv_status pkv_stream_state(const pkv_stream* s, int64_t* n_retrieval, int32_t* n_local, int32_t* n_buffer,
                             const void** K_store, const void** V_store, const void** K_hot, const void** V_hot);
 
+/* Inverted-list collision variant ("collision processing scales with rho*n"): with
+ * enable = 1 the index also keeps, per chunk of 8192 keys and per subspace, its keys bucketed by centroid id
+ * (32 B per key and KV head, built now and maintained by encode_keys / append_decode_keys), and retrievals
+ * visit only the buckets of probed centroids instead of scanning every key's 16 ids. Scores, candidates and
+ * results are identical to the dense scan's. enable = 0 returns to the dense scan (buffers are kept).
+ * Errors: UNSUPPORTED if the capacity exceeds 256 chunks (2,097,152 keys), CUDA on allocation failure. */
+pkv_status pkv_index_set_postings(pkv_index* index, int32_t enable, cudaStream_t stream);
+
 /* Diagnostics: copy metadata of positions [start, start+count) into caller device buffers in the
  * canonical layout: ids uint8 [batch][n_kv][count][16] (subspace order), codes uint8
  * [batch][n_kv][count][64] (coordinate c -> byte c>>1, low nibble for even c; nibble = sign<<3 | idx),

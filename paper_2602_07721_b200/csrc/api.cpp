@@ -184,7 +184,9 @@ pkv_status phase_scan(pkv_index* ix, const void* q, const pkv_retrieve_params* p
   const int64_t n = ix->n;
   PKV_CUDA(launch_qprep(ix, q, p->probes_T, p->dbg_q_rot, s), "qprep");
   plan = plan_scan(ix, n > 0 ? n : 1);
-  if (n > 0) {
+  if (n > 0 && ix->postings) {
+    PKV_CUDA(launch_postings_scan(ix, n, score_stride(ix), s), "postings scan");
+  } else if (n > 0) {
     PKV_CUDA(launch_scan(ix, n, plan, s), "scan");
   } else {
     PKV_CUDA(cudaMemsetAsync(ix->ws->chunk_hist, 0,
@@ -308,6 +310,7 @@ pkv_status pkv_index_create(const pkv_config* cfg, int32_t batch, int64_t capaci
   if (st == PKV_OK) {
     e = init_scan_attrs();
     if (e == cudaSuccess) e = init_rerank_attrs();
+    if (e == cudaSuccess) e = init_postings_attrs();
     if (e != cudaSuccess) st = cuda_status(e, "cudaFuncSetAttribute");
   }
   if (st != PKV_OK) {
@@ -328,7 +331,35 @@ pkv_status pkv_index_destroy(pkv_index* ix) {
   release_workspace(ix->ws);
   cudaFree(ix->ids);
   cudaFree(ix->rec);
+  cudaFree(ix->post_off);
+  cudaFree(ix->post_key);
   delete ix;
+  return PKV_OK;
+}
+
+pkv_status pkv_index_set_postings(pkv_index* ix, int32_t enable, cudaStream_t stream) {
+  if (!ix) return set_error(PKV_ERR_INVALID_ARG, "pkv_index_set_postings: null index");
+  DeviceGuard g(ix->device);
+  if (!enable) {
+    ix->postings = false;
+    return PKV_OK;
+  }
+  if (!ix->post_off) {
+    const int64_t units = (int64_t)ix->batch * ix->cfg.n_kv_heads;
+    const int64_t nch = (ix->cap + POST_CHUNK - 1) / POST_CHUNK;
+    if (nch > MAX_CHUNKS) return set_error(PKV_ERR_UNSUPPORTED, "pkv_index_set_postings: capacity > 256 chunks of 8192");
+    cudaError_t e = cudaMalloc(&ix->post_off, (size_t)units * nch * NB * (NC + 1) * 2);
+    if (e == cudaSuccess) e = cudaMalloc(&ix->post_key, (size_t)units * nch * NB * POST_CHUNK * 2);
+    if (e != cudaSuccess) {
+      cudaFree(ix->post_off);
+      cudaFree(ix->post_key);
+      ix->post_off = nullptr;
+      ix->post_key = nullptr;
+      return cuda_status(e, "pkv_index_set_postings");
+    }
+  }
+  ix->postings = true;
+  PKV_CUDA(launch_postings_build(ix, 0, (ix->n + POST_CHUNK - 1) / POST_CHUNK, stream), "postings");
   return PKV_OK;
 }
 
@@ -363,6 +394,7 @@ pkv_status encode_keys(pkv_index* ix, const void* K, int64_t sb, int64_t sh, int
   DeviceGuard g(ix->device);
   if (n > 0) PKV_CUDA(launch_encode(ix, K, sb, sh, st, 0, n, stream), "encode");
   ix->n = n;
+  if (ix->postings) PKV_CUDA(launch_postings_build(ix, 0, (n + POST_CHUNK - 1) / POST_CHUNK, stream), "postings");
   return PKV_OK;
 }
 
@@ -377,7 +409,10 @@ pkv_status append_decode_keys(pkv_index* ix, const void* K, int64_t sb, int64_t 
   }
   DeviceGuard g(ix->device);
   if (t > 0) PKV_CUDA(launch_encode(ix, K, sb, sh, st, ix->n, t, stream), "encode(append)");
+  const int64_t first = ix->n / POST_CHUNK;  // the partial chunk and the new ones are rebuilt
   ix->n += t;
+  if (ix->postings && t > 0)
+    PKV_CUDA(launch_postings_build(ix, first, (ix->n + POST_CHUNK - 1) / POST_CHUNK, stream), "postings(append)");
   return PKV_OK;
 }
 

@@ -77,6 +77,11 @@ struct pkv_index {
   int64_t n = 0;
   uint8_t* ids = nullptr;   // [batch][n_kv][cap][16]; row of key t rotated left by (t mod 16) bytes
   uint8_t* rec = nullptr;   // [batch][n_kv][cap][rec_bytes]: 64 B nibbles + 16 x fp32 w' (or 16 x fp16 w')
+  // inverted lists (pkv_index_set_postings): per (b, kv, chunk of POST_CHUNK keys, subspace)
+  // bucket offsets u16 [257] and the chunk's key offsets u16 [POST_CHUNK] sorted by centroid id
+  bool postings = false;
+  uint16_t* post_off = nullptr;
+  uint16_t* post_key = nullptr;
   pkv::Workspace* ws = nullptr;
   pkv::Comm* comm = nullptr;
   int rank = 0, world = 1;
@@ -122,11 +127,18 @@ cudaError_t launch_export(const pkv_index* ix, int64_t start, int64_t count, uin
                           float* w, cudaStream_t stream);
 cudaError_t launch_qprep(const pkv_index* ix, const void* q, int T, float* dbg_q_rot, cudaStream_t stream);
 
+constexpr int POST_CHUNK = 8192;  // keys per inverted-list chunk (u16 offsets)
+
 struct ScanPlan {
   int nchunks;
   int64_t chunk;  // keys per chunk (multiple of 32)
 };
 ScanPlan plan_scan(const pkv_index* ix, int64_t n);
+int64_t score_stride(const pkv_index* ix);
+cudaError_t init_postings_attrs();
+cudaError_t launch_postings_build(const pkv_index* ix, int64_t chunk0, int64_t chunk1, cudaStream_t stream);
+// inverted-list variant of the scan: same scores / per-chunk histograms, chunks of POST_CHUNK keys
+cudaError_t launch_postings_scan(const pkv_index* ix, int64_t n, int64_t sstride, cudaStream_t stream);
 cudaError_t init_scan_attrs();
 cudaError_t init_rerank_attrs();
 cudaError_t launch_scan(const pkv_index* ix, int64_t n, const ScanPlan& plan, cudaStream_t stream);

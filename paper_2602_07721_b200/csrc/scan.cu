@@ -10,6 +10,7 @@
 //                  in shared memory; per-chunk totals to global (deterministic, no global atomics).
 // select_kernel    threshold s* = max{s : #(score >= s) >= C} per query head from cumulative chunk histograms,
 //                  ties in the s* bucket handed out newest first (AMB-12), then the chunk's candidate ids.
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -501,9 +502,15 @@ cudaError_t init_scan_attrs() {
 
 // packed-score row stride: the capacity rounded to 4 keys, so every row is 16-byte aligned for the select's
 // vector loads
-static int64_t score_stride(const pkv_index* ix) { return (ix->cap + 3) & ~(int64_t)3; }
+int64_t score_stride(const pkv_index* ix) { return (ix->cap + 3) & ~(int64_t)3; }
 
 ScanPlan plan_scan(const pkv_index* ix, int64_t n) {
+  if (ix->postings) {  // the inverted-list scan works on fixed chunks
+    ScanPlan p;
+    p.chunk = POST_CHUNK;
+    p.nchunks = (int)std::max<int64_t>(1, (n + POST_CHUNK - 1) / POST_CHUNK);
+    return p;
+  }
   // One 1024-thread CTA per SM (~114 KB smem): never more CTAs than SMs, so there is no second wave.
   ScanPlan p;
   const int units = ix->batch * ix->cfg.n_kv_heads;

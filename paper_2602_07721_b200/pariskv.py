@@ -53,6 +53,7 @@ _sigs = {
     "pkv_index_destroy": [_vp],
     "pkv_index_len": [_vp, ctypes.POINTER(_i64)],
     "pkv_index_share_workspace": [_vp, _vp],
+    "pkv_index_set_postings": [_vp, _i32, _vp],
     "encode_keys": [_vp, _vp, _i64, _i64, _i64, _i64, _vp],
     "append_decode_keys": [_vp, _vp, _i64, _i64, _i64, _i64, _vp],
     "retrieve_topk": [_vp, _vp, ctypes.POINTER(RetrieveParams), _vp, _vp, _vp],
@@ -178,6 +179,10 @@ class Index:
         n = _i64(0)
         _check(_lib.pkv_index_len(self.handle, ctypes.byref(n)))
         return int(n.value)
+
+    def set_postings(self, enable: bool = True, stream=None):
+        """Inverted-list collision variant: same results, buckets of probed centroids only."""
+        _check(_lib.pkv_index_set_postings(self.handle, int(enable), _stream(stream)))
 
     def share_workspace(self, donor: "Index"):
         _check(_lib.pkv_index_share_workspace(self.handle, donor.handle))

@@ -33,7 +33,7 @@ def prewait_loads(obj):
 
 def main():
     allres = {}
-    for f in ("qprep.cu.o", "scan.cu.o", "rerank.cu.o", "attend.cu.o"):
+    for f in ("qprep.cu.o", "scan.cu.o", "rerank.cu.o", "attend.cu.o", "postings.cu.o"):
         p = os.path.join(BUILD, f)
         if os.path.exists(p):
             allres.update(prewait_loads(p))

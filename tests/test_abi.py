@@ -94,7 +94,7 @@ def test_no_predecessor_output_read_before_griddepcontrol_wait(pkv):
     spec.loader.exec_module(mod)
     build_dir = os.path.join(ROOT, "paper_2602_07721_b200", "build")
     res = {}
-    for f in ("qprep.cu.o", "scan.cu.o", "rerank.cu.o", "attend.cu.o"):
+    for f in ("qprep.cu.o", "scan.cu.o", "rerank.cu.o", "attend.cu.o", "postings.cu.o"):
         res.update(mod.prewait_loads(os.path.join(build_dir, f)))
     assert len(res) >= 10, sorted(res)
 
