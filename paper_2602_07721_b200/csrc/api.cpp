@@ -208,6 +208,31 @@ pkv_status phase_select_rerank(pkv_index* ix, const pkv_retrieve_params* p, cons
   return PKV_OK;
 }
 
+// Key encoder: by default the half-warp kernel (encode.cu, 464 us per 1M keys at 128K); PKV_ENCODER=tc selects the
+// tensor-core kernel (encode_tc.cu: exact 8-bit-digit GEMMs, 3.5x slower in round 1 — its digit split and the
+// integer recombination cost more ALU work than the butterflies they replace) with the half-warp kernel for the
+// keys it hands back. Read at every call (tests switch it).
+bool use_tc_encoder() {
+  const char* e = getenv("PKV_ENCODER");
+  return e && std::string(e) == "tc";
+}
+
+pkv_status run_encoder(pkv_index* ix, const void* K, int64_t sb, int64_t sh, int64_t st, int64_t t0, int64_t count,
+                       cudaStream_t stream) {
+  if (count <= 0) return PKV_OK;
+  if (!use_tc_encoder()) {
+    PKV_CUDA(launch_encode(ix, K, sb, sh, st, t0, count, stream), "encode");
+    return PKV_OK;
+  }
+  const int64_t units = (int64_t)ix->batch * ix->cfg.n_kv_heads;
+  if (!ix->enc_fb) PKV_CUDA(cudaMalloc(&ix->enc_fb, (size_t)(units * ix->cap + 1) * 4), "encoder list");
+  int32_t* fb_n = ix->enc_fb + units * ix->cap;
+  PKV_CUDA(cudaMemsetAsync(fb_n, 0, 4, stream), "encoder list reset");
+  PKV_CUDA(launch_encode_tc(ix, K, sb, sh, st, t0, count, ix->enc_fb, fb_n, stream), "encode (tensor cores)");
+  PKV_CUDA(launch_encode_list(ix, K, sb, sh, st, t0, count, ix->enc_fb, fb_n, stream), "encode (fallback)");
+  return PKV_OK;
+}
+
 pkv_status check_retrieve(const pkv_index* ix, const void* q, const pkv_retrieve_params* p, int64_t n_global,
                           const int32_t* out_idx, const float* out_est) {
   if (!ix || !q || !p || !out_idx || !out_est) return set_error(PKV_ERR_INVALID_ARG, "retrieve_topk: null pointer");
@@ -311,6 +336,7 @@ pkv_status pkv_index_create(const pkv_config* cfg, int32_t batch, int64_t capaci
     e = init_scan_attrs();
     if (e == cudaSuccess) e = init_rerank_attrs();
     if (e == cudaSuccess) e = init_postings_attrs();
+    if (e == cudaSuccess) e = init_encode_tc_attrs();
     if (e != cudaSuccess) st = cuda_status(e, "cudaFuncSetAttribute");
   }
   if (st != PKV_OK) {
@@ -333,6 +359,7 @@ pkv_status pkv_index_destroy(pkv_index* ix) {
   cudaFree(ix->rec);
   cudaFree(ix->post_off);
   cudaFree(ix->post_key);
+  cudaFree(ix->enc_fb);
   delete ix;
   return PKV_OK;
 }
@@ -392,7 +419,10 @@ pkv_status encode_keys(pkv_index* ix, const void* K, int64_t sb, int64_t sh, int
     if (s != PKV_OK) return s;
   }
   DeviceGuard g(ix->device);
-  if (n > 0) PKV_CUDA(launch_encode(ix, K, sb, sh, st, 0, n, stream), "encode");
+  if (n > 0) {
+    pkv_status se = run_encoder(ix, K, sb, sh, st, 0, n, stream);
+    if (se != PKV_OK) return se;
+  }
   ix->n = n;
   if (ix->postings) PKV_CUDA(launch_postings_build(ix, 0, (n + POST_CHUNK - 1) / POST_CHUNK, stream), "postings");
   return PKV_OK;
@@ -408,7 +438,10 @@ pkv_status append_decode_keys(pkv_index* ix, const void* K, int64_t sb, int64_t 
     if (s != PKV_OK) return s;
   }
   DeviceGuard g(ix->device);
-  if (t > 0) PKV_CUDA(launch_encode(ix, K, sb, sh, st, ix->n, t, stream), "encode(append)");
+  if (t > 0) {
+    pkv_status se = run_encoder(ix, K, sb, sh, st, ix->n, t, stream);
+    if (se != PKV_OK) return se;
+  }
   const int64_t first = ix->n / POST_CHUNK;  // the partial chunk and the new ones are rebuilt
   ix->n += t;
   if (ix->postings && t > 0)

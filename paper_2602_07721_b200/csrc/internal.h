@@ -79,6 +79,7 @@ struct pkv_index {
   uint8_t* rec = nullptr;   // [batch][n_kv][cap][rec_bytes]: 64 B nibbles + 16 x fp32 w' (or 16 x fp16 w')
   // inverted lists (pkv_index_set_postings): per (b, kv, chunk of POST_CHUNK keys, subspace)
   // bucket offsets u16 [257] and the chunk's key offsets u16 [POST_CHUNK] sorted by centroid id
+  int32_t* enc_fb = nullptr;  // [batch*n_kv*cap + 1]: tensor-core encoder fallback list, count at the end
   bool postings = false;
   uint16_t* post_off = nullptr;
   uint16_t* post_key = nullptr;
@@ -121,6 +122,13 @@ extern std::atomic<uint64_t> g_launches;
 void prop1_levels(int m, double out_levels[8]);
 
 // Launchers (*.cu). All enqueue on `stream` and return the launch error.
+// tensor-core encoder (encode_tc.cu): keys outside its exact range are appended to fb_list (count fb_count)
+cudaError_t init_encode_tc_attrs();
+cudaError_t launch_encode_tc(const pkv_index* ix, const void* K, int64_t sb, int64_t sh, int64_t st, int64_t t0,
+                             int64_t count, int32_t* fb_list, int32_t* fb_count, cudaStream_t stream);
+// half-warp encoder over a device list (entries bh * count + tt)
+cudaError_t launch_encode_list(const pkv_index* ix, const void* K, int64_t sb, int64_t sh, int64_t st, int64_t t0,
+                               int64_t count, const int32_t* list, const int32_t* list_n, cudaStream_t stream);
 cudaError_t launch_encode(const pkv_index* ix, const void* K, int64_t sb, int64_t sh, int64_t st, int64_t t0,
                           int64_t count, cudaStream_t stream);
 cudaError_t launch_export(const pkv_index* ix, int64_t start, int64_t count, uint8_t* ids, uint8_t* codes,

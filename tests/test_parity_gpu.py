@@ -528,3 +528,19 @@ def test_inverted_list_scan_equals_dense(pkv, n, k):
         meta = oracle_meta(bf16_f64(Kall[0, 3]))
         r = oracle_retrieval(meta, bf16_f64(q[0, 13]), db["T"], db["C"], k)
         assert np.array_equal(db["scores"][0, 13].cpu().numpy().astype(np.int64), r["score"])
+
+
+def test_tensor_core_encoder_bit_exact(pkv, monkeypatch):
+    """The tcgen05 encoder variant (PKV_ENCODER=tc, encode_tc.cu): exact digit GEMMs for the rotation; ids and
+    codes bit-exact against the oracle, including keys it must hand to the half-warp encoder (wide range, zero,
+    subnormal) and partial tiles."""
+    monkeypatch.setenv("PKV_ENCODER", "tc")
+    K, q, V = make_problem(81, 2, 8, 2, 3000)
+    K[0, 0, 5] = 0
+    K[0, 0, 6, 16:24] = 0
+    K[1, 1, 10:40, 3] = 1e-9
+    K[1, 0, 40:60, 100] = 3e-30
+    K[0, 1, 60:70, :] = torch.randn(10, 128, device="cuda").to(torch.bfloat16) * 1e-20
+    run_and_check(pkv, K, q, V, k=64, n_hot=16)
+    K, q, V = make_problem(82, 1, 4, 1, 333, plant=False)
+    run_and_check(pkv, K, q, V, k=32, cfg=w16_cfg(pkv, 4, 1))
