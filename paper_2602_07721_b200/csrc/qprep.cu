@@ -49,49 +49,67 @@ __global__ void __launch_bounds__(QP_THREADS) qprep_kernel(const uint16_t* q, in
   pdl_wait();  // the query of this layer follows the previous layer's work
   pdl_trigger();
   phase_mark(K_QPREP, 1);
-  // every warp redoes the (tiny) butterflies so no cross-warp exchange is needed
-  const uint16_t* qh = q + ((int64_t)b * cfg.n_q + h) * D;
-  const uint2 raw = ldg_v2(qh + 4 * lane);
-  const float qf[4] = {bf16_lo(raw.x), bf16_hi(raw.x), bf16_lo(raw.y), bf16_hi(raw.y)};
-  double v[4];
-  float qn2 = 0.f;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    qn2 = fmaf(qf[i], qf[i], qn2);
-    v[i] = sign_bit(cfg, 4 * lane + i) ? -(double)qf[i] : (double)qf[i];
-  }
-#pragma unroll
-  for (int x = 1; x < 4; x <<= 1) {
+  // warp 0 rotates the query (fp64 butterflies) and publishes this subspace's 8 coordinates and 1/||y'||
+  __shared__ double s_yb[8];
+  __shared__ double s_inv;
+  if (warp == 0) {
+    const uint16_t* qh = q + ((int64_t)b * cfg.n_q + h) * D;
+    const uint2 raw = ldg_v2(qh + 4 * lane);
+    const float qf[4] = {bf16_lo(raw.x), bf16_hi(raw.x), bf16_lo(raw.y), bf16_hi(raw.y)};
+    double v[4];
+    float qn2 = 0.f;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      if ((i & x) == 0) {
-        const double a = v[i], c = v[i + x];
-        v[i] = __dadd_rn(a, c);
-        v[i + x] = __dsub_rn(a, c);
+      qn2 = fmaf(qf[i], qf[i], qn2);
+      v[i] = sign_bit(cfg, 4 * lane + i) ? -(double)qf[i] : (double)qf[i];
+    }
+#pragma unroll
+    for (int x = 1; x < 4; x <<= 1) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if ((i & x) == 0) {
+          const double a2 = v[i], c = v[i + x];
+          v[i] = __dadd_rn(a2, c);
+          v[i + x] = __dsub_rn(a2, c);
+        }
       }
     }
-  }
 #pragma unroll
-  for (int x = 1; x < 32; x <<= 1) {
-    const bool upper = (lane & x) != 0;
+    for (int x = 1; x < 32; x <<= 1) {
+      const bool upper = (lane & x) != 0;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const double o = shfl_xor_d(v[i], x);
-      v[i] = upper ? __dsub_rn(o, v[i]) : __dadd_rn(v[i], o);
+      for (int i = 0; i < 4; ++i) {
+        const double o = shfl_xor_d(v[i], x);
+        v[i] = upper ? __dsub_rn(o, v[i]) : __dadd_rn(v[i], o);
+      }
     }
-  }
-  double yn2 = 0.0;
+    double yn2 = 0.0;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) yn2 = fma(v[i], v[i], yn2);
+    for (int i = 0; i < 4; ++i) yn2 = fma(v[i], v[i], yn2);
 #pragma unroll
-  for (int x = 16; x > 0; x >>= 1) {
-    yn2 += shfl_xor_d(yn2, x);
-    qn2 += __shfl_xor_sync(0xffffffffu, qn2, x);
+    for (int x = 16; x > 0; x >>= 1) {
+      yn2 += shfl_xor_d(yn2, x);
+      qn2 += __shfl_xor_sync(0xffffffffu, qn2, x);
+    }
+    const double inv_yn = yn2 > 0.0 ? 1.0 / sqrt(yn2) : 0.0;
+    if (lane == 2 * sb || lane == 2 * sb + 1) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) s_yb[4 * (lane - 2 * sb) + i] = v[i];
+      float* qr = qrot + ((int64_t)b * cfg.n_q + h) * D;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        qr[4 * lane + i] = (float)(v[i] * inv_yn);
+        if (dbg_q_rot) dbg_q_rot[((int64_t)b * cfg.n_q + h) * D + 4 * lane + i] = (float)(v[i] * inv_yn);
+      }
+    }
+    if (lane == 0) s_inv = inv_yn;
+    if (sb == 0 && lane == 0) qnorm[(int64_t)b * cfg.n_q + h] = sqrtf(qn2);
   }
-  const double inv_yn = yn2 > 0.0 ? 1.0 / sqrt(yn2) : 0.0;
+  __syncthreads();
   double yb[8];
 #pragma unroll
-  for (int j = 0; j < 8; ++j) yb[j] = __shfl_sync(0xffffffffu, v[j & 3], 2 * sb + (j >> 2));
+  for (int j = 0; j < 8; ++j) yb[j] = s_yb[j];
+  const double inv_yn = s_inv;
   // rerank table rows for coordinates 8sb..8sb+7 (one entry per thread): sign(n) L[n&7] q~_{8sb+j}
   {
     const int j = t >> 4, nb = t & 15;
@@ -102,15 +120,6 @@ __global__ void __launch_bounds__(QP_THREADS) qprep_kernel(const uint16_t* q, in
     const float L = cfg.levels[nb & 7];
     rtab[(((int64_t)b * cfg.n_q + h) * D + 8 * sb) * 16 + t] = (nb & 8) ? L * qt : -L * qt;
   }
-  if (t < 32 && (lane == 2 * sb || lane == 2 * sb + 1)) {
-    float* qr = qrot + ((int64_t)b * cfg.n_q + h) * D;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      qr[4 * lane + i] = (float)(v[i] * inv_yn);
-      if (dbg_q_rot) dbg_q_rot[((int64_t)b * cfg.n_q + h) * D + 4 * lane + i] = (float)(v[i] * inv_yn);
-    }
-  }
-  if (sb == 0 && t == 0) qnorm[(int64_t)b * cfg.n_q + h] = sqrtf(qn2);
   phase_mark(K_QPREP, 2);
   // scores of the two centroids at positions 2t, 2t+1 (ids = positions before sorting)
   KV e[2];
