@@ -5,8 +5,8 @@
 //
 // Grid (16 subspaces, n_q heads, batch), 128 threads. Exact contract shared with the oracle (AMB-9):
 // y' = fp64 butterflies of s (.) q; score_c = fp64 left-to-right sum of +-y'_j from 0.0; order (score desc,
-// id asc). Each thread owns 2 of the 256 (key, id) pairs; the bitonic network runs in registers and warp
-// shuffles, and only its 3 stages with pair distance >= 64 go through shared memory.
+// id asc). The complement symmetry score(255-c) = -score(c) halves the sort to 128 "leaders", one per thread;
+// the bitonic network runs in registers and warp shuffles, only its 3 stages with distance >= 32 in smem.
 #include "common.cuh"
 
 namespace pkv {
@@ -40,8 +40,8 @@ __global__ void __launch_bounds__(QP_THREADS) qprep_kernel(const uint16_t* q, in
                                                           uint32_t* lut, float* rtab,
                                                           float* qnorm, float* qrot,
                                                           float* dbg_q_rot) {
-  __shared__ unsigned long long sk[NC];
-  __shared__ uint32_t si[NC];
+  __shared__ unsigned long long sk[NC / 2];
+  __shared__ uint32_t si[NC / 2];
   phase_mark(K_QPREP, 0);
   const int sb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -121,53 +121,49 @@ __global__ void __launch_bounds__(QP_THREADS) qprep_kernel(const uint16_t* q, in
     rtab[(((int64_t)b * cfg.n_q + h) * D + 8 * sb) * 16 + t] = (nb & 8) ? L * qt : -L * qt;
   }
   phase_mark(K_QPREP, 2);
-  // scores of the two centroids at positions 2t, 2t+1 (ids = positions before sorting)
-  KV e[2];
-#pragma unroll
-  for (int u = 0; u < 2; ++u) {
-    const uint32_t c = 2u * t + u;
+  // Complement symmetry: score(255 - c) == -score(c) exactly (every partial sum of the left-to-right fp64 sum
+  // is negated, round-to-nearest is odd-symmetric and an exact zero is +0.0 either way). So the (score desc,
+  // id asc) order of all 256 is: the 128 "leaders" (of each pair {c, 255-c} the one that comes first) in
+  // order, then their complements in reverse order -> rank(255 - c) = 255 - rank(c). Only the leaders are
+  // sorted, one per thread. Thread t owns the pair {t, 255 - t}; t < 128 <= 255 - t breaks a zero tie.
+  KV e;
+  {
     double acc = 0.0;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc = __dadd_rn(acc, ((c >> j) & 1u) ? yb[j] : -yb[j]);
-    e[u].k = ~ord_f64(acc);  // ascending key == descending score; ties by ascending id
-    e[u].id = c;
+    for (int j = 0; j < 8; ++j) acc = __dadd_rn(acc, ((t >> j) & 1) ? yb[j] : -yb[j]);
+    const bool neg = acc < 0.0;
+    e.k = ~ord_f64(neg ? -acc : acc);  // ascending key == descending score; ties by ascending id
+    e.id = neg ? (uint32_t)(NC - 1 - t) : (uint32_t)t;
   }
-  const int p0 = 2 * t, p1 = 2 * t + 1;
 #pragma unroll
-  for (int k = 2; k <= NC; k <<= 1) {
+  for (int k = 2; k <= NC / 2; k <<= 1) {
 #pragma unroll
     for (int j = k >> 1; j > 0; j >>= 1) {
-      if (j == 1) {
-        const KV a0 = e[0], a1 = e[1];
-        ce(e[0], a1, p0, k, 1);
-        ce(e[1], a0, p1, k, 1);
-      } else if (j <= 32) {
-        const KV o0 = shfl_kv(e[0], j >> 1), o1 = shfl_kv(e[1], j >> 1);
-        ce(e[0], o0, p0, k, j);
-        ce(e[1], o1, p1, k, j);
+      KV o;
+      if (j < 32) {
+        o = shfl_kv(e, j);
       } else {
-        sk[p0] = e[0].k;
-        sk[p1] = e[1].k;
-        si[p0] = e[0].id;
-        si[p1] = e[1].id;
+        sk[t] = e.k;
+        si[t] = e.id;
         __syncthreads();
-        const KV o0{sk[p0 ^ j], si[p0 ^ j]}, o1{sk[p1 ^ j], si[p1 ^ j]};
+        o = KV{sk[t ^ j], si[t ^ j]};
         __syncthreads();
-        ce(e[0], o0, p0, k, j);
-        ce(e[1], o1, p1, k, j);
       }
+      ce(e, o, t, k, j);
     }
   }
   phase_mark(K_QPREP, 3);
-  // position == rank; write this head's bonus byte of the packed LUT entry of each centroid
+  // position t == rank of leader e.id, 255 - t == rank of its complement; write this head's bonus byte of the
+  // packed LUT entry of both
   const int chunk = max(1, T / cfg.n_tiers);
   uint8_t* lb = reinterpret_cast<uint8_t*>(lut + ((int64_t)b * cfg.n_kv + g) * NC * NB);
 #pragma unroll
   for (int u = 0; u < 2; ++u) {
-    const int rank = 2 * t + u;
+    const int rank = u ? NC - 1 - t : t;
+    const uint32_t id = u ? NC - 1 - e.id : e.id;
     int bonus = 0;
     if (rank < T) bonus = cfg.tier_bonus[min(rank / chunk, cfg.n_tiers - 1)];
-    lb[((int64_t)e[u].id * NB + sb) * 4 + hh] = (uint8_t)bonus;
+    lb[((int64_t)id * NB + sb) * 4 + hh] = (uint8_t)bonus;
   }
   phase_mark(K_QPREP, 4);
 }

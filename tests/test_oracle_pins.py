@@ -433,3 +433,21 @@ def test_p8_probe_ranking_exact_ties_by_ascending_id():
         rank = codebook.rank_centroids(codebook.centroid_scores(y))
         ex = [c for c, _ in codebook.brute_probe_list(y, 256)]
         assert list(np.argsort(rank)) == ex
+
+
+def test_p8_complement_symmetry_of_ranking():
+    """score(255 - c) == -score(c) bit-exactly for the AMB-9 left-to-right fp64 sum (zeros are +0.0), so
+    rank(255 - c) == 255 - rank(c): the property the CUDA query prep uses to sort only 128 leaders
+    (qprep). Random, wide-range, tie-heavy and all-zero subspaces."""
+    rng = np.random.default_rng(12)
+    ys = [rng.standard_normal(8) for _ in range(50)]
+    ys += [rng.standard_normal(8) * 10.0 ** rng.integers(-30, 30, 8) for _ in range(50)]
+    ys += [np.array(v, dtype=np.float64) for v in
+           ([0, 1, -1, 2, 0, -2, 3, 1], [1, 1, 1, 1, -1, -1, -1, -1], [0] * 8, [1e300, 1e-300, -1e300, 0, 0, 1, 1, 1])]
+    c = np.arange(256)
+    for y in ys:
+        s = codebook.centroid_scores(y)
+        assert np.array_equal(s[255 - c], -s[c])
+        assert not np.any(np.signbit(s[s == 0]))
+        rank = codebook.rank_centroids(s)
+        assert np.array_equal(rank[255 - c], 255 - rank[c])
