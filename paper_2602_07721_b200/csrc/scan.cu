@@ -208,6 +208,23 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(
   const int b = bh / n_kv, g = bh % n_kv;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t* chb = chunk_hist + (int64_t)bh * MAX_CHUNKS * GMAX * HB;
+  // B's input does not depend on the threshold: the first VB groups of this warp's segment are loaded now, so
+  // their L2 latency overlaps A1-A3. Warp segments are whole multiples of 128 keys: a lane reads 4 consecutive
+  // keys as one 16-byte vector.
+  const uint32_t t_begin = (uint32_t)j * (uint32_t)chunk;
+  const uint32_t t_end = (uint32_t)min(n, (int64_t)t_begin + chunk);
+  const uint32_t len = t_end - t_begin;
+  const uint32_t seg = ((len + 32 * 128 - 1) / (32 * 128)) * 128;
+  const uint32_t seg0 = t_begin + warp * seg;
+  const uint32_t seg1 = min(t_end, seg0 + seg);
+  const uint32_t* sc = scores + (int64_t)bh * cap;
+  uint4 vreg[VB];
+  const uint32_t ngrp = (seg1 > seg0) ? (seg1 - seg0 + 127) / 128 : 0;  // 128-key groups of this warp
+#pragma unroll
+  for (int k2 = 0; k2 < VB; ++k2) {
+    const uint32_t t = seg0 + 128u * k2 + 4u * lane;
+    vreg[k2] = (t < seg1) ? *reinterpret_cast<const uint4*>(sc + t) : make_uint4(0, 0, 0, 0);
+  }
   // A1: local and global cumulative totals. Thread (half, hh, s): half of the chunks, loads batched 16 at a time
   // so that many L2 requests are in flight (a load->add chain per chunk would serialise their latency).
   __shared__ uint32_t Hpart[GMAX][HB];
@@ -322,14 +339,6 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(
   // Packed comparisons (scores <= 127, 4 query heads per u32): with K_gt = 0x7f - s*, K_ge = 0x80 - s* per byte,
   // bit 7 of byte h of (score + K_gt) is [score_h > s*_h] and of (score + K_ge) is [score_h >= s*_h] — no carries
   // cross bytes. Unused heads get s* = 127, which no score reaches.
-  const uint32_t t_begin = (uint32_t)j * (uint32_t)chunk;
-  const uint32_t t_end = (uint32_t)min(n, (int64_t)t_begin + chunk);
-  const uint32_t len = t_end - t_begin;
-  // warp segments are whole multiples of 128 keys: a lane reads 4 consecutive keys as one 16-byte vector
-  const uint32_t seg = ((len + 32 * 128 - 1) / (32 * 128)) * 128;
-  const uint32_t seg0 = t_begin + warp * seg;
-  const uint32_t seg1 = min(t_end, seg0 + seg);
-  const uint32_t* sc = scores + (int64_t)bh * cap;
   uint32_t kgt = 0, kge = 0;
 #pragma unroll
   for (int hh = 0; hh < GMAX; ++hh) {
@@ -339,14 +348,14 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(
   }
   // pass 1: per-head counts of this warp's segment; lane l reads keys 4l..4l+3 of each 128-key group, VB groups
   // (16 keys per lane) in flight, kept in registers for pass 2 when the segment is short enough (the 128K case)
-  uint4 vreg[VB];
-  const uint32_t ngrp = (seg1 > seg0) ? (seg1 - seg0 + 127) / 128 : 0;  // 128-key groups of this warp
   uint32_t tot_gt[GMAX] = {0, 0, 0, 0}, tot_eq[GMAX] = {0, 0, 0, 0};
   for (uint32_t g0 = 0; g0 < ngrp; g0 += VB) {
+    if (g0 > 0) {
 #pragma unroll
-    for (int k2 = 0; k2 < VB; ++k2) {
-      const uint32_t t = seg0 + 128u * (g0 + k2) + 4u * lane;
-      vreg[k2] = (t < seg1) ? *reinterpret_cast<const uint4*>(sc + t) : make_uint4(0, 0, 0, 0);
+      for (int k2 = 0; k2 < VB; ++k2) {
+        const uint32_t t = seg0 + 128u * (g0 + k2) + 4u * lane;
+        vreg[k2] = (t < seg1) ? *reinterpret_cast<const uint4*>(sc + t) : make_uint4(0, 0, 0, 0);
+      }
     }
     uint32_t cgt = 0, ceq = 0;  // per-byte counts (<= 16 per batch: no carries)
 #pragma unroll
