@@ -96,7 +96,7 @@ pkv_status alloc_workspace(Workspace* ws, int batch, int n_q, int n_kv, int64_t 
   ws->n_kv = n_kv;
   ws->cap = cap;
   const size_t bq = (size_t)batch * n_q, bk = (size_t)batch * n_kv;
-  size_t sizes[16] = {
+  size_t sizes[19] = {
       bk * NC * NB * 4,                                  // lut
       bq * D * 16 * 4,                                   // rtab
       bq * 4,                                            // qnorm
@@ -112,7 +112,10 @@ pkv_status alloc_workspace(Workspace* ws, int batch, int n_q, int n_kv, int64_t 
       (size_t)MAX_RANKS * bq * MAX_SPLITS * PART * 4,    // part
       bk * 4,                                            // ticket
       (size_t)MAX_RANKS * bq * MAX_TOPK * 4,             // seg_est
-      (size_t)MAX_RANKS * bq * MAX_TOPK * 4};            // seg_idx
+      (size_t)MAX_RANKS * bq * MAX_TOPK * 4,             // seg_idx
+      bk * 4,                                            // ucount
+      bk * (size_t)cap * 4,                              // uid
+      bk * (size_t)cap * 16};                            // upos
   size_t total = 0;
   for (size_t s : sizes) total += align_up(s);
   void* base = nullptr;
@@ -141,6 +144,9 @@ pkv_status alloc_workspace(Workspace* ws, int batch, int n_q, int n_kv, int64_t 
   ws->ticket = reinterpret_cast<unsigned int*>(take(13));
   ws->seg_est = reinterpret_cast<float*>(take(14));
   ws->seg_idx = reinterpret_cast<int32_t*>(take(15));
+  ws->ucount = reinterpret_cast<unsigned int*>(take(16));
+  ws->uid = reinterpret_cast<int32_t*>(take(17));
+  ws->upos = reinterpret_cast<int32_t*>(take(18));
   ws->base = base;
   ws->bytes = total;
   e = cudaMemset(base, 0, total);

@@ -57,6 +57,11 @@ struct Workspace {
   unsigned int* ticket = nullptr; // [batch][n_kv] split-completion counters of the fused attention merge
   float* seg_est = nullptr;       // [MAX_RANKS][batch][n_q][MAX_TOPK] segmented top-k of long candidate lists
   int32_t* seg_idx = nullptr;
+  // GQA-union rerank: per (sequence, KV head) the keys that are a candidate of at least one of
+  // its query heads, each with its candidate position in every head's list (-1: not a candidate of that head)
+  unsigned int* ucount = nullptr; // [batch][n_kv] union sizes (zeroed by qprep, counted by select)
+  int32_t* uid = nullptr;         // [batch][n_kv][cap] local key index
+  int32_t* upos = nullptr;        // [batch][n_kv][cap][4] candidate positions per query head of the group
   void* base = nullptr;
   size_t bytes = 0;
   int refs = 1;
@@ -157,6 +162,10 @@ cudaError_t launch_head_hist(const pkv_index* ix, const ScanPlan& plan, uint32_t
 cudaError_t launch_select(const pkv_index* ix, int64_t n, const ScanPlan& plan, const uint32_t* all_hist, int P,
                           int rank, int64_t C, int64_t id_offset, cudaStream_t stream);
 cudaError_t launch_rerank(const pkv_index* ix, int64_t C_cap, int64_t id_offset, cudaStream_t stream);
+// GQA-union rerank (PKV_RERANK=union; measured slower than the per-query-head kernel, which stays the default):
+// select emits the union lists, the rerank reads every record once per KV head and scores it for all the
+// group's query heads
+bool union_rerank();
 cudaError_t launch_dbg_scores(const pkv_index* ix, int64_t n, uint8_t* out, cudaStream_t stream);
 cudaError_t launch_topk(const pkv_index* ix, int64_t C_cap, int k, int32_t* out_idx, float* out_est,
                         int out_stride, cudaStream_t stream);

@@ -39,7 +39,7 @@ __device__ __forceinline__ void ce(KV& mine, const KV& o, int p, int k, int j) {
 __global__ void __launch_bounds__(QP_THREADS) qprep_kernel(const uint16_t* q, int T, DevCfg cfg,
                                                           uint32_t* lut, float* rtab,
                                                           float* qnorm, float* qrot,
-                                                          float* dbg_q_rot) {
+                                                          float* dbg_q_rot, unsigned int* ucount) {
   __shared__ unsigned long long sk[NC / 2];
   __shared__ uint32_t si[NC / 2];
   phase_mark(K_QPREP, 0);
@@ -48,6 +48,7 @@ __global__ void __launch_bounds__(QP_THREADS) qprep_kernel(const uint16_t* q, in
   const int g = h / cfg.G, hh = h % cfg.G;
   pdl_wait();  // the query of this layer follows the previous layer's work
   pdl_trigger();
+  if (sb == 0 && hh == 0 && t == 0) ucount[b * cfg.n_kv + g] = 0u;  // the select of this step counts from 0
   phase_mark(K_QPREP, 1);
   // warp 0 rotates the query (fp64 butterflies) and publishes this subspace's 8 coordinates and 1/||y'||
   __shared__ double s_yb[8];
@@ -175,7 +176,7 @@ cudaError_t launch_qprep(const pkv_index* ix, const void* q, int T, float* dbg_q
   dim3 grid(NB, ix->cfg.n_q_heads, ix->batch);
   ProfScope p_(K_QPREP, stream);
   return pdl_launch(qprep_kernel, grid, dim3(QP_THREADS), 0, stream, static_cast<const uint16_t*>(q), T, ix->dcfg,
-                    ws->lut, ws->rtab, ws->qnorm, ws->qrot, dbg_q_rot);
+                    ws->lut, ws->rtab, ws->qnorm, ws->qrot, dbg_q_rot, ws->ucount);
 }
 
 cudaError_t set_phase_qprep(unsigned long long* p) { return set_phase_ptr_tu(p); }

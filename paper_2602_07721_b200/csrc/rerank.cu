@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <string>
 
 #include "common.cuh"
 
@@ -132,6 +133,111 @@ __global__ void __launch_bounds__(RR_THREADS) rerank_cpt_kernel(const uint8_t* _
     const float e = est[u] + __shfl_xor_sync(0xffffffffu, est[u], 1);
     const int pos = pos0 + u * PER_CTA;
     if (!half && pos < C_local) eo[pos] = e * qn;
+  }
+}
+
+// GQA-union rerank: one record read per (key, KV head) for the union of the group's candidate
+// lists. A half-warp per record, lane = subspace b: the lane reads the record's 4-byte nibble word and weight of
+// its subspace (a half-warp reads the 128-byte record in two fully used 64-byte pieces), decodes each nibble to
+// the signed level sign*L[idx] (16-entry smem table: distinct entries sit in distinct banks) and accumulates it
+// against its 8 rotated query coordinates of every query head of the group (registers, loaded once per CTA):
+// est_h = ||q_h|| sum_b w'_b sum_j v_{b,j} q~_{h,b,j}, the 16 subspace partials of the G <= 4 heads reduced
+// with one reduce-scatter over the half-warp (5 shuffles), est_h written at the key's position in head h's list.
+constexpr int UR_THREADS = 256;
+#ifndef PKV_UR_PER
+#define PKV_UR_PER 4
+#endif
+constexpr int UR_PER = PKV_UR_PER;                     // records per half-warp in flight
+constexpr int UR_TILE = (UR_THREADS / 16) * UR_PER;   // records per CTA iteration
+
+template <bool W16>
+__global__ void __launch_bounds__(UR_THREADS) rerank_union_kernel(const uint8_t* __restrict__ rec, const int32_t* uid,
+                                                                   const int32_t* upos, const unsigned int* ucount,
+                                                                   const float* qrot, const float* qnorm, DevCfg cfg,
+                                                                   int64_t cap, int n_q, int n_kv, int G,
+                                                                   int64_t ustride, int64_t cand_stride,
+                                                                   float* est_out) {
+  constexpr int RB = W16 ? 96 : REC;
+  __shared__ float sLv[16];  // nibble (sign << 3 | idx) -> sign * L[idx]
+  const int g = blockIdx.y, b = blockIdx.z;
+  const int64_t bg = (int64_t)b * n_kv + g;
+  const int sb = threadIdx.x & 15, hw = threadIdx.x >> 4, hsel = sb >> 2;
+  if (threadIdx.x < 16) {
+    const float L = cfg.levels[threadIdx.x & 7];
+    sLv[threadIdx.x] = (threadIdx.x & 8) ? L : -L;
+  }
+  pdl_trigger();
+  pdl_wait();
+  float qv[GMAX][8];
+#pragma unroll
+  for (int hh = 0; hh < GMAX; ++hh) {
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f), c = a;
+    if (hh < G) {
+      const float4* qp = reinterpret_cast<const float4*>(qrot + ((int64_t)b * n_q + g * G + hh) * D + 8 * sb);
+      a = qp[0];
+      c = qp[1];
+    }
+    qv[hh][0] = a.x; qv[hh][1] = a.y; qv[hh][2] = a.z; qv[hh][3] = a.w;
+    qv[hh][4] = c.x; qv[hh][5] = c.y; qv[hh][6] = c.z; qv[hh][7] = c.w;
+  }
+  const float qn = hsel < G ? qnorm[(int64_t)b * n_q + g * G + hsel] : 0.f;
+  float* eo = est_out + ((int64_t)b * n_q + g * G + (hsel < G ? hsel : 0)) * cand_stride;
+  const int64_t n_u = ucount[bg];
+  __syncthreads();
+  const uint8_t* rb = rec + bg * cap * RB;
+  const int32_t* ub = uid + bg * ustride;
+  const int32_t* pb = upos + bg * ustride * 4 + hsel;
+  const bool b3 = (sb & 8) != 0, b2 = (sb & 4) != 0;
+  for (int64_t u0 = (int64_t)blockIdx.x * UR_TILE + hw; u0 < n_u; u0 += (int64_t)gridDim.x * UR_TILE) {
+    int key[UR_PER], pos[UR_PER];
+    uint32_t cw[UR_PER], wb[UR_PER];
+#pragma unroll
+    for (int i = 0; i < UR_PER; ++i) {
+      const int64_t u = u0 + 16 * i;
+      key[i] = u < n_u ? ub[u] : -1;
+      pos[i] = (u < n_u && (sb & 3) == 0) ? pb[4 * u] : -1;
+    }
+#pragma unroll
+    for (int i = 0; i < UR_PER; ++i) {
+      cw[i] = 0u;
+      wb[i] = 0u;
+      if (key[i] >= 0) {
+        const uint8_t* r = rb + (int64_t)key[i] * RB;
+        cw[i] = __ldg(reinterpret_cast<const uint32_t*>(r) + sb);
+        wb[i] = W16 ? (uint32_t)__ldg(reinterpret_cast<const unsigned short*>(r + 64) + sb)
+                    : __ldg(reinterpret_cast<const uint32_t*>(r + 64) + sb);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < UR_PER; ++i) {
+      float d[GMAX] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float v = sLv[(cw[i] >> (4 * j)) & 15u];
+#pragma unroll
+        for (int hh = 0; hh < GMAX; ++hh) d[hh] = fmaf(v, qv[hh][j], d[hh]);
+      }
+      float w, escale = 1.f;
+      if (W16) {  // E: bit (b mod 8) in the sign bit of h_b (encode.cu); lanes 0-7 of the half-warp hold bits 0-7
+        const uint32_t m = __ballot_sync(0xffffffffu, (wb[i] >> 15) & 1u);
+        const int e8 = (int)(int8_t)((m >> (threadIdx.x & 16)) & 0xffu);
+        escale = __int_as_float((127 + e8) << 23);
+        w = __half2float(__ushort_as_half((unsigned short)(wb[i] & 0x7fffu)));
+      } else {
+        w = __uint_as_float(wb[i]);
+      }
+#pragma unroll
+      for (int hh = 0; hh < GMAX; ++hh) d[hh] *= w;
+      // reduce-scatter over the half-warp: afterwards lane b holds the sum of head b >> 2
+      float k0 = b3 ? d[2] : d[0], k1 = b3 ? d[3] : d[1];
+      k0 += __shfl_xor_sync(0xffffffffu, b3 ? d[0] : d[2], 8);
+      k1 += __shfl_xor_sync(0xffffffffu, b3 ? d[1] : d[3], 8);
+      float k = b2 ? k1 : k0;
+      k += __shfl_xor_sync(0xffffffffu, b2 ? k0 : k1, 4);
+      k += __shfl_xor_sync(0xffffffffu, k, 2);
+      k += __shfl_xor_sync(0xffffffffu, k, 1);
+      if (pos[i] >= 0) eo[pos[i]] = k * qn * escale;
+    }
   }
 }
 
@@ -1236,6 +1342,11 @@ __global__ void dbg_cand_kernel(const int32_t* __restrict__ cand, const float* _
 static int topk_cluster(const pkv_index* ix, int64_t C_cap, int* slice) {
   const int64_t heads = (int64_t)ix->cfg.n_q_heads * ix->batch;
   int R = (int)std::max<int64_t>(1, std::min<int64_t>(CL_MAX, ix->num_sms / heads));
+  static const int r_env = [] {  // PKV_CL_R=1..8: cluster size override (A/B only; results are identical)
+    const char* e = getenv("PKV_CL_R");
+    return e ? atoi(e) : 0;
+  }();
+  if (r_env >= 1 && r_env <= CL_MAX) R = r_env;
   if (C_cap < 1) C_cap = 1;
   while (R < CL_MAX && (C_cap + R - 1) / R > CL_SLICE) ++R;
   if ((C_cap + R - 1) / R > CL_SLICE) return 0;
@@ -1271,8 +1382,33 @@ cudaError_t init_rerank_attrs() {
   return cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TK_SMEM);
 }
 
+// Read at every call (tests switch it); select and rerank of one step read it back to back.
+bool union_rerank() {
+  const char* e = getenv("PKV_RERANK");
+  return e && std::string(e) == "union";
+}
+
 cudaError_t launch_rerank(const pkv_index* ix, int64_t C_cap, int64_t id_offset, cudaStream_t stream) {
   const Workspace* ws = ix->ws;
+  if (union_rerank()) {
+    static int occ = 0;
+    if (!occ) {
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rerank_union_kernel<false>, UR_THREADS, 0) !=
+              cudaSuccess || occ < 1)
+        occ = 1;
+    }
+    const int64_t bk = (int64_t)ix->batch * ix->cfg.n_kv_heads;
+    const int64_t most = std::min<int64_t>((int64_t)ix->dcfg.G * C_cap, ix->n);  // union size bound
+    const int64_t tiles = std::max<int64_t>(1, (most + UR_TILE - 1) / UR_TILE);
+    const int64_t persist = std::max<int64_t>(1, (int64_t)ix->num_sms * occ / bk);
+    const dim3 grid((unsigned)std::min(tiles, persist), ix->cfg.n_kv_heads, ix->batch);
+    ProfScope p_(K_RERANK, stream);
+    auto kern = ix->dcfg.w16 ? rerank_union_kernel<true> : rerank_union_kernel<false>;
+    return pdl_launch(kern, grid, dim3(UR_THREADS), 0, stream, (const uint8_t*)ix->rec, (const int32_t*)ws->uid,
+                      (const int32_t*)ws->upos, (const unsigned int*)ws->ucount, (const float*)ws->qrot,
+                      (const float*)ws->qnorm, ix->dcfg, ix->cap, ix->cfg.n_q_heads, ix->cfg.n_kv_heads, ix->dcfg.G,
+                      ws->cap, ws->cap, ws->est);
+  }
   static const int cpt_env = [] {  // candidates per thread pair: 2 measured best at 128K (PKV_RR_CPT=1|2|4)
     const char* e = getenv("PKV_RR_CPT");
     return e ? atoi(e) : 2;

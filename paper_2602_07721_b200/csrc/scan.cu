@@ -192,7 +192,8 @@ template <int VB>  // 128-key groups per lane batch (VB * 4 keys per lane in fli
 __global__ void __launch_bounds__(SEL_THREADS) select_kernel(
     const uint32_t* chunk_hist, const uint32_t* all_hist, int P, int rank, int batch, const uint32_t* scores,
     int64_t cap, int64_t n, int64_t chunk, int nchunks, int n_q, int n_kv, int G, int64_t C, int64_t id_offset,
-    int64_t cand_stride, int32_t* cand, int32_t* sel, const uint8_t* rec, int64_t rec_head_bytes, int rec_bytes) {
+    int64_t cand_stride, int32_t* cand, int32_t* sel, const uint8_t* rec, int64_t rec_head_bytes, int rec_bytes,
+    unsigned int* ucount, int32_t* uid, int32_t* upos) {
   phase_mark(K_SELECT, 0);
   cta_mark(K_SELECT, 1);
   __shared__ uint32_t Hg[GMAX][HB];   // global cumulative counts
@@ -465,20 +466,35 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(
         asm volatile("prefetch.global.L2 [%0];" ::"l"(r));
         if (rec_bytes != 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(r + rec_bytes - 1));
       }
+      int pos[GMAX];
 #pragma unroll
       for (int hh = 0; hh < GMAX; ++hh) {
         const bool fg = (ent.y >> (8 * hh + 7)) & 1u;
         const bool fe = (ent.y >> (8 * hh + 6)) & 1u;
         const uint32_t mg = __ballot_sync(0xffffffffu, fg);
         const uint32_t me = __ballot_sync(0xffffffffu, fe);
-        if (fg) cd[hh][p_gt_off[hh] + run_gt[hh] + __popc(mg & lt)] = (int32_t)(ent.x + id_offset);
+        pos[hh] = -1;
+        if (fg) pos[hh] = p_gt_off[hh] + run_gt[hh] + __popc(mg & lt);
         if (fe) {
           const int asc = (int)(run_eq[hh] + __popc(me & lt));
           const int from_end = p_eq[hh] - 1 - asc;
-          if (from_end < p_take[hh]) cd[hh][p_tie_off[hh] + from_end] = (int32_t)(ent.x + id_offset);
+          if (from_end < p_take[hh]) pos[hh] = p_tie_off[hh] + from_end;
         }
+        if (pos[hh] >= 0) cd[hh][pos[hh]] = (int32_t)(ent.x + id_offset);
         run_gt[hh] += __popc(mg);
         run_eq[hh] += __popc(me);
+      }
+      if (uid != nullptr) {  // union entry: the key once, with its position in every head's candidate list
+        const bool any = (pos[0] & pos[1] & pos[2] & pos[3]) != -1;  // positions >= 0, or -1
+        const uint32_t ma = __ballot_sync(0xffffffffu, any);
+        uint32_t ub = 0;
+        if (lane == 0 && ma) ub = atomicAdd(&ucount[bh], (uint32_t)__popc(ma));
+        ub = __shfl_sync(0xffffffffu, ub, 0);
+        if (any) {
+          const int64_t u = (int64_t)bh * cand_stride + ub + __popc(ma & lt);
+          uid[u] = (int32_t)ent.x;
+          reinterpret_cast<int4*>(upos)[u] = make_int4(pos[0], pos[1], pos[2], pos[3]);
+        }
       }
     }
     __syncwarp();
@@ -583,7 +599,8 @@ cudaError_t launch_select(const pkv_index* ix, int64_t n, const ScanPlan& plan, 
                     prefetch_rec() && (int64_t)ix->batch * ix->cfg.n_q_heads * C * ix->dcfg.rec_bytes <= (48ll << 20)
                         ? (const uint8_t*)ix->rec
                         : (const uint8_t*)nullptr,
-                    ix->cap * ix->dcfg.rec_bytes, ix->dcfg.rec_bytes);
+                    ix->cap * ix->dcfg.rec_bytes, ix->dcfg.rec_bytes, ws->ucount,
+                    union_rerank() ? ws->uid : (int32_t*)nullptr, ws->upos);
 }
 
 cudaError_t launch_dbg_scores(const pkv_index* ix, int64_t n, uint8_t* out, cudaStream_t stream) {

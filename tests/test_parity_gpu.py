@@ -544,3 +544,19 @@ def test_tensor_core_encoder_bit_exact(pkv, monkeypatch):
     run_and_check(pkv, K, q, V, k=64, n_hot=16)
     K, q, V = make_problem(82, 1, 4, 1, 333, plant=False)
     run_and_check(pkv, K, q, V, k=32, cfg=w16_cfg(pkv, 4, 1))
+
+
+def test_gqa_union_rerank(pkv, monkeypatch):
+    """SURVEY §8(f2) GQA dedupe (PKV_RERANK=union): the select emits, per KV head, the union of its query heads'
+    candidate lists with every key's position in each list; the rerank reads each record once and scores it for
+    all heads of the group. Same oracle checks as the per-head kernel (G = 4, 2, 1; fp32 and fp16 weights;
+    ties in the s* bucket; hot rows)."""
+    monkeypatch.setenv("PKV_RERANK", "union")
+    K, q, V = make_problem(91, 2, 8, 2, 5000)
+    run_and_check(pkv, K, q, V, k=64, n_hot=16)
+    K, q, V = make_problem(92, 1, 4, 2, 3000, plant=False)
+    run_and_check(pkv, K, q, V, k=32, T=26, C=900)
+    K, q, V = make_problem(93, 1, 3, 3, 2000, plant=False)
+    run_and_check(pkv, K, q, V, k=32)
+    K, q, V = make_problem(94, 1, 8, 2, 4000)
+    run_and_check(pkv, K, q, V, k=64, cfg=w16_cfg(pkv, 8, 2))
