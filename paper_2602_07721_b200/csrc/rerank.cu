@@ -45,8 +45,11 @@ __global__ void __launch_bounds__(RR_THREADS) rerank_cpt_kernel(const uint8_t* _
                                                                  float* est_out) {
   constexpr int RB = W16 ? 96 : REC;  // record stride
   __shared__ __align__(16) float T[RT_ROWS * 16];
+  phase_mark(K_RERANK, 0);
   pdl_trigger();
   pdl_wait();
+  phase_mark(K_RERANK, 1);
+  cta_mark(K_RERANK, 1);
   const int h = blockIdx.y, b = blockIdx.z;
   const int g = h / G;
   const int64_t bhq = (int64_t)b * n_q + h;
@@ -91,6 +94,7 @@ __global__ void __launch_bounds__(RR_THREADS) rerank_cpt_kernel(const uint8_t* _
     }
   }
   __syncthreads();
+  phase_mark(K_RERANK, 2);
   const char* Tb = reinterpret_cast<const char*>(T);
   const uint32_t hoff = half ? 64u : 0u;
   float est[CPT];
@@ -134,6 +138,8 @@ __global__ void __launch_bounds__(RR_THREADS) rerank_cpt_kernel(const uint8_t* _
     const int pos = pos0 + u * PER_CTA;
     if (!half && pos < C_local) eo[pos] = e * qn;
   }
+  phase_mark(K_RERANK, 3);
+  cta_mark(K_RERANK, 0);
 }
 
 // GQA-union rerank: one record read per (key, KV head) for the union of the group's candidate

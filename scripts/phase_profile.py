@@ -52,6 +52,9 @@ for rep in range(3):
             print(f"  {nm} CTAs: n={len(ends)} start min/med/max {min(starts):.2f}/{statistics.median(starts):.2f}/{max(starts):.2f}"
                   f"  end min/med/max {min(ends):.2f}/{statistics.median(ends):.2f}/{max(ends):.2f}"
                   f"  dur(us) med/max {statistics.median(dur)/1000:.2f}/{max(dur)/1000:.2f}")
+            qs = lambda v: "/".join(f"{x:.1f}" for x in statistics.quantiles(v, n=10)) if len(v) > 1 else ""
+            print(f"   {nm} start deciles {qs(starts)}")
+            print(f"   {nm} end deciles   {qs(ends)}")
             if nm == "select":
                 slow = sorted(range(len(ends)), key=lambda i: -ends[i])[:8]
                 print("   slowest select CTAs (linear id -> end):", [(i, round(ends[i], 2)) for i in slow])
