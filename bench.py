@@ -372,6 +372,20 @@ def run_ours(args):
             traffic = None
     roof = {"bound": "hbm", "kernel": dom, "achieved": kern[dom]["gbs"], "peak": hbm_peak, "unit": "GB/s",
             "frac": round(kern[dom]["gbs"] / hbm_peak, 4), "traffic": traffic, "peak_source": peak_kind}
+    # context: measured data-movement floors of the two gathers (profiles/floors_r01.json, scripts/hbm_gather.cu,
+    # scripts/uva_bw.cu) — the rerank's random 128 B record gather from HBM and, at 1M, the UVA row gather
+    fl_file = os.path.join(ROOT, "profiles", "floors_r01.json")
+    if os.path.exists(fl_file) and world == 1 and not args.w16:
+        try:
+            fl = json.load(open(fl_file)).get(args.config)
+        except Exception:
+            fl = None
+        if fl and "rerank" in kern:
+            roof["rerank_gather_floor_us"] = fl["rerank_gather_us"]
+            roof["rerank_frac_of_gather_floor"] = round(fl["rerank_gather_us"] / kern["rerank"]["avg_us"], 4)
+            if uva and "uva_gather_3200_rows_us" in fl:
+                roof["host_link_gbs"] = fl["uva_stream_read_gbs"]
+                roof["uva_row_gather_floor_us"] = fl["uva_gather_3200_rows_us"]
     scan_gbs = kern.get("scan", {}).get("gbs")
 
     # ---- CPU oracle baseline (rank 0, N = 1 only) ----

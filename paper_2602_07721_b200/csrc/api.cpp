@@ -108,7 +108,7 @@ pkv_status alloc_workspace(Workspace* ws, int batch, int n_q, int n_kv, int64_t 
       bq * (size_t)cap * 4,                              // cand
       bq * (size_t)cap * 4,                              // est
       (size_t)MAX_RANKS * bq * MAX_TOPK * 8,             // topk exchange: per rank [idx | est] (one all-gather)
-      0,                                                 // (unused)
+      (size_t)std::max<size_t>(bk, 256) * 32 * GMAX * HB * 2,  // warp_hist (scan CTAs <= max(units, SMs))
       (size_t)MAX_RANKS * bq * MAX_SPLITS * PART * 4,    // part
       bk * 4,                                            // ticket
       (size_t)MAX_RANKS * bq * MAX_TOPK * 4,             // seg_est
@@ -139,7 +139,8 @@ pkv_status alloc_workspace(Workspace* ws, int batch, int n_q, int n_kv, int64_t 
   ws->est = reinterpret_cast<float*>(take(9));
   ws->topk_idx = reinterpret_cast<int32_t*>(take(10));
   ws->topk_est = reinterpret_cast<float*>(ws->topk_idx + bq * MAX_TOPK);  // rank r: idx at 2r*slot, est after
-  take(11);
+  ws->warp_hist = reinterpret_cast<uint16_t*>(take(11));
+  ws->warp_hist_ctas = (int64_t)std::max<size_t>(bk, 256);
   ws->part = reinterpret_cast<float*>(take(12));
   ws->ticket = reinterpret_cast<unsigned int*>(take(13));
   ws->seg_est = reinterpret_cast<float*>(take(14));

@@ -33,6 +33,20 @@ __device__ __forceinline__ uint4 ldg_nc_v4_early(const void* p) {
   return r;
 }
 
+// 32-byte load (sm_100 LDG.256), ordered like ldg_nc_v4_early: one request covers a whole 32-byte sector, where
+// two 16-byte loads from different instructions each request the same sector from L2 again.
+struct u32x8 {
+  uint32_t w[8];
+};
+__device__ __forceinline__ u32x8 ldg_nc_v8_early(const void* p) {
+  u32x8 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3]), "=r"(r.w[4]), "=r"(r.w[5]), "=r"(r.w[6]),
+                 "=r"(r.w[7])
+               : "l"(p));
+  return r;
+}
+
 __device__ __forceinline__ uint4 ldg_v4(const void* p) {
   uint4 r;
   asm("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));

@@ -62,6 +62,8 @@ struct Workspace {
   unsigned int* ucount = nullptr; // [batch][n_kv] union sizes (zeroed by qprep, counted by select)
   int32_t* uid = nullptr;         // [batch][n_kv][cap] local key index
   int32_t* upos = nullptr;        // [batch][n_kv][cap][4] candidate positions per query head of the group
+  uint16_t* warp_hist = nullptr;  // [warp_hist_ctas][32 warps][GMAX][HB] per-warp cumulative score counts (scan)
+  int64_t warp_hist_ctas = 0;
   void* base = nullptr;
   size_t bytes = 0;
   int refs = 1;
@@ -144,7 +146,8 @@ constexpr int POST_CHUNK = 8192;  // keys per inverted-list chunk (u16 offsets)
 
 struct ScanPlan {
   int nchunks;
-  int64_t chunk;  // keys per chunk (multiple of 32)
+  int64_t chunk;           // keys per chunk (multiple of 32)
+  bool warp_hist = false;  // the scan records per-warp cumulative histograms for the select (dense scan only)
 };
 ScanPlan plan_scan(const pkv_index* ix, int64_t n);
 int64_t score_stride(const pkv_index* ix);

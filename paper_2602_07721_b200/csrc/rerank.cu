@@ -38,7 +38,7 @@ constexpr int RT_ROWS = D;
 // W16: records of 96 bytes with fp16 weights h_b and a per-key exponent E in their sign bits (encode.cu):
 // each thread of the pair reads its 32 B of nibbles + 16 B of halves and decodes E from its own 8 halves.
 template <int CPT, bool W16>
-__global__ void __launch_bounds__(RR_THREADS) rerank_cpt_kernel(const uint8_t* __restrict__ rec, const int32_t* cand,
+__global__ void __launch_bounds__(RR_THREADS, 6) rerank_cpt_kernel(const uint8_t* __restrict__ rec, const int32_t* cand,
                                                                  const int32_t* sel, const float* rtab,
                                                                  const float* qnorm, int64_t cap, int n_q, int n_kv,
                                                                  int G, int64_t cand_stride, int64_t id_offset,
@@ -54,13 +54,16 @@ __global__ void __launch_bounds__(RR_THREADS) rerank_cpt_kernel(const uint8_t* _
   const int g = h / G;
   const int64_t bhq = (int64_t)b * n_q + h;
   constexpr int PER_CTA = RR_THREADS / 2;
+  constexpr int TILE = PER_CTA * CPT;
   const int32_t* cd = cand + bhq * cand_stride;
-  const int pos0 = blockIdx.x * (PER_CTA * CPT) + (threadIdx.x >> 1);
   const int C_local = sel[bhq * SEL_STRIDE + 2];
+  // candidate tiles blockIdx.x, blockIdx.x + gridDim.x, ...: the grid is capped at the resident CTA count, so the
+  // query table below is staged once per CTA, not once per tile (at 1M tokens: 205 tiles per head)
+  int tile = blockIdx.x;
   int32_t cid[CPT];
 #pragma unroll
   for (int u = 0; u < CPT; ++u) {
-    const int pos = pos0 + u * PER_CTA;
+    const int pos = tile * TILE + (threadIdx.x >> 1) + u * PER_CTA;
     cid[u] = pos < cand_stride ? cd[pos] : 0;  // speculative (inside the capacity); used only if pos < C_local
   }
   const float4* tsrc = reinterpret_cast<const float4*>(rtab + bhq * D * 16);
@@ -68,7 +71,7 @@ __global__ void __launch_bounds__(RR_THREADS) rerank_cpt_kernel(const uint8_t* _
 #pragma unroll
   for (int u = 0; u < D * 4 / RR_THREADS; ++u) tv[u] = tsrc[threadIdx.x + u * RR_THREADS];
   const float qn = qnorm[bhq];
-  if (blockIdx.x * (PER_CTA * CPT) >= C_local) return;
+  if (tile * TILE >= C_local) return;
 #pragma unroll
   for (int u = 0; u < D * 4 / RR_THREADS; ++u) {  // coordinate c -> physical row 2(c%64)+c/64
     const int i = threadIdx.x + u * RR_THREADS;
@@ -77,36 +80,55 @@ __global__ void __launch_bounds__(RR_THREADS) rerank_cpt_kernel(const uint8_t* _
   }
   const int half = threadIdx.x & 1;
   const uint8_t* rec_bh = rec + ((int64_t)b * n_kv + g) * cap * RB + 32 * half;
-  uint4 cr[CPT][2], wr[CPT][2];
+  float* eo = est_out + bhq * cand_stride;
+  const char* Tb = reinterpret_cast<const char*>(T);
+  const uint32_t hoff = half ? 64u : 0u;
+  bool staged = false;
+  for (; tile * TILE < C_local; tile += gridDim.x) {
+  const int pos0 = tile * TILE + (threadIdx.x >> 1);
+  // each thread's 32 B of nibbles and 32 B of weights (fp32) in one 256-bit load each: every request is a
+  // whole sector (two 16-byte halves from two instructions would each fetch the sector from L2)
+  u32x8 cr[CPT], wr[CPT];
 #pragma unroll
   for (int u = 0; u < CPT; ++u) {
-    cr[u][0] = cr[u][1] = wr[u][0] = wr[u][1] = make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) cr[u].w[i] = wr[u].w[i] = 0u;
     if (pos0 + u * PER_CTA < C_local) {
       const uint8_t* r = rec_bh + ((int64_t)cid[u] - id_offset) * RB;
-      cr[u][0] = ldg_nc_v4_early(r);
-      cr[u][1] = ldg_nc_v4_early(r + 16);
+      cr[u] = ldg_nc_v8_early(r);
       if (W16) {
-        wr[u][0] = ldg_nc_v4_early(r + 64 - 16 * half);  // halves of subspaces 8*half .. 8*half+7
+        const uint4 hv = ldg_nc_v4_early(r + 64 - 16 * half);  // halves of subspaces 8*half .. 8*half+7
+        wr[u].w[0] = hv.x;
+        wr[u].w[1] = hv.y;
+        wr[u].w[2] = hv.z;
+        wr[u].w[3] = hv.w;
       } else {
-        wr[u][0] = ldg_nc_v4_early(r + 64);
-        wr[u][1] = ldg_nc_v4_early(r + 80);
+        wr[u] = ldg_nc_v8_early(r + 64);  // w' of subspaces 8*half .. 8*half+7 (r includes 32*half)
       }
     }
   }
-  __syncthreads();
+  // the next tile's candidate ids, in flight during this tile's lookups
+  const int nxt = tile + gridDim.x;
+#pragma unroll
+  for (int u = 0; u < CPT; ++u) {
+    const int pos = nxt * TILE + (threadIdx.x >> 1) + u * PER_CTA;
+    cid[u] = (nxt * TILE < C_local && pos < cand_stride) ? cd[pos] : 0;
+  }
+  if (!staged) {
+    __syncthreads();
+    staged = true;
+  }
   phase_mark(K_RERANK, 2);
-  const char* Tb = reinterpret_cast<const char*>(T);
-  const uint32_t hoff = half ? 64u : 0u;
   float est[CPT];
 #pragma unroll
   for (int u = 0; u < CPT; ++u) {
-    const uint32_t cw[8] = {cr[u][0].x, cr[u][0].y, cr[u][0].z, cr[u][0].w,
-                            cr[u][1].x, cr[u][1].y, cr[u][1].z, cr[u][1].w};
-    uint32_t ww[8] = {wr[u][0].x, wr[u][0].y, wr[u][0].z, wr[u][0].w,
-                      wr[u][1].x, wr[u][1].y, wr[u][1].z, wr[u][1].w};
+    const uint32_t* cw = cr[u].w;
+    uint32_t ww[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) ww[i] = wr[u].w[i];
     float escale = 1.f;
     if (W16) {
-      const uint32_t h4[4] = {wr[u][0].x, wr[u][0].y, wr[u][0].z, wr[u][0].w};
+      const uint32_t h4[4] = {wr[u].w[0], wr[u].w[1], wr[u].w[2], wr[u].w[3]};
       uint32_t e8 = 0;
 #pragma unroll
       for (int i = 0; i < 4; ++i) e8 |= (((h4[i] >> 15) & 1u) << (2 * i)) | (((h4[i] >> 31) & 1u) << (2 * i + 1));
@@ -131,13 +153,13 @@ __global__ void __launch_bounds__(RR_THREADS) rerank_cpt_kernel(const uint8_t* _
     }
     est[u] = W16 ? e * escale : e;
   }
-  float* eo = est_out + bhq * cand_stride;
 #pragma unroll
   for (int u = 0; u < CPT; ++u) {
     const float e = est[u] + __shfl_xor_sync(0xffffffffu, est[u], 1);
     const int pos = pos0 + u * PER_CTA;
     if (!half && pos < C_local) eo[pos] = e * qn;
   }
+  }  // tiles
   phase_mark(K_RERANK, 3);
   cta_mark(K_RERANK, 0);
 }
@@ -1415,18 +1437,29 @@ cudaError_t launch_rerank(const pkv_index* ix, int64_t C_cap, int64_t id_offset,
                       (const float*)ws->qnorm, ix->dcfg, ix->cap, ix->cfg.n_q_heads, ix->cfg.n_kv_heads, ix->dcfg.G,
                       ws->cap, ws->cap, ws->est);
   }
-  static const int cpt_env = [] {  // candidates per thread pair: 2 measured best at 128K (PKV_RR_CPT=1|2|4)
+  static const int cpt_env = [] {  // candidates per thread pair (PKV_RR_CPT=1|2|4; default by list length)
     const char* e = getenv("PKV_RR_CPT");
-    return e ? atoi(e) : 2;
+    return e ? atoi(e) : 0;
   }();
-  const int cpt = (cpt_env == 1 || cpt_env == 4) ? cpt_env : 2;
+  // 2 measured best for short lists (128K), 1 for long ones that loop over tiles (1M: 186.7 vs 192.6 us/layer)
+  const int cpt = (cpt_env == 1 || cpt_env == 2 || cpt_env == 4) ? cpt_env : (C_cap > 16384 ? 1 : 2);
   const int64_t per = (int64_t)(RR_THREADS / 2) * cpt;
-  const dim3 grid((unsigned)std::max<int64_t>(1, (C_cap + per - 1) / per), ix->cfg.n_q_heads, ix->batch);
-  ProfScope p_(K_RERANK, stream);
   auto kern = ix->dcfg.w16 ? (cpt == 1 ? rerank_cpt_kernel<1, true> : cpt == 2 ? rerank_cpt_kernel<2, true>
                                                                               : rerank_cpt_kernel<4, true>)
                            : (cpt == 1 ? rerank_cpt_kernel<1, false> : cpt == 2 ? rerank_cpt_kernel<2, false>
                                                                                : rerank_cpt_kernel<4, false>);
+  // at most the resident CTA count per (sequence, query head): longer lists loop over tiles inside the CTA
+  static int occ_cache[2][5] = {};
+  int& occ = occ_cache[ix->dcfg.w16 ? 1 : 0][cpt];
+  if (!occ) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, RR_THREADS, 0) != cudaSuccess || occ < 1) occ = 1;
+  }
+  const int64_t tiles = std::max<int64_t>(1, (C_cap + per - 1) / per);
+  const int64_t persist = std::max<int64_t>(1, (int64_t)ix->num_sms * occ / ((int64_t)ix->batch * ix->cfg.n_q_heads));
+  // capped only when the tiles exceed two full waves: a short list (128K: 31 tiles per head vs 27 resident CTAs)
+  // runs one CTA per tile, a long one (1M: 205+) loops over tiles in resident CTAs
+  const dim3 grid((unsigned)(tiles > 2 * persist ? persist : tiles), ix->cfg.n_q_heads, ix->batch);
+  ProfScope p_(K_RERANK, stream);
   return pdl_launch(kern, grid, dim3(RR_THREADS), 0, stream, (const uint8_t*)ix->rec, (const int32_t*)ws->cand,
                     (const int32_t*)ws->sel, (const float*)ws->rtab, (const float*)ws->qnorm, ix->cap,
                     ix->cfg.n_q_heads, ix->cfg.n_kv_heads, ix->dcfg.G, ws->cap, id_offset, ws->est);

@@ -35,12 +35,16 @@ __device__ __forceinline__ uint32_t lut_load(uint32_t addr, uint32_t lut_base) {
   return v;
 }
 
+// Warp w of a chunk's CTA owns the contiguous key segment [t_begin + w*seg, +seg), seg a multiple of 128 keys; the
+// select kernel uses the same segments, so the per-warp histograms of the scan give it every warp's output offsets.
+__host__ __device__ __forceinline__ uint32_t warp_seg(uint32_t len) { return ((len + 32 * 128 - 1) / (32 * 128)) * 128; }
+
 template <bool CHECK>
 __device__ __forceinline__ void load_rows(uint4 (&row)[SCAN_UNROLL], const uint8_t* __restrict__ ids_bh, uint32_t base,
                                           uint32_t t_end) {
 #pragma unroll
   for (int u = 0; u < SCAN_UNROLL; ++u) {
-    const uint32_t t = base + (uint32_t)u * SCAN_WARPS * 32;
+    const uint32_t t = base + (uint32_t)u * 32;
     row[u] = (!CHECK || t < t_end) ? ldg_nc_v4(ids_bh + (size_t)t * NB) : make_uint4(0, 0, 0, 0);
   }
 }
@@ -61,45 +65,40 @@ __device__ __forceinline__ void score_key(const uint4& r, const uint32_t (&p)[16
   for (int hh = 0; hh < G; ++hh) atomicAdd(&hist_w[hh * HB + prmt(acc, 0u, 0x4440u | (uint32_t)hh)], 1u);
 }
 
-// Main loop, software-pipelined: rows of the next round are in flight while this round is scored. Full rounds
-// run without per-key bounds checks; only the last round checks.
+// Main loop over this warp's segment [seg0, seg1), software-pipelined: rows of the next round are in flight while
+// this round is scored. Full rounds run without per-key bounds checks; only the last round checks.
 template <int RES, bool FAST, int G>
 __device__ __forceinline__ void scan_loop(uint4 (&row)[SCAN_UNROLL], const uint8_t* __restrict__ ids_bh,
-                                          uint32_t* __restrict__ scores_bh, uint32_t* hist_w, uint32_t t_begin,
-                                          uint32_t t_end, uint32_t lut_base) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+                                          uint32_t* __restrict__ scores_bh, uint32_t* hist_w, uint32_t seg0,
+                                          uint32_t seg1, uint32_t lut_base) {
+  const int lane = threadIdx.x & 31;
   uint32_t p[16];
 #pragma unroll
   for (int i = 0; i < 16; ++i) p[i] = (uint32_t)(lane + i) * 4u;
-  constexpr uint32_t ROW = SCAN_WARPS * 32;
-  constexpr uint32_t STEP = ROW * SCAN_UNROLL;
-  uint32_t wbase = t_begin + (uint32_t)warp * 32;  // warp-uniform
-  for (; wbase + (SCAN_UNROLL - 1) * ROW + 32 <= t_end; wbase += STEP) {  // all rows of this warp in range
+  constexpr uint32_t STEP = 32 * SCAN_UNROLL;
+  uint32_t wbase = seg0;  // warp-uniform
+  for (; wbase + STEP <= seg1; wbase += STEP) {  // all rows of this round in range
     uint4 nxt[SCAN_UNROLL];
-    load_rows<true>(nxt, ids_bh, wbase + STEP + lane, t_end);
+    load_rows<true>(nxt, ids_bh, wbase + STEP + lane, seg1);
 #pragma unroll
     for (int u = 0; u < SCAN_UNROLL; ++u)
-      score_key<RES, FAST, G>(row[u], p, lut_base, scores_bh, hist_w, wbase + lane + u * ROW);
+      score_key<RES, FAST, G>(row[u], p, lut_base, scores_bh, hist_w, wbase + lane + u * 32);
 #pragma unroll
     for (int u = 0; u < SCAN_UNROLL; ++u) row[u] = nxt[u];
   }
-  for (; wbase < t_end; wbase += STEP) {
-    uint4 nxt[SCAN_UNROLL];
-    load_rows<true>(nxt, ids_bh, wbase + STEP + lane, t_end);
+  if (wbase < seg1) {  // last, partial round (no further rows to prefetch)
 #pragma unroll
     for (int u = 0; u < SCAN_UNROLL; ++u) {
-      const uint32_t t = wbase + lane + u * ROW;
-      if (t < t_end) score_key<RES, FAST, G>(row[u], p, lut_base, scores_bh, hist_w, t);
+      const uint32_t t = wbase + lane + u * 32;
+      if (t < seg1) score_key<RES, FAST, G>(row[u], p, lut_base, scores_bh, hist_w, t);
     }
-#pragma unroll
-    for (int u = 0; u < SCAN_UNROLL; ++u) row[u] = nxt[u];
   }
 }
 
 template <int RES>
 __global__ void __launch_bounds__(SCAN_THREADS, 1)
     scan_kernel(const uint8_t* __restrict__ ids, const uint32_t* lut_g, uint32_t* scores, uint32_t* chunk_hist,
-                int64_t cap, int64_t sstride, int64_t n, int64_t chunk, int G) {
+                uint16_t* warp_hist, int64_t cap, int64_t sstride, int64_t n, int64_t chunk, int G) {
   extern __shared__ __align__(16) uint32_t smem[];
   uint32_t* lut = smem;
   uint32_t* hist = smem + LUT_WORDS;
@@ -110,8 +109,11 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1)
   pdl_trigger();
   phase_mark(K_SCAN, 0);
   // the centroid ids do not depend on the query: start streaming them before qprep has finished
+  const uint32_t seg = warp_seg((uint32_t)(t_end - t_begin));
+  const uint32_t seg0 = (uint32_t)t_begin + (threadIdx.x >> 5) * seg;
+  const uint32_t seg1 = min((uint32_t)t_end, seg0 + seg);
   uint4 row[SCAN_UNROLL];
-  load_rows<true>(row, ids_bh, (uint32_t)t_begin + (threadIdx.x >> 5) * 32 + (threadIdx.x & 31), (uint32_t)t_end);
+  load_rows<true>(row, ids_bh, seg0 + (threadIdx.x & 31), seg1);
   for (int i = threadIdx.x; i < SCAN_WARPS * GMAX * HB; i += SCAN_THREADS) hist[i] = 0u;
   pdl_wait();  // lookup table comes from qprep
   phase_mark(K_SCAN, 1);
@@ -132,14 +134,42 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1)
   phase_mark(K_SCAN, 2);
   uint32_t* scores_bh = scores + (int64_t)bh * sstride;
   uint32_t* hist_w = hist + (threadIdx.x >> 5) * GMAX * HB;
-  const uint32_t tb = (uint32_t)t_begin, te = (uint32_t)t_end;
   if (lut_base == (uint32_t)RES) {
-    if (G == 4) scan_loop<RES, true, 4>(row, ids_bh, scores_bh, hist_w, tb, te, lut_base);
-    else if (G == 2) scan_loop<RES, true, 2>(row, ids_bh, scores_bh, hist_w, tb, te, lut_base);
-    else if (G == 3) scan_loop<RES, true, 3>(row, ids_bh, scores_bh, hist_w, tb, te, lut_base);
-    else scan_loop<RES, true, 1>(row, ids_bh, scores_bh, hist_w, tb, te, lut_base);
+    if (G == 4) scan_loop<RES, true, 4>(row, ids_bh, scores_bh, hist_w, seg0, seg1, lut_base);
+    else if (G == 2) scan_loop<RES, true, 2>(row, ids_bh, scores_bh, hist_w, seg0, seg1, lut_base);
+    else if (G == 3) scan_loop<RES, true, 3>(row, ids_bh, scores_bh, hist_w, seg0, seg1, lut_base);
+    else scan_loop<RES, true, 1>(row, ids_bh, scores_bh, hist_w, seg0, seg1, lut_base);
   } else {
-    scan_loop<RES, false, 4>(row, ids_bh, scores_bh, hist_w, tb, te, lut_base);  // G <= 4: unused bytes are 0
+    scan_loop<RES, false, 4>(row, ids_bh, scores_bh, hist_w, seg0, seg1, lut_base);  // G <= 4: unused bytes are 0
+  }
+  if (warp_hist != nullptr) {
+    // this warp's cumulative counts cum_w[h][s] = #(score_h >= s) in its segment (u16: a segment holds < 2^16 keys),
+    // read by the select kernel instead of a counting pass over the scores
+    __syncwarp();
+    const int lane = threadIdx.x & 31;
+    uint16_t* wo = warp_hist + (((int64_t)bh * gridDim.x + j) * SCAN_WARPS + (threadIdx.x >> 5)) * GMAX * HB;
+    for (int hh = 0; hh < G; ++hh) {
+      uint32_t v[4], tot = 0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        v[e] = hist_w[hh * HB + 4 * lane + e];
+        tot += v[e];
+      }
+      uint32_t inc = tot;
+#pragma unroll
+      for (int x = 1; x < 32; x <<= 1) {
+        const uint32_t o = __shfl_down_sync(0xffffffffu, inc, x);
+        if (lane + x < 32) inc += o;
+      }
+      uint32_t run = inc - tot;
+      uint32_t c[4];
+#pragma unroll
+      for (int e = 3; e >= 0; --e) {
+        run += v[e];
+        c[e] = run;
+      }
+      reinterpret_cast<uint2*>(wo + hh * HB)[lane] = make_uint2(c[0] | (c[1] << 16), c[2] | (c[3] << 16));
+    }
   }
   __syncthreads();
   phase_mark(K_SCAN, 3);
@@ -193,7 +223,7 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(
     const uint32_t* chunk_hist, const uint32_t* all_hist, int P, int rank, int batch, const uint32_t* scores,
     int64_t cap, int64_t n, int64_t chunk, int nchunks, int n_q, int n_kv, int G, int64_t C, int64_t id_offset,
     int64_t cand_stride, int32_t* cand, int32_t* sel, const uint8_t* rec, int64_t rec_head_bytes, int rec_bytes,
-    unsigned int* ucount, int32_t* uid, int32_t* upos) {
+    unsigned int* ucount, int32_t* uid, int32_t* upos, const uint16_t* warp_hist) {
   phase_mark(K_SELECT, 0);
   cta_mark(K_SELECT, 1);
   __shared__ uint32_t Hg[GMAX][HB];   // global cumulative counts
@@ -215,7 +245,7 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(
   const uint32_t t_begin = (uint32_t)j * (uint32_t)chunk;
   const uint32_t t_end = (uint32_t)min(n, (int64_t)t_begin + chunk);
   const uint32_t len = t_end - t_begin;
-  const uint32_t seg = ((len + 32 * 128 - 1) / (32 * 128)) * 128;
+  const uint32_t seg = warp_seg(len);
   const uint32_t seg0 = t_begin + warp * seg;
   const uint32_t seg1 = min(t_end, seg0 + seg);
   const uint32_t* sc = scores + (int64_t)bh * cap;
@@ -350,7 +380,19 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(
   // pass 1: per-head counts of this warp's segment; lane l reads keys 4l..4l+3 of each 128-key group, VB groups
   // (16 keys per lane) in flight, kept in registers for pass 2 when the segment is short enough (the 128K case)
   uint32_t tot_gt[GMAX] = {0, 0, 0, 0}, tot_eq[GMAX] = {0, 0, 0, 0};
-  for (uint32_t g0 = 0; g0 < ngrp; g0 += VB) {
+  if (warp_hist != nullptr) {
+    // the dense scan recorded this warp segment's cumulative counts: #(> s*) = cum[s*+1], #(== s*) = cum[s*] - cum[s*+1]
+    const uint16_t* wh = warp_hist + (((int64_t)bh * nchunks + j) * 32 + warp) * GMAX * HB;
+#pragma unroll
+    for (int hh = 0; hh < GMAX; ++hh) {
+      const int st = (hh < G) ? s_star[hh] : HB;
+      const uint32_t ge = st < HB ? wh[hh * HB + st] : 0u;
+      const uint32_t gt = st + 1 < HB ? wh[hh * HB + st + 1] : 0u;
+      tot_gt[hh] = lane == 0 ? gt : 0u;  // summed over the warp's lanes below
+      tot_eq[hh] = lane == 0 ? ge - gt : 0u;
+    }
+  }
+  for (uint32_t g0 = 0; warp_hist == nullptr && g0 < ngrp; g0 += VB) {
     if (g0 > 0) {
 #pragma unroll
       for (int k2 = 0; k2 < VB; ++k2) {
@@ -408,15 +450,20 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(
     }
   }
   __syncthreads();
-  uint32_t run_gt[GMAX], run_eq[GMAX];
+  // per-head running state in registers (the entry loop below is the select's hot loop; 1024-thread CTAs leave
+  // 64 registers per thread, so nothing in it is re-read from shared memory or the parameter bank):
+  //   gtp: list position of the next key with score > s*;  eqe: distance from the end of the s* bucket of the
+  //   next key with score == s* (the bucket is handed out newest first: taken iff eqe < take)
+  int gtp[GMAX], eqe[GMAX], take[GMAX], toff[GMAX];
 #pragma unroll
   for (int hh = 0; hh < GMAX; ++hh) {
-    run_gt[hh] = wcnt[warp][2 * hh];
-    run_eq[hh] = wcnt[warp][2 * hh + 1];
+    gtp[hh] = p_gt_off[hh] + (int)wcnt[warp][2 * hh];
+    eqe[hh] = p_eq[hh] - 1 - (int)wcnt[warp][2 * hh + 1];
+    take[hh] = p_take[hh];
+    toff[hh] = p_tie_off[hh];
   }
-  int32_t* cd[GMAX];
-#pragma unroll
-  for (int hh = 0; hh < GMAX; ++hh) cd[hh] = cand + ((int64_t)b * n_q + g * G + (hh < G ? hh : 0)) * cand_stride;
+  int32_t* const cd0 = cand + ((int64_t)b * n_q + g * G) * cand_stride;
+  const int32_t idoff = (int32_t)id_offset;
   const uint32_t lt = (1u << lane) - 1u;
   phase_mark(K_SELECT, 4);
   // pass 2: keys with score >= s* for at least one head (~4 x beta of them) are first compacted, in key
@@ -473,16 +520,11 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(
         const bool fe = (ent.y >> (8 * hh + 6)) & 1u;
         const uint32_t mg = __ballot_sync(0xffffffffu, fg);
         const uint32_t me = __ballot_sync(0xffffffffu, fe);
-        pos[hh] = -1;
-        if (fg) pos[hh] = p_gt_off[hh] + run_gt[hh] + __popc(mg & lt);
-        if (fe) {
-          const int asc = (int)(run_eq[hh] + __popc(me & lt));
-          const int from_end = p_eq[hh] - 1 - asc;
-          if (from_end < p_take[hh]) pos[hh] = p_tie_off[hh] + from_end;
-        }
-        if (pos[hh] >= 0) cd[hh][pos[hh]] = (int32_t)(ent.x + id_offset);
-        run_gt[hh] += __popc(mg);
-        run_eq[hh] += __popc(me);
+        const int fend = eqe[hh] - __popc(me & lt);
+        pos[hh] = fg ? gtp[hh] + __popc(mg & lt) : (fe && fend < take[hh]) ? toff[hh] + fend : -1;
+        if (pos[hh] >= 0) cd0[hh * cand_stride + pos[hh]] = (int32_t)ent.x + idoff;
+        gtp[hh] += __popc(mg);
+        eqe[hh] -= __popc(me);
       }
       if (uid != nullptr) {  // union entry: the key once, with its position in every head's candidate list
         const bool any = (pos[0] & pos[1] & pos[2] & pos[3]) != -1;  // positions >= 0, or -1
@@ -529,6 +571,15 @@ cudaError_t init_scan_attrs() {
 // vector loads
 int64_t score_stride(const pkv_index* ix) { return (ix->cap + 3) & ~(int64_t)3; }
 
+// PKV_NO_WARP_HIST=1: the select counts its warps' keys itself (A/B switch; results are identical)
+static bool warp_hist_on() {
+  static const bool on = [] {
+    const char* e = getenv("PKV_NO_WARP_HIST");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
 ScanPlan plan_scan(const pkv_index* ix, int64_t n) {
   if (ix->postings) {  // the inverted-list scan works on fixed chunks
     ScanPlan p;
@@ -552,6 +603,13 @@ ScanPlan plan_scan(const pkv_index* ix, int64_t n) {
   if (nch < 1) nch = 1;
   p.nchunks = nch;
   p.chunk = chunk;
+  // per-warp histograms (u16 counts): segments below 2^16 keys and the workspace's CTA slots
+  // used only when a select warp's segment spans several register batches (> 512 keys: the 1M case), where
+  // the select's counting pass would read the scores twice; below that the counting pass runs on registers and
+  // measured faster than the scan's extra epilogue (128K: 48.0 vs 48.9 us/layer; 1M: 192.6 vs 194.7)
+  const uint32_t wseg = warp_seg((uint32_t)std::min<int64_t>(chunk, 1 << 30));
+  p.warp_hist = wseg > 4 * 128 && wseg < 65536 &&
+                (int64_t)nch * units <= ix->ws->warp_hist_ctas && warp_hist_on();
   return p;
 }
 
@@ -562,13 +620,13 @@ cudaError_t launch_scan(const pkv_index* ix, int64_t n, const ScanPlan& plan, cu
   if (ix->smem_reserved == 1024) {
     ProfScope p_(K_SCAN, stream);
     e = pdl_launch(scan_kernel<1024>, grid, dim3(SCAN_THREADS), SCAN_SMEM, stream, (const uint8_t*)ix->ids,
-                   (const uint32_t*)ws->lut, ws->scores, ws->chunk_hist, ix->cap, score_stride(ix), n, plan.chunk,
-                   ix->dcfg.G);
+                   (const uint32_t*)ws->lut, ws->scores, ws->chunk_hist, plan.warp_hist ? ws->warp_hist : nullptr,
+                   ix->cap, score_stride(ix), n, plan.chunk, ix->dcfg.G);
   } else {
     ProfScope p_(K_SCAN, stream);
     e = pdl_launch(scan_kernel<0>, grid, dim3(SCAN_THREADS), SCAN_SMEM, stream, (const uint8_t*)ix->ids,
-                   (const uint32_t*)ws->lut, ws->scores, ws->chunk_hist, ix->cap, score_stride(ix), n, plan.chunk,
-                   ix->dcfg.G);
+                   (const uint32_t*)ws->lut, ws->scores, ws->chunk_hist, plan.warp_hist ? ws->warp_hist : nullptr,
+                   ix->cap, score_stride(ix), n, plan.chunk, ix->dcfg.G);
   }
   return e;
 }
@@ -600,7 +658,8 @@ cudaError_t launch_select(const pkv_index* ix, int64_t n, const ScanPlan& plan, 
                         ? (const uint8_t*)ix->rec
                         : (const uint8_t*)nullptr,
                     ix->cap * ix->dcfg.rec_bytes, ix->dcfg.rec_bytes, ws->ucount,
-                    union_rerank() ? ws->uid : (int32_t*)nullptr, ws->upos);
+                    union_rerank() ? ws->uid : (int32_t*)nullptr, ws->upos,
+                    plan.warp_hist ? (const uint16_t*)ws->warp_hist : (const uint16_t*)nullptr);
 }
 
 cudaError_t launch_dbg_scores(const pkv_index* ix, int64_t n, uint8_t* out, cudaStream_t stream) {
