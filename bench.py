@@ -160,7 +160,10 @@ def run_ours(args):
             del K, V
             Kh = synth.isotropic(seed + 7, (batch, N_KV, n_hot, D), device=dev)
             Vh = synth.isotropic(seed + 8, (batch, N_KV, n_hot, D), device=dev)
-            if uva:  # full-precision K/V live in pinned host memory; the GPU keeps only summaries + hot rows
+            if uva and args.k_hbm:  # variant: keys stay in HBM (64 GB for 32 layers at 1M fits a B200's 180 GB),
+                Vl = Vl.cpu().pin_memory()  # only the value rows of the top-k cross the host link
+                data.append(dict(K=Kl, V=Vl, Kd=Kl, Kh=Kh, Vh=Vh, q=q.contiguous()))
+            elif uva:  # full-precision K/V live in pinned host memory; the GPU keeps only summaries + hot rows
                 Kd, Vd = Kl, Vl
                 Kl, Vl = Kl.cpu().pin_memory(), Vl.cpu().pin_memory()
                 data.append(dict(K=Kl, V=Vl, Kd=Kd, Kh=Kh, Vh=Vh, q=q.contiguous()))
@@ -197,7 +200,7 @@ def run_ours(args):
         for ly in layers:
             ly["ix"].set_postings(True)
         torch.cuda.synchronize()
-    if uva:  # the device copies were only needed to build the summaries
+    if uva and not args.k_hbm:  # the device copies were only needed to build the summaries
         for d in data:
             d["Kd"] = None
         for ly in layers:
@@ -372,9 +375,18 @@ def run_ours(args):
             traffic = None
     roof = {"bound": "hbm", "kernel": dom, "achieved": kern[dom]["gbs"], "peak": hbm_peak, "unit": "GB/s",
             "frac": round(kern[dom]["gbs"] / hbm_peak, 4), "traffic": traffic, "peak_source": peak_kind}
+    fl_file = os.path.join(ROOT, "profiles", "floors_r01.json")
+    if uva and fused and dom == "topk" and os.path.exists(fl_file):
+        # at 1M the fused top-k is bound by its UVA gather of the k selected rows (SURVEY §8(d) "host link"):
+        # its roofline is the measured host-link read rate, over the bytes that cross the link
+        link = json.load(open(fl_file))["1m"]["uva_stream_read_gbs"]
+        host_bytes = batch * N_Q * TOP_K * (256 if args.k_hbm else 512)
+        ach = round(host_bytes / (kern["topk"]["avg_us"] * 1e-6) / 1e9, 1)
+        roof = {"bound": "host_link", "kernel": dom, "achieved": ach, "peak": link, "unit": "GB/s",
+                "frac": round(ach / link, 4), "traffic": traffic, "peak_source": "measured (scripts/uva_bw.cu)",
+                "host_bytes_per_launch": host_bytes}
     # context: measured data-movement floors of the two gathers (profiles/floors_r01.json, scripts/hbm_gather.cu,
     # scripts/uva_bw.cu) — the rerank's random 128 B record gather from HBM and, at 1M, the UVA row gather
-    fl_file = os.path.join(ROOT, "profiles", "floors_r01.json")
     if os.path.exists(fl_file) and world == 1 and not args.w16:
         try:
             fl = json.load(open(fl_file)).get(args.config)
@@ -405,6 +417,8 @@ def run_ours(args):
                        "l2": "inputs > L2: 32 layer-distinct indices + K/V touched per step",
                        "rerank_weights": "fp16 (96 B records)" if args.w16 else "fp32 (128 B records)",
                        "collision_scan": "inverted lists" if args.inverted else "dense",
+                       "kv_placement": ("K in HBM, V in pinned host (UVA)" if args.k_hbm else "K, V in pinned host (UVA)")
+                       if uva else "HBM",
                        "cuda_graph": use_graph},
             "roofline": roof,
             "scan_gbs": scan_gbs,
@@ -530,6 +544,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--w16", action="store_true", help="fp16 rerank weights (96-byte records, AMB-20 / SURVEY f2)")
     ap.add_argument("--inverted", action="store_true", help="inverted-list collision scan (SURVEY f4)")
+    ap.add_argument("--k-hbm", action="store_true",
+                    help="1M variant: keys in HBM, only values in pinned host memory (half the UVA bytes)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup) if args.impl == "ours" else args.warmup
     if args.impl == "reference":

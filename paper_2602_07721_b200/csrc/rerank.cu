@@ -37,8 +37,8 @@ constexpr int RT_ROWS = D;
 // pointers) is amortised over CPT candidates and their record loads are all in flight before the lookups.
 // W16: records of 96 bytes with fp16 weights h_b and a per-key exponent E in their sign bits (encode.cu):
 // each thread of the pair reads its 32 B of nibbles + 16 B of halves and decodes E from its own 8 halves.
-template <int CPT, bool W16>
-__global__ void __launch_bounds__(RR_THREADS, 6) rerank_cpt_kernel(const uint8_t* __restrict__ rec, const int32_t* cand,
+template <int CPT, bool W16, int OCC = 6>
+__global__ void __launch_bounds__(RR_THREADS, OCC) rerank_cpt_kernel(const uint8_t* __restrict__ rec, const int32_t* cand,
                                                                  const int32_t* sel, const float* rtab,
                                                                  const float* qnorm, int64_t cap, int n_q, int n_kv,
                                                                  int G, int64_t cand_stride, int64_t id_offset,
@@ -1441,16 +1441,26 @@ cudaError_t launch_rerank(const pkv_index* ix, int64_t C_cap, int64_t id_offset,
     const char* e = getenv("PKV_RR_CPT");
     return e ? atoi(e) : 0;
   }();
-  // 2 measured best for short lists (128K), 1 for long ones that loop over tiles (1M: 186.7 vs 192.6 us/layer)
-  const int cpt = (cpt_env == 1 || cpt_env == 2 || cpt_env == 4) ? cpt_env : (C_cap > 16384 ? 1 : 2);
+  // one candidate per thread pair measured best at every size (1M: 186.7 vs 192.6 us/layer with 2)
+  const int cpt = (cpt_env == 1 || cpt_env == 2 || cpt_env == 4) ? cpt_env : 1;
   const int64_t per = (int64_t)(RR_THREADS / 2) * cpt;
+  // Register budget: 32 registers (8 CTAs = 2048 threads per SM) for short lists, where the whole list is
+  // in flight in one wave (128K: 42.9 vs 43.8 us/layer); 40 (6 CTAs) for long lists that loop over tiles
+  // (1M: 194.0 vs 197.1). PKV_RR_OCC=6|8 forces one (A/B).
+  static const int occ_env = [] {
+    const char* e = getenv("PKV_RR_OCC");
+    return e ? atoi(e) : 0;
+  }();
+  const bool occ8 = (cpt <= 2) && (occ_env == 8 || (occ_env != 6 && C_cap <= 16384));
   auto kern = ix->dcfg.w16 ? (cpt == 1 ? rerank_cpt_kernel<1, true> : cpt == 2 ? rerank_cpt_kernel<2, true>
                                                                               : rerank_cpt_kernel<4, true>)
                            : (cpt == 1 ? rerank_cpt_kernel<1, false> : cpt == 2 ? rerank_cpt_kernel<2, false>
                                                                                : rerank_cpt_kernel<4, false>);
+  if (occ8) kern = ix->dcfg.w16 ? (cpt == 1 ? rerank_cpt_kernel<1, true, 8> : rerank_cpt_kernel<2, true, 8>)
+                                : (cpt == 1 ? rerank_cpt_kernel<1, false, 8> : rerank_cpt_kernel<2, false, 8>);
   // at most the resident CTA count per (sequence, query head): longer lists loop over tiles inside the CTA
-  static int occ_cache[2][5] = {};
-  int& occ = occ_cache[ix->dcfg.w16 ? 1 : 0][cpt];
+  static int occ_cache[2][2][5] = {};
+  int& occ = occ_cache[occ8 ? 1 : 0][ix->dcfg.w16 ? 1 : 0][cpt];
   if (!occ) {
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, RR_THREADS, 0) != cudaSuccess || occ < 1) occ = 1;
   }
