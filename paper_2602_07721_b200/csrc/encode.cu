@@ -53,13 +53,17 @@ __device__ __forceinline__ void fwht128(T v[8], int lane16) {
 // One key (sequence/KV head bh, key tt of the call) per half-warp; lane16 = subspace.
 __device__ __forceinline__ void encode_one(const uint16_t* __restrict__ K, int64_t sb, int64_t sh, int64_t st,
                                            int64_t t0, int n_kv, int64_t cap, const DevCfg& cfg,
-                                           uint8_t* __restrict__ ids, uint8_t* __restrict__ rec, const float* sL,
-                                           int bh, int64_t tt, bool live) {
+                                           uint8_t* __restrict__ ids, uint8_t* __restrict__ rec, float* sL,
+                                           int bh, int64_t tt, bool live, bool stage) {
   const int lane16 = threadIdx.x & 15;
   const int b = bh / n_kv, h = bh - b * n_kv;
   const int64_t t = t0 + tt;
 
   const uint4 raw = ldg_nc_v4(K + b * sb + h * sh + tt * st + 8 * lane16);
+  if (stage) {  // the levels go to shared memory while the key is in flight (block-uniform)
+    if (threadIdx.x < 8) sL[threadIdx.x] = cfg.levels[threadIdx.x];
+    __syncthreads();
+  }
   const uint32_t w4[4] = {raw.x, raw.y, raw.z, raw.w};
   uint32_t e[8], mant[8], sgn[8];
   int emax = 0;
@@ -186,28 +190,33 @@ __device__ __forceinline__ void encode_one(const uint16_t* __restrict__ K, int64
   }
 }
 
-// list == nullptr: grid (ceil(count / 16), batch * n_kv), keys [t0, t0 + count). Otherwise the keys
-// list[0 .. *list_n) (entry = bh * count + tt, written by the tensor-core encoder for keys outside its exact
-// range), grid-stride over the list.
-__global__ void __launch_bounds__(256) encode_kernel(const uint16_t* __restrict__ K, int64_t sb, int64_t sh,
-                                                     int64_t st, int64_t t0, int64_t count, int n_kv,
-                                                     int64_t cap, DevCfg cfg, uint8_t* __restrict__ ids,
-                                                     uint8_t* __restrict__ rec, const int32_t* list,
-                                                     const int32_t* list_n) {
+// Grid (ceil(count / 16), batch * n_kv), keys [t0, t0 + count): 64 registers, 4 CTAs per SM (the list variant
+// below is a separate kernel: its grid-stride loop and index division in this one cost 95 registers and 27%).
+__global__ void __launch_bounds__(256, 4) encode_kernel(const uint16_t* __restrict__ K, int64_t sb, int64_t sh,
+                                                        int64_t st, int64_t t0, int64_t count, int n_kv,
+                                                        int64_t cap, DevCfg cfg, uint8_t* __restrict__ ids,
+                                                        uint8_t* __restrict__ rec) {
   __shared__ float sL[8];  // magnitude levels: per-lane indexed (a divergent constant-bank read would serialise)
+  int64_t tt = (int64_t)blockIdx.x * KEYS_PER_BLOCK + (threadIdx.x >> 4);
+  const bool live = tt < count;
+  if (!live) tt = count - 1;  // keep the half-warp shuffles full; results discarded
+  encode_one(K, sb, sh, st, t0, n_kv, cap, cfg, ids, rec, sL, blockIdx.y, tt, live, true);
+}
+
+// The keys list[0 .. *list_n) (entry = bh * count + tt, written by the tensor-core encoder for keys outside its
+// exact range), grid-stride over the list.
+__global__ void __launch_bounds__(256) encode_list_kernel(const uint16_t* __restrict__ K, int64_t sb, int64_t sh,
+                                                          int64_t st, int64_t t0, int64_t count, int n_kv,
+                                                          int64_t cap, DevCfg cfg, uint8_t* __restrict__ ids,
+                                                          uint8_t* __restrict__ rec, const int32_t* list,
+                                                          const int32_t* list_n) {
+  __shared__ float sL[8];
   if (threadIdx.x < 8) sL[threadIdx.x] = cfg.levels[threadIdx.x];
   __syncthreads();
-  if (list == nullptr) {
-    int64_t tt = (int64_t)blockIdx.x * KEYS_PER_BLOCK + (threadIdx.x >> 4);
-    const bool live = tt < count;
-    if (!live) tt = count - 1;  // keep the half-warp shuffles full; results discarded
-    encode_one(K, sb, sh, st, t0, n_kv, cap, cfg, ids, rec, sL, blockIdx.y, tt, live);
-  } else {
-    const int n = *list_n;
-    for (int kk = blockIdx.x * KEYS_PER_BLOCK + (threadIdx.x >> 4); kk < n; kk += gridDim.x * KEYS_PER_BLOCK) {
-      const int e = list[kk];
-      encode_one(K, sb, sh, st, t0, n_kv, cap, cfg, ids, rec, sL, (int)(e / count), e % count, true);
-    }
+  const int n = *list_n;
+  for (int kk = blockIdx.x * KEYS_PER_BLOCK + (threadIdx.x >> 4); kk < n; kk += gridDim.x * KEYS_PER_BLOCK) {
+    const int e = list[kk];
+    encode_one(K, sb, sh, st, t0, n_kv, cap, cfg, ids, rec, sL, (int)(e / count), e % count, true, false);
   }
 }
 
@@ -242,7 +251,7 @@ __global__ void export_kernel(const uint8_t* __restrict__ ids_in, const uint8_t*
 cudaError_t launch_encode_list(const pkv_index* ix, const void* K, int64_t sb, int64_t sh, int64_t st, int64_t t0,
                                int64_t count, const int32_t* list, const int32_t* list_n, cudaStream_t stream) {
   ProfScope p_(K_ENCODE, stream);
-  encode_kernel<<<ix->num_sms * 2, 256, 0, stream>>>(static_cast<const uint16_t*>(K), sb, sh, st, t0, count,
+  encode_list_kernel<<<ix->num_sms * 2, 256, 0, stream>>>(static_cast<const uint16_t*>(K), sb, sh, st, t0, count,
                                                      ix->cfg.n_kv_heads, ix->cap, ix->dcfg, ix->ids, ix->rec, list,
                                                      list_n);
   return cudaGetLastError();
@@ -254,7 +263,7 @@ cudaError_t launch_encode(const pkv_index* ix, const void* K, int64_t sb, int64_
   const dim3 grid((unsigned)((count + KEYS_PER_BLOCK - 1) / KEYS_PER_BLOCK), ix->batch * ix->cfg.n_kv_heads);
   ProfScope p_(K_ENCODE, stream);
   encode_kernel<<<grid, 256, 0, stream>>>(static_cast<const uint16_t*>(K), sb, sh, st, t0, count,
-                                          ix->cfg.n_kv_heads, ix->cap, ix->dcfg, ix->ids, ix->rec, nullptr, nullptr);
+                                          ix->cfg.n_kv_heads, ix->cap, ix->dcfg, ix->ids, ix->rec);
   return cudaGetLastError();
 }
 

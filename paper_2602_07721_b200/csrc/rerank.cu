@@ -979,6 +979,7 @@ __global__ void __launch_bounds__(BS_THREADS) topk_cl_kernel(const float* est, c
       if ((mb >> lane) & 1u) bnd[baseb + __popc(mb & below)] = ckey(e, icache[i]);
     }
     __syncthreads();
+    phase_mark(K_TOPK, 12);
     // ---- 4. exact selection inside the boundary bin (keys are unique), then the local order
     const int wc = s_wc, nb = s_bc, need = s_need;
     for (int i = tid; i < nb; i += BS_THREADS) {
@@ -990,6 +991,7 @@ __global__ void __launch_bounds__(BS_THREADS) topk_cl_kernel(const float* est, c
     __syncthreads();  // histogram reads done before it is reused as rk
     for (int i = tid; i < kl; i += BS_THREADS) rk[i] = 0;
     __syncthreads();
+    phase_mark(K_TOPK, 13);
     const int seg = (kl + CL_PARTS - 1) / CL_PARTS;
     for (int e = tid; e < CL_PARTS * kl; e += BS_THREADS) {
       const int i = e % kl, part = e / kl;
@@ -1000,6 +1002,7 @@ __global__ void __launch_bounds__(BS_THREADS) topk_cl_kernel(const float* est, c
       if (rr) atomicAdd(&rk[i], rr);
     }
     __syncthreads();
+    phase_mark(K_TOPK, 14);
     for (int i = tid; i < kl; i += BS_THREADS) lst[rk[i]] = win[i];
   }
   if (tid == 0) s_kl = kl;
