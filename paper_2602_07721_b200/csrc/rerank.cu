@@ -735,17 +735,15 @@ __global__ void __launch_bounds__(BS_THREADS) topk_kernel(const float* est, cons
 // ---------------------------------------------------------------- cluster top-k (+ gather/attention)
 // One thread-block cluster of R CTAs per (sequence, query head). CTA r owns candidates [r*per, (r+1)*per)
 // (per = ceil(count/R)), caches them in shared memory and selects their local top-k with the value-range
-// bucket select (exact, composite keys), sorted descending. The global top-k is contained in the union of the
-// R local lists, so after one cluster barrier every CTA copies its peers' lists (at most R*k*8 bytes of
+// bucket select (exact, composite keys), in no particular order. The global top-k is contained in the union of
+// the R local lists, so after one cluster barrier every CTA copies its peers' lists (at most R*k*8 bytes of
 // distributed shared memory — DSMEM bandwidth is ~20 B/clk per SM, so only these short lists cross it) and
-// ranks its own entries by binary search in them: global rank = local index + #peer entries greater. Entries
-// with rank < k are a prefix of the local list; the CTA writes them to out[rank] and, when ATTEND, gathers and
-// attends those rows (the hot rows r*per .. (r+1)*per were attended before the dependency wait, seeding the
+// ranks its own entries by counting: global rank = #entries greater in the R lists. The CTA writes its entries
+// with rank < k to out[rank] and, when ATTEND, gathers and attends those rows (the hot rows r*per .. (r+1)*per were attended before the dependency wait, seeding the
 // online-softmax state), sending one (m, l, o) partial to CTA 0, which merges the
 // R partials (log2 domain) after the second and last cluster barrier.
 constexpr int CL_MAX = 8;
 constexpr int CL_SLICE = 16384;  // candidates per CTA (est + id cached: 8 B each)
-constexpr int CL_PARTS = 8;      // threads counting one local winner's rank
 
 struct SmemCand {  // radix fallback source: the CTA's cached slice
   const float* est;
@@ -774,7 +772,7 @@ __global__ void __launch_bounds__(BS_THREADS) topk_cl_kernel(const float* est, c
   __shared__ float cpart[CL_MAX][PART];  // CTA 0: the cluster's attention partials
   __shared__ float red_mn[NW], red_mx[NW];
   __shared__ unsigned int wsum[NW];
-  __shared__ int s_wc, s_bc, s_bstar, s_need, s_bcount, s_kl, s_nwin;
+  __shared__ int s_wc, s_bc, s_bstar, s_need, s_bcount, s_kl;
   const int R = (int)cl.num_blocks(), r = (int)cl.block_rank();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int h = blockIdx.y, b = blockIdx.z;
@@ -895,7 +893,6 @@ __global__ void __launch_bounds__(BS_THREADS) topk_cl_kernel(const float* est, c
     s_bstar = -1;
     s_need = 0;
     s_bcount = 0;
-    s_nwin = 0;
   }
   __syncthreads();
   mn = red_mn[lane % NW];
@@ -956,7 +953,34 @@ __global__ void __launch_bounds__(BS_THREADS) topk_cl_kernel(const float* est, c
     __syncthreads();
     for (int i = tid; i < kl; i += BS_THREADS) lst[i] = ckey(tes[i], tix[i]);
   } else {
-    // ---- 3. partition: above the boundary bin -> win, inside it -> bnd (warp-aggregated smem atomics)
+    // ---- 3. partition: above the boundary bin -> win, inside it -> bnd. Two passes over the cached slice: the
+    // per-warp counts, one scan of them, then every warp writes at its own offsets (no contended atomics;
+    // deterministic order)
+    __shared__ int pw_w[NW], pw_b[NW];
+    int cw = 0, cb = 0;
+    for (int i0 = 0; i0 < n_loc; i0 += BS_THREADS) {
+      const int i = i0 + tid;
+      const int bb = i < n_loc ? ((bstar < 0) ? BS_BINS : bin_of(ecache[i])) : -2;
+      cw += __popc(__ballot_sync(0xffffffffu, i < n_loc && bb > bstar));
+      cb += __popc(__ballot_sync(0xffffffffu, i < n_loc && bb == bstar));
+    }
+    if (lane == 0) {
+      pw_w[warp] = cw;
+      pw_b[warp] = cb;
+    }
+    __syncthreads();
+    int basew = 0, baseb = 0, totw = 0, totb = 0;
+    for (int w = 0; w < NW; ++w) {
+      basew += w < warp ? pw_w[w] : 0;
+      baseb += w < warp ? pw_b[w] : 0;
+      totw += pw_w[w];
+      totb += pw_b[w];
+    }
+    if (tid == 0) {
+      s_wc = totw;
+      s_bc = totb;
+    }
+    const unsigned below = (1u << lane) - 1u;
     for (int i0 = 0; i0 < n_loc; i0 += BS_THREADS) {
       const int i = i0 + tid;
       float e = 0.f;
@@ -967,20 +991,14 @@ __global__ void __launch_bounds__(BS_THREADS) topk_cl_kernel(const float* est, c
       }
       const unsigned mw = __ballot_sync(0xffffffffu, i < n_loc && bb > bstar);
       const unsigned mb = __ballot_sync(0xffffffffu, i < n_loc && bb == bstar);
-      int basew = 0, baseb = 0;
-      if (lane == 0) {
-        if (mw) basew = atomicAdd(&s_wc, __popc(mw));
-        if (mb) baseb = atomicAdd(&s_bc, __popc(mb));
-      }
-      basew = __shfl_sync(0xffffffffu, basew, 0);
-      baseb = __shfl_sync(0xffffffffu, baseb, 0);
-      const unsigned below = (1u << lane) - 1u;
       if ((mw >> lane) & 1u) win[basew + __popc(mw & below)] = ckey(e, icache[i]);
       if ((mb >> lane) & 1u) bnd[baseb + __popc(mb & below)] = ckey(e, icache[i]);
+      basew += __popc(mw);
+      baseb += __popc(mb);
     }
     __syncthreads();
     phase_mark(K_TOPK, 12);
-    // ---- 4. exact selection inside the boundary bin (keys are unique), then the local order
+    // ---- 4. exact selection inside the boundary bin (keys are unique): the local top-kl, in no order
     const int wc = s_wc, nb = s_bc, need = s_need;
     for (int i = tid; i < nb; i += BS_THREADS) {
       const unsigned long long x = bnd[i];
@@ -988,57 +1006,51 @@ __global__ void __launch_bounds__(BS_THREADS) topk_cl_kernel(const float* est, c
       for (int j2 = 0; j2 < nb; ++j2) rr += bnd[j2] > x;
       if (rr < need) win[wc + rr] = x;
     }
-    __syncthreads();  // histogram reads done before it is reused as rk
-    for (int i = tid; i < kl; i += BS_THREADS) rk[i] = 0;
     __syncthreads();
     phase_mark(K_TOPK, 13);
-    const int seg = (kl + CL_PARTS - 1) / CL_PARTS;
-    for (int e = tid; e < CL_PARTS * kl; e += BS_THREADS) {
-      const int i = e % kl, part = e / kl;
-      const unsigned long long x = win[i];
-      int rr = 0;
-      const int j1 = min(kl, (part + 1) * seg);
-      for (int j2 = part * seg; j2 < j1; ++j2) rr += win[j2] > x;
-      if (rr) atomicAdd(&rk[i], rr);
-    }
-    __syncthreads();
-    phase_mark(K_TOPK, 14);
-    for (int i = tid; i < kl; i += BS_THREADS) lst[rk[i]] = win[i];
+    for (int i = tid; i < kl; i += BS_THREADS) lst[i] = win[i];
   }
   if (tid == 0) s_kl = kl;
   phase_mark(K_TOPK, 4);
-  cl.sync();  // #1: every CTA's sorted local list is published
+  cl.sync();  // #1: every CTA's local list is published
   phase_mark(K_TOPK, 5);
 
-  // ---- 5. peers' lists copied in (DSMEM), global rank of the local entries by binary search
+  // ---- 5. all R lists side by side (peers' over DSMEM, this CTA's own), then the global rank of each local
+  // entry x by counting: rank(x) = #{entries > x in the R lists} (composite keys are unique). Thread (i, pr)
+  // counts list pr for entry i with broadcast shared-memory reads — no sort of the local list, no binary
+  // searches. The rank-indexed slots win[0..kv) receive this CTA's winners.
+  constexpr unsigned long long EMPTY = ~0ull;  // no candidate key has id 0xffffffff
   unsigned long long* plist = reinterpret_cast<unsigned long long*>(ecache);  // [R][k]
   __shared__ int pk[CL_MAX];
-  if (tid < R) pk[tid] = (tid == r) ? 0 : *cl.map_shared_rank(&s_kl, tid);
+  if (tid < R) pk[tid] = (tid == r) ? kl : *cl.map_shared_rank(&s_kl, tid);
   __syncthreads();
-  for (int pr = 0; pr < R; ++pr) {
-    if (pr == r) continue;
-    const unsigned long long* src = cl.map_shared_rank(lst, pr);
-    for (int i = tid; i < pk[pr]; i += BS_THREADS) plist[pr * k + i] = src[i];
+  for (int e = tid; e < R * k; e += BS_THREADS) {  // one element per thread: all DSMEM reads in flight at once
+    const int pr = e / k, i = e - pr * k;
+    if (i < pk[pr]) plist[e] = (pr == r) ? lst[i] : *cl.map_shared_rank(lst + i, pr);
   }
+  for (int i = tid; i < kl; i += BS_THREADS) rk[i] = 0;  // (the histogram it aliases is dead)
+  for (int i = tid; i < kv; i += BS_THREADS) win[i] = EMPTY;
   __syncthreads();
   phase_mark(K_TOPK, 6);
-  for (int i = tid; i < kl; i += BS_THREADS) {
+  for (int e = tid; e < kl * R; e += BS_THREADS) {
+    const int i = e % kl, pr = e / kl;
     const unsigned long long x = lst[i];
-    int rank = i;
-    for (int pr = 0; pr < R; ++pr) {
-      const unsigned long long* L = plist + pr * k;
-      int a = 0, z = pk[pr];  // number of entries > x in the descending list L[0..pk)
-      while (a < z) {
-        const int m = (a + z) >> 1;
-        if (L[m] > x) a = m + 1;
-        else z = m;
-      }
-      rank += a;
-    }
+    const unsigned long long* L = plist + pr * k;
+    const int n_l = pk[pr];
+    int c = 0;
+#pragma unroll 8
+    for (int j = 0; j < n_l; ++j) c += L[j] > x;
+    if (c) atomicAdd(&rk[i], c);
+  }
+  __syncthreads();
+  phase_mark(K_TOPK, 14);
+  for (int i = tid; i < kl; i += BS_THREADS) {
+    const int rank = rk[i];
     if (rank < kv) {
+      const unsigned long long x = lst[i];
       oi[rank] = (int32_t)(uint32_t)(x & 0xffffffffull);
       oe[rank] = unord_f32((uint32_t)(x >> 32));
-      atomicMax(&s_nwin, i + 1);
+      win[rank] = x;
     }
   }
   if (r == 0)
@@ -1047,11 +1059,28 @@ __global__ void __launch_bounds__(BS_THREADS) topk_cl_kernel(const float* est, c
       oe[i] = -INFINITY;
     }
   __syncthreads();
+  // this CTA's winners compacted in rank order into bnd[0..nwin) (ordered ballot compaction over the slots)
+  int nwin = 0;
+  for (int t0 = 0; t0 < kv; t0 += BS_THREADS) {
+    const int t = t0 + tid;
+    const bool f = t < kv && win[t] != EMPTY;
+    const unsigned mk = __ballot_sync(0xffffffffu, f);
+    if (lane == 0) wsum[warp] = __popc(mk);
+    __syncthreads();
+    int before = nwin, tot = 0;
+    for (int w = 0; w < NW; ++w) {
+      const int c = (int)wsum[w];
+      before += w < warp ? c : 0;
+      tot += c;
+    }
+    if (f) bnd[before + __popc(mk & ((1u << lane) - 1u))] = win[t];
+    nwin += tot;
+    __syncthreads();
+  }
   phase_mark(K_TOPK, 7);
 
   if constexpr (ATTEND) {
-    // ---- 6. attention over the local winners lst[0..nwin), continuing the hot-row state
-    const int nwin = s_nwin;
+    // ---- 6. attention over this CTA's winners bnd[0..nwin), continuing the hot-row state
     const int g = h / ep.G;
     const uint16_t* Kb = static_cast<const uint16_t*>(ep.K) + (int64_t)b * ep.sb + (int64_t)g * ep.sh + 4 * lane;
     const uint16_t* Vb = static_cast<const uint16_t*>(ep.V) + (int64_t)b * ep.sb + (int64_t)g * ep.sh + 4 * lane;
@@ -1062,7 +1091,7 @@ __global__ void __launch_bounds__(BS_THREADS) topk_cl_kernel(const float* est, c
 #pragma unroll
       for (int u = 0; u < RB; ++u) {
         const int j = j0 + u * NW;
-        id[u] = j < nwin ? (int)(uint32_t)(lst[j] & 0xffffffffull) : -1;
+        id[u] = j < nwin ? (int)(uint32_t)(bnd[j] & 0xffffffffull) : -1;
       }
       uint2 kr[RB], vr[RB];
 #pragma unroll
