@@ -136,21 +136,47 @@ __global__ void __launch_bounds__(QP_THREADS) qprep_kernel(const uint16_t* q, in
     e.k = ~ord_f64(neg ? -acc : acc);  // ascending key == descending score; ties by ascending id
     e.id = neg ? (uint32_t)(NC - 1 - t) : (uint32_t)t;
   }
+  // Fast path: when the fp64 scores have 8 trailing zero mantissa bits (always, unless the query spans more than
+  // ~27 binades: each y' is an exact sum of bf16 values and the 8-term score sums are exact too), the leader id
+  // fits in those bits and the sort moves one 64-bit composite (2 shuffles per stage instead of 3): ordering by
+  // composite == ordering by (key, id). Otherwise the (key, id) pair network below.
+  if (__syncthreads_and((e.k & 0xffull) == 0xffull)) {
+    unsigned long long c = (e.k & ~0xffull) | e.id;
 #pragma unroll
-  for (int k = 2; k <= NC / 2; k <<= 1) {
+    for (int k = 2; k <= NC / 2; k <<= 1) {
 #pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      KV o;
-      if (j < 32) {
-        o = shfl_kv(e, j);
-      } else {
-        sk[t] = e.k;
-        si[t] = e.id;
-        __syncthreads();
-        o = KV{sk[t ^ j], si[t ^ j]};
-        __syncthreads();
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        unsigned long long o;
+        if (j < 32) {
+          o = __shfl_xor_sync(0xffffffffu, c, j);
+        } else {
+          sk[t] = c;
+          __syncthreads();
+          o = sk[t ^ j];
+          __syncthreads();
+        }
+        const bool keep_min = (((t & j) == 0) == ((t & k) == 0));
+        c = (keep_min == (o < c)) ? o : c;
       }
-      ce(e, o, t, k, j);
+    }
+    e.id = (uint32_t)(c & 0xffull);
+  } else {
+#pragma unroll
+    for (int k = 2; k <= NC / 2; k <<= 1) {
+#pragma unroll
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        KV o;
+        if (j < 32) {
+          o = shfl_kv(e, j);
+        } else {
+          sk[t] = e.k;
+          si[t] = e.id;
+          __syncthreads();
+          o = KV{sk[t ^ j], si[t ^ j]};
+          __syncthreads();
+        }
+        ce(e, o, t, k, j);
+      }
     }
   }
   phase_mark(K_QPREP, 3);

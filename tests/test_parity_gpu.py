@@ -165,6 +165,15 @@ def test_degenerate_and_wide_range_keys(pkv):
     run_and_check(pkv, K, q, V, k=64)
 
 
+def test_wide_range_queries(pkv):
+    """Queries spanning > 27 binades: the fp64 centroid scores lose their 8 trailing zero bits, so the query prep
+    ranks with the (key, id) pair network instead of the packed 64-bit composite; one head per path."""
+    K, q, V = make_problem(19, 1, 4, 1, 3000, plant=False)
+    q[0, 0, :64] = q[0, 0, :64] * 1e-10   # 2^-33 next to O(1) values: after the rotation every subspace mixes them
+    q[0, 1, 1::2] = q[0, 1, 1::2] * 1e-12
+    run_and_check(pkv, K, q, V, k=64)
+
+
 def test_append_equals_prefill(pkv):
     K, q, V = make_problem(10, 1, 8, 2, 4000)
     cfg = pkv.config_init(8, 2, SB)
