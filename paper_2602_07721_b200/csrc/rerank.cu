@@ -735,14 +735,16 @@ __global__ void __launch_bounds__(BS_THREADS) topk_kernel(const float* est, cons
 // ---------------------------------------------------------------- cluster top-k (+ gather/attention)
 // One thread-block cluster of R CTAs per (sequence, query head). CTA r owns candidates [r*per, (r+1)*per)
 // (per = ceil(count/R)), caches them in shared memory and selects their local top-k with the value-range
-// bucket select (exact, composite keys), in no particular order. The global top-k is contained in the union of
-// the R local lists, so after one cluster barrier every CTA copies its peers' lists (at most R*k*8 bytes of
-// distributed shared memory — DSMEM bandwidth is ~20 B/clk per SM, so only these short lists cross it) and
-// ranks its own entries by counting: global rank = #entries greater in the R lists. The CTA writes its entries
+// bucket select (exact, composite keys), sorted descending by split rank counting. The global top-k is contained
+// in the union of the R local lists, so after one cluster barrier every CTA copies its peers' lists (at most
+// R*k*8 bytes of distributed shared memory — DSMEM bandwidth is ~20 B/clk per SM, so only these short lists
+// cross it) and ranks its own entries: global rank = local index + #peer entries greater, one binary search per
+// (entry, peer list) pair, all in parallel. The CTA writes its entries
 // with rank < k to out[rank] and, when ATTEND, gathers and attends those rows (the hot rows r*per .. (r+1)*per were attended before the dependency wait, seeding the
 // online-softmax state), sending one (m, l, o) partial to CTA 0, which merges the
 // R partials (log2 domain) after the second and last cluster barrier.
 constexpr int CL_MAX = 8;
+constexpr int CL_PARTS = 8;  // threads counting one local entry's rank within the CTA's list
 constexpr int CL_SLICE = 16384;  // candidates per CTA (est + id cached: 8 B each)
 
 struct SmemCand {  // radix fallback source: the CTA's cached slice
@@ -857,17 +859,17 @@ __global__ void __launch_bounds__(BS_THREADS) topk_cl_kernel(const float* est, c
   float* oe = out_est + bhq * out_stride;
   // ---- 1. cache the slice, min / max
   float mn = INFINITY, mx = -INFINITY;
-  for (int i0 = 0; i0 < n_loc; i0 += 8 * BS_THREADS) {
-    float ev[8];
-    int32_t iv[8];
+  for (int i0 = 0; i0 < n_loc; i0 += 16 * BS_THREADS) {  // 16 per thread: an 8K slice (1M) in one round trip
+    float ev[16];
+    int32_t iv[16];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < 16; ++u) {
       const int i = i0 + u * BS_THREADS + tid;
       ev[u] = i < n_loc ? es[lo + i] : 0.f;
       iv[u] = i < n_loc ? ids[lo + i] : 0;
     }
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < 16; ++u) {
       const int i = i0 + u * BS_THREADS + tid;
       if (i < n_loc) {
         ecache[i] = ev[u];
@@ -1008,7 +1010,20 @@ __global__ void __launch_bounds__(BS_THREADS) topk_cl_kernel(const float* est, c
     }
     __syncthreads();
     phase_mark(K_TOPK, 13);
-    for (int i = tid; i < kl; i += BS_THREADS) lst[i] = win[i];
+    // local order (descending) by split rank counting: CL_PARTS threads per entry, kl/CL_PARTS comparisons each
+    for (int i = tid; i < kl; i += BS_THREADS) rk[i] = 0;  // rk aliases the histogram (dead since step 2)
+    __syncthreads();
+    const int seg = (kl + CL_PARTS - 1) / CL_PARTS;
+    for (int e = tid; e < CL_PARTS * kl; e += BS_THREADS) {
+      const int i = e % kl, part = e / kl;
+      const unsigned long long x = win[i];
+      int rr = 0;
+      const int j1 = min(kl, (part + 1) * seg);
+      for (int j2 = part * seg; j2 < j1; ++j2) rr += win[j2] > x;
+      if (rr) atomicAdd(&rk[i], rr);
+    }
+    __syncthreads();
+    for (int i = tid; i < kl; i += BS_THREADS) lst[rk[i]] = win[i];
   }
   if (tid == 0) s_kl = kl;
   phase_mark(K_TOPK, 4);
@@ -1016,9 +1031,8 @@ __global__ void __launch_bounds__(BS_THREADS) topk_cl_kernel(const float* est, c
   phase_mark(K_TOPK, 5);
 
   // ---- 5. all R lists side by side (peers' over DSMEM, this CTA's own), then the global rank of each local
-  // entry x by counting: rank(x) = #{entries > x in the R lists} (composite keys are unique). Thread (i, pr)
-  // counts list pr for entry i with broadcast shared-memory reads — no sort of the local list, no binary
-  // searches. The rank-indexed slots win[0..kv) receive this CTA's winners.
+  // entry x: rank(x) = #{entries > x in the R lists} (composite keys are unique) = its local index + one binary
+  // search per peer list. The rank-indexed slots win[0..kv) receive this CTA's winners.
   constexpr unsigned long long EMPTY = ~0ull;  // no candidate key has id 0xffffffff
   unsigned long long* plist = reinterpret_cast<unsigned long long*>(ecache);  // [R][k]
   __shared__ int pk[CL_MAX];
@@ -1032,14 +1046,20 @@ __global__ void __launch_bounds__(BS_THREADS) topk_cl_kernel(const float* est, c
   for (int i = tid; i < kv; i += BS_THREADS) win[i] = EMPTY;
   __syncthreads();
   phase_mark(K_TOPK, 6);
-  for (int e = tid; e < kl * R; e += BS_THREADS) {
+  for (int e = tid; e < kl * R; e += BS_THREADS) {  // thread (entry i, list pr): binary search, all in parallel
     const int i = e % kl, pr = e / kl;
     const unsigned long long x = lst[i];
-    const unsigned long long* L = plist + pr * k;
-    const int n_l = pk[pr];
-    int c = 0;
-#pragma unroll 8
-    for (int j = 0; j < n_l; ++j) c += L[j] > x;
+    int c = i;  // own list: sorted descending, so i entries are greater
+    if (pr != r) {
+      const unsigned long long* L = plist + pr * k;
+      int a = 0, z = pk[pr];  // number of entries > x in the descending list L[0..pk)
+      while (a < z) {
+        const int m = (a + z) >> 1;
+        if (L[m] > x) a = m + 1;
+        else z = m;
+      }
+      c = a;
+    }
     if (c) atomicAdd(&rk[i], c);
   }
   __syncthreads();

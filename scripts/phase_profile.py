@@ -14,7 +14,7 @@ from paper_2602_07721_b200 import pariskv as pkv  # noqa: E402
 
 pkv._lib.pkv_phase_profile.argtypes = [ctypes.c_void_p]
 dev = torch.device("cuda", 0)
-n = 131072 - 272
+n = int(os.environ.get("PHASE_CTX", "131072")) - 272  # PHASE_CTX=1048576 PHASE_UVA=1: the 1M configuration
 stats = synth.head_stats(0, 8, device=dev)
 K = synth.llm_keys(0, 1, 8, n, device=dev, stats=stats)
 q = synth.llm_queries(0, 1, 32, 8, device=dev, stats=stats)
@@ -25,6 +25,10 @@ Vh = synth.isotropic(8, (1, 8, 272, 128), device=dev)
 cfg = pkv.config_init(32, 8, synth.rotation_sign_bits())
 ix = pkv.Index(cfg, 1, n)
 pkv.encode_keys(ix, K)
+if os.environ.get("PHASE_UVA") == "1":  # K/V rows read through UVA from pinned host memory
+    torch.cuda.synchronize()
+    K, V = K.cpu().pin_memory(), V.cpu().pin_memory()
+    torch.cuda.empty_cache()
 for _ in range(3):
     pkv.retrieve_and_attend(ix, q, K, V, 100, Kh, Vh)
 torch.cuda.synchronize()
