@@ -463,8 +463,10 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(
     toff[hh] = p_tie_off[hh];
   }
   int32_t* const cd0 = cand + ((int64_t)b * n_q + g * G) * cand_stride;
+  const int cs = (int)cand_stride;  // the group's lists span < 4 * capacity < 2^31 entries: 32-bit offsets
   const int32_t idoff = (int32_t)id_offset;
   const uint32_t lt = (1u << lane) - 1u;
+  const bool do_prefetch = rec != nullptr, do_union = uid != nullptr;
   phase_mark(K_SELECT, 4);
   // pass 2: keys with score >= s* for at least one head (~4 x beta of them) are first compacted, in key
   // order, into a per-warp list; the per-head ballots then run over that list only. Key (lane l, element e)
@@ -508,25 +510,26 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(
     for (uint32_t l0 = 0; l0 < nl; l0 += 32) {
       const bool valid = l0 + lane < nl;
       const uint2 ent = valid ? wl[l0 + lane] : make_uint2(0u, 0u);
-      if (valid && rec != nullptr) {  // warm L2 with the record the rerank kernel will gather for this key
+      if (valid && do_prefetch) {  // warm L2 with the record the rerank kernel will gather for this key
         const uint8_t* r = rec + (int64_t)bh * rec_head_bytes + (int64_t)ent.x * rec_bytes;
         asm volatile("prefetch.global.L2 [%0];" ::"l"(r));
         if (rec_bytes != 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(r + rec_bytes - 1));
       }
       int pos[GMAX];
+      const int32_t gid = (int32_t)ent.x + idoff;
 #pragma unroll
       for (int hh = 0; hh < GMAX; ++hh) {
-        const bool fg = (ent.y >> (8 * hh + 7)) & 1u;
-        const bool fe = (ent.y >> (8 * hh + 6)) & 1u;
+        const bool fg = (ent.y & (0x80u << (8 * hh))) != 0u;
+        const bool fe = (ent.y & (0x40u << (8 * hh))) != 0u;
         const uint32_t mg = __ballot_sync(0xffffffffu, fg);
         const uint32_t me = __ballot_sync(0xffffffffu, fe);
         const int fend = eqe[hh] - __popc(me & lt);
         pos[hh] = fg ? gtp[hh] + __popc(mg & lt) : (fe && fend < take[hh]) ? toff[hh] + fend : -1;
-        if (pos[hh] >= 0) cd0[hh * cand_stride + pos[hh]] = (int32_t)ent.x + idoff;
+        if (pos[hh] >= 0) cd0[hh * cs + pos[hh]] = gid;
         gtp[hh] += __popc(mg);
         eqe[hh] -= __popc(me);
       }
-      if (uid != nullptr) {  // union entry: the key once, with its position in every head's candidate list
+      if (do_union) {  // union entry: the key once, with its position in every head's candidate list
         const bool any = (pos[0] & pos[1] & pos[2] & pos[3]) != -1;  // positions >= 0, or -1
         const uint32_t ma = __ballot_sync(0xffffffffu, any);
         uint32_t ub = 0;
