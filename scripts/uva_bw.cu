@@ -33,6 +33,18 @@ __global__ void gather_rows(const uint16_t* __restrict__ K, const uint16_t* __re
   if (acc == 0x12345678u) out[0] = acc;
 }
 
+// one instruction per row: lanes 0-15 read the K row (16 B each), lanes 16-31 the V row
+__global__ void gather_rows_v4(const uint16_t* __restrict__ K, const uint16_t* __restrict__ V,
+                               const int* __restrict__ ids, int R, unsigned* out) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= R) return;
+  const int64_t row = ids[warp];
+  const uint16_t* src = (lane < 16 ? K : V) + row * 128 + 8 * (lane & 15);
+  const uint4 v = *reinterpret_cast<const uint4*>(src);
+  const uint32_t acc = v.x ^ v.y ^ v.z ^ v.w;
+  if (acc == 0x12345678u) out[0] = acc;
+}
+
 int main() {
   const size_t bytes = 256ull << 20;
   void *hbuf, *dbuf;
@@ -88,6 +100,16 @@ int main() {
       if (ms < best) best = ms;
     }
     printf("uva_gather rows=%d bytes=%d us=%.2f GBs=%.1f\n", R, R * 512, best * 1e3, R * 512.0 / (best * 1e-3) / 1e9);
+    best = 1e30f;
+    for (int it = 0; it < 10; ++it) {
+      CK(cudaEventRecord(a));
+      gather_rows_v4<<<(R * 32 + 255) / 256, 256>>>(K, V, dids, R, dout);
+      CK(cudaEventRecord(b));
+      CK(cudaEventSynchronize(b));
+      CK(cudaEventElapsedTime(&ms, a, b));
+      if (ms < best) best = ms;
+    }
+    printf("uva_gather_v4 rows=%d bytes=%d us=%.2f GBs=%.1f\n", R, R * 512, best * 1e3, R * 512.0 / (best * 1e-3) / 1e9);
     CK(cudaFree(dids));
   }
   return 0;
