@@ -3,10 +3,10 @@
 // multi-tier collision bonuses, written as one byte per query head into the packed u32 lookup table
 // of the scan; also the rerank tables sign*L[idx]*q~_j used by the RSQ-IP estimate (Eq. 10).
 //
-// Grid (16 subspaces, n_q heads, batch), 128 threads. Exact contract shared with the oracle (AMB-9):
+// Grid (8 subspace pairs, n_q heads, batch), 128 threads. Exact contract shared with the oracle (AMB-9):
 // y' = fp64 butterflies of s (.) q; score_c = fp64 left-to-right sum of +-y'_j from 0.0; order (score desc,
-// id asc). The complement symmetry score(255-c) = -score(c) halves the sort to 128 "leaders", one per thread;
-// the bitonic network runs in registers and warp shuffles, only its 3 stages with distance >= 32 in smem.
+// id asc). The complement symmetry score(255-c) = -score(c) halves the sort to 128 "leaders", two per thread;
+// the bitonic network runs in registers and warp shuffles, only its stage with distance 64 in smem.
 #include "common.cuh"
 
 namespace pkv {
@@ -36,23 +36,29 @@ __device__ __forceinline__ void ce(KV& mine, const KV& o, int p, int k, int j) {
   mine.id = take ? o.id : mine.id;
 }
 
+// CTA = two subspaces (sb0 = 2*blockIdx.x, sb0 + 1) of one query head, 64 threads each, 2 leaders per thread
+// (position p = 2*tl + i): distance 1 inside a thread, 2..32 by shuffles, 64 through shared memory. 128-thread
+// CTAs, half the CTAs of one subspace per CTA: a batch of 8 x 32 heads fits one wave.
 __global__ void __launch_bounds__(QP_THREADS) qprep_kernel(const uint16_t* q, int T, DevCfg cfg,
                                                           uint32_t* lut, float* rtab,
                                                           float* qnorm, float* qrot,
                                                           float* dbg_q_rot, unsigned int* ucount) {
-  __shared__ unsigned long long sk[NC / 2];
-  __shared__ uint32_t si[NC / 2];
+  __shared__ unsigned long long sk[2][NC / 2];
+  __shared__ uint32_t si[2][NC / 2];
   phase_mark(K_QPREP, 0);
-  const int sb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int h = blockIdx.y, b = blockIdx.z;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int half = t >> 6, tl = t & 63;  // this thread's subspace (of the pair) and its index in that sort
+  const int sb = 2 * blockIdx.x + half;
   const int g = h / cfg.G, hh = h % cfg.G;
   pdl_wait();  // the query of this layer follows the previous layer's work
   pdl_trigger();
-  if (sb == 0 && hh == 0 && t == 0) ucount[b * cfg.n_kv + g] = 0u;  // the select of this step counts from 0
+  if (blockIdx.x == 0 && hh == 0 && t == 0) ucount[b * cfg.n_kv + g] = 0u;  // the select counts from 0
   phase_mark(K_QPREP, 1);
-  // warp 0 rotates the query (fp64 butterflies) and publishes this subspace's 8 coordinates and 1/||y'||
-  __shared__ double s_yb[8];
+  // warp 0 rotates the query (fp64 butterflies) and publishes the pair's 16 coordinates and 1/||y'||
+  __shared__ double s_yb[16];
   __shared__ double s_inv;
+  const int sp = 2 * blockIdx.x;  // first subspace of the pair: coordinates 8sp .. 8sp+15 = lanes 2sp .. 2sp+3
   if (warp == 0) {
     const uint16_t* qh = q + ((int64_t)b * cfg.n_q + h) * D;
     const uint2 raw = ldg_v2(qh + 4 * lane);
@@ -93,9 +99,9 @@ __global__ void __launch_bounds__(QP_THREADS) qprep_kernel(const uint16_t* q, in
       qn2 += __shfl_xor_sync(0xffffffffu, qn2, x);
     }
     const double inv_yn = yn2 > 0.0 ? 1.0 / sqrt(yn2) : 0.0;
-    if (lane == 2 * sb || lane == 2 * sb + 1) {
+    if (lane >= 2 * sp && lane < 2 * sp + 4) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) s_yb[4 * (lane - 2 * sb) + i] = v[i];
+      for (int i = 0; i < 4; ++i) s_yb[4 * (lane - 2 * sp) + i] = v[i];
       float* qr = qrot + ((int64_t)b * cfg.n_q + h) * D;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
@@ -104,93 +110,126 @@ __global__ void __launch_bounds__(QP_THREADS) qprep_kernel(const uint16_t* q, in
       }
     }
     if (lane == 0) s_inv = inv_yn;
-    if (sb == 0 && lane == 0) qnorm[(int64_t)b * cfg.n_q + h] = sqrtf(qn2);
+    if (blockIdx.x == 0 && lane == 0) qnorm[(int64_t)b * cfg.n_q + h] = sqrtf(qn2);
   }
   __syncthreads();
   double yb[8];
 #pragma unroll
-  for (int j = 0; j < 8; ++j) yb[j] = s_yb[j];
+  for (int j = 0; j < 8; ++j) yb[j] = s_yb[8 * half + j];
   const double inv_yn = s_inv;
-  // rerank table rows for coordinates 8sb..8sb+7 (one entry per thread): sign(n) L[n&7] q~_{8sb+j}
-  {
-    const int j = t >> 4, nb = t & 15;
+  // rerank table rows for coordinates 8sb..8sb+7 (two entries per thread): sign(n) L[n&7] q~_{8sb+j}
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int te = 2 * tl + i;
+    const int j = te >> 4, nb = te & 15;
     double yj = yb[0];
 #pragma unroll
     for (int jj = 1; jj < 8; ++jj) yj = (j == jj) ? yb[jj] : yj;
     const float qt = (float)(yj * inv_yn);
     const float L = cfg.levels[nb & 7];
-    rtab[(((int64_t)b * cfg.n_q + h) * D + 8 * sb) * 16 + t] = (nb & 8) ? L * qt : -L * qt;
+    rtab[(((int64_t)b * cfg.n_q + h) * D + 8 * sb) * 16 + te] = (nb & 8) ? L * qt : -L * qt;
   }
   phase_mark(K_QPREP, 2);
   // Complement symmetry: score(255 - c) == -score(c) exactly (every partial sum of the left-to-right fp64 sum
   // is negated, round-to-nearest is odd-symmetric and an exact zero is +0.0 either way). So the (score desc,
   // id asc) order of all 256 is: the 128 "leaders" (of each pair {c, 255-c} the one that comes first) in
   // order, then their complements in reverse order -> rank(255 - c) = 255 - rank(c). Only the leaders are
-  // sorted, one per thread. Thread t owns the pair {t, 255 - t}; t < 128 <= 255 - t breaks a zero tie.
-  KV e;
-  {
+  // sorted. Element i of thread tl is the pair {c, 255 - c}, c = 2*tl + i (c < 128 <= 255 - c breaks a zero tie).
+  KV e[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int c = 2 * tl + i;
     double acc = 0.0;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc = __dadd_rn(acc, ((t >> j) & 1) ? yb[j] : -yb[j]);
+    for (int j = 0; j < 8; ++j) acc = __dadd_rn(acc, ((c >> j) & 1) ? yb[j] : -yb[j]);
     const bool neg = acc < 0.0;
-    e.k = ~ord_f64(neg ? -acc : acc);  // ascending key == descending score; ties by ascending id
-    e.id = neg ? (uint32_t)(NC - 1 - t) : (uint32_t)t;
+    e[i].k = ~ord_f64(neg ? -acc : acc);  // ascending key == descending score; ties by ascending id
+    e[i].id = neg ? (uint32_t)(NC - 1 - c) : (uint32_t)c;
   }
   // Fast path: when the fp64 scores have 8 trailing zero mantissa bits (always, unless the query spans more than
   // ~27 binades: each y' is an exact sum of bf16 values and the 8-term score sums are exact too), the leader id
-  // fits in those bits and the sort moves one 64-bit composite (2 shuffles per stage instead of 3): ordering by
-  // composite == ordering by (key, id). Otherwise the (key, id) pair network below.
-  if (__syncthreads_and((e.k & 0xffull) == 0xffull)) {
-    unsigned long long c = (e.k & ~0xffull) | e.id;
+  // fits in those bits and the sort moves one 64-bit composite (2 shuffles per element and stage instead of 3):
+  // ordering by composite == ordering by (key, id). Otherwise the (key, id) pair network below.
+  if (__syncthreads_and(((e[0].k & 0xffull) == 0xffull) && ((e[1].k & 0xffull) == 0xffull))) {
+    unsigned long long c[2] = {(e[0].k & ~0xffull) | e[0].id, (e[1].k & ~0xffull) | e[1].id};
 #pragma unroll
     for (int k = 2; k <= NC / 2; k <<= 1) {
 #pragma unroll
       for (int j = k >> 1; j > 0; j >>= 1) {
-        unsigned long long o;
-        if (j < 32) {
-          o = __shfl_xor_sync(0xffffffffu, c, j);
+        if (j == 1) {  // positions 2tl, 2tl + 1: inside the thread
+          const bool asc = ((2 * tl) & k) == 0;
+          const unsigned long long lo = c[0] < c[1] ? c[0] : c[1], hi = c[0] < c[1] ? c[1] : c[0];
+          c[0] = asc ? lo : hi;
+          c[1] = asc ? hi : lo;
         } else {
-          sk[t] = c;
-          __syncthreads();
-          o = sk[t ^ j];
-          __syncthreads();
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int p = 2 * tl + i;
+            unsigned long long o;
+            if (j < 64) {
+              o = __shfl_xor_sync(0xffffffffu, c[i], j >> 1);
+            } else {
+              sk[half][p] = c[i];
+              __syncthreads();
+              o = sk[half][p ^ j];
+              __syncthreads();
+            }
+            const bool keep_min = (((p & j) == 0) == ((p & k) == 0));
+            c[i] = (keep_min == (o < c[i])) ? o : c[i];
+          }
         }
-        const bool keep_min = (((t & j) == 0) == ((t & k) == 0));
-        c = (keep_min == (o < c)) ? o : c;
       }
     }
-    e.id = (uint32_t)(c & 0xffull);
+    e[0].id = (uint32_t)(c[0] & 0xffull);
+    e[1].id = (uint32_t)(c[1] & 0xffull);
   } else {
 #pragma unroll
     for (int k = 2; k <= NC / 2; k <<= 1) {
 #pragma unroll
       for (int j = k >> 1; j > 0; j >>= 1) {
-        KV o;
-        if (j < 32) {
-          o = shfl_kv(e, j);
+        if (j == 1) {
+          const KV lo = e[0], hi = e[1];
+          KV a2 = lo, b2 = hi;
+          ce(a2, hi, 2 * tl, k, 1);
+          ce(b2, lo, 2 * tl + 1, k, 1);
+          e[0] = a2;
+          e[1] = b2;
         } else {
-          sk[t] = e.k;
-          si[t] = e.id;
-          __syncthreads();
-          o = KV{sk[t ^ j], si[t ^ j]};
-          __syncthreads();
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int p = 2 * tl + i;
+            KV o;
+            if (j < 64) {
+              o = shfl_kv(e[i], j >> 1);
+            } else {
+              sk[half][p] = e[i].k;
+              si[half][p] = e[i].id;
+              __syncthreads();
+              o = KV{sk[half][p ^ j], si[half][p ^ j]};
+              __syncthreads();
+            }
+            ce(e[i], o, p, k, j);
+          }
         }
-        ce(e, o, t, k, j);
       }
     }
   }
   phase_mark(K_QPREP, 3);
-  // position t == rank of leader e.id, 255 - t == rank of its complement; write this head's bonus byte of the
-  // packed LUT entry of both
+  // position p = 2*tl + i == rank of leader e[i].id, 255 - p == rank of its complement; write this head's bonus
+  // byte of the packed LUT entry of both
   const int chunk = max(1, T / cfg.n_tiers);
   uint8_t* lb = reinterpret_cast<uint8_t*>(lut + ((int64_t)b * cfg.n_kv + g) * NC * NB);
 #pragma unroll
-  for (int u = 0; u < 2; ++u) {
-    const int rank = u ? NC - 1 - t : t;
-    const uint32_t id = u ? NC - 1 - e.id : e.id;
-    int bonus = 0;
-    if (rank < T) bonus = cfg.tier_bonus[min(rank / chunk, cfg.n_tiers - 1)];
-    lb[((int64_t)id * NB + sb) * 4 + hh] = (uint8_t)bonus;
+  for (int i = 0; i < 2; ++i) {
+    const int p = 2 * tl + i;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int rank = u ? NC - 1 - p : p;
+      const uint32_t id = u ? NC - 1 - e[i].id : e[i].id;
+      int bonus = 0;
+      if (rank < T) bonus = cfg.tier_bonus[min(rank / chunk, cfg.n_tiers - 1)];
+      lb[((int64_t)id * NB + sb) * 4 + hh] = (uint8_t)bonus;
+    }
   }
   phase_mark(K_QPREP, 4);
 }
@@ -199,7 +238,7 @@ __global__ void __launch_bounds__(QP_THREADS) qprep_kernel(const uint16_t* q, in
 
 cudaError_t launch_qprep(const pkv_index* ix, const void* q, int T, float* dbg_q_rot, cudaStream_t stream) {
   const Workspace* ws = ix->ws;
-  dim3 grid(NB, ix->cfg.n_q_heads, ix->batch);
+  dim3 grid(NB / 2, ix->cfg.n_q_heads, ix->batch);
   ProfScope p_(K_QPREP, stream);
   return pdl_launch(qprep_kernel, grid, dim3(QP_THREADS), 0, stream, static_cast<const uint16_t*>(q), T, ix->dcfg,
                     ws->lut, ws->rtab, ws->qnorm, ws->qrot, dbg_q_rot, ws->ucount);
