@@ -343,6 +343,40 @@ def test_full_size_128k_sampled_head(pkv):
         assert np.all(np.abs(og - o) <= ATT_ABS + 2.0 ** -8 * np.abs(o))
 
 
+@pytest.mark.slow
+def test_300k_warp_histograms_and_rerank_tile_loop(pkv):
+    """n = 300,000 (Llama shape): the scan's warp segments exceed 512 keys, so the select takes its per-warp
+    offsets from the scan's per-warp histograms, and C = 15,000 candidates per head make the rerank loop over
+    tiles inside resident CTAs — the 1M code paths at a size the oracle checks in full for one KV head."""
+    n = 300000
+    K, q, V = make_problem(23, 1, 32, 8, n, device="cuda")
+    cfg = pkv.config_init(32, 8, SB)
+    ix = pkv.Index(cfg, 1, n)
+    pkv.encode_keys(ix, K)
+    idx, est, dbg = pkv.retrieve_topk(ix, q, 100, debug=True)
+    assert (dbg["T"], dbg["C"]) == (21, 15000)
+    out, lse = pkv.sparse_attend(ix, q, K, V, idx)
+    g = 2
+    Kf = bf16_f64(K[0, g])
+    meta = oracle_meta(Kf)
+    for hh in range(4):
+        h = 4 * g + hh
+        qf = bf16_f64(q[0, h])
+        r = oracle_retrieval(meta, qf, dbg["T"], dbg["C"], 100)
+        assert np.array_equal(dbg["scores"][0, h].cpu().numpy().astype(np.int64), r["score"])
+        cg = dbg["cand"][0, h].cpu().numpy()
+        assert np.array_equal(np.sort(cg), r["cand"])
+        eg = dict(zip(cg.tolist(), dbg["est"][0, h].cpu().numpy().tolist()))
+        egv = np.array([eg[int(i)] for i in r["cand"]])
+        tol = 1e-3 * np.maximum(np.abs(r["est"]), 1e-2 * meta["knorm"][r["cand"]] * r["qnorm"])
+        assert np.all(np.abs(egv - r["est"]) <= tol)
+        check_topk(idx[0, h].cpu().numpy(), est[0, h].cpu().numpy(), r["cand"], r["est"],
+                   dict(zip(range(n), meta["knorm"].tolist())), r["qnorm"], 100)
+        o, l = pipeline.attend(qf, Kf, bf16_f64(V[0, g]), idx[0, h].cpu().numpy())
+        og = out[0, h].float().cpu().numpy()
+        assert np.all(np.abs(og - o) <= ATT_ABS + 2.0 ** -8 * np.abs(o))
+
+
 def check_group_fused(pkv, K, q, V, Kh, Vh, idx, est, out, lse, b, g, T, C, k, dbg=None):
     """One (sequence, KV head) group of a fused retrieve_and_attend call against the oracle: retrieval of its
     query heads (AMB-15/16) and attention over hot rows U retrieved rows (AMB-17, GPU's own index set)."""
