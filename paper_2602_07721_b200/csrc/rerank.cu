@@ -337,6 +337,7 @@ __device__ void radix_topk(const Src& src, int count, int k, int32_t* out_idx, f
     __syncthreads();
     if (tid < 32) {
       // lane l covers digits 255-8l .. 248-8l (descending)
+      const unsigned int need = (unsigned int)need_s;  // read by every lane before the owner lane updates it
       unsigned int c[8], s = 0;
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
@@ -350,8 +351,8 @@ __device__ void radix_topk(const Src& src, int count, int k, int32_t* out_idx, f
         if (tid >= x) inc += o;
       }
       const unsigned int before = inc - s;
-      const unsigned int need = (unsigned int)need_s;
       const bool mine = before < need && inc >= need;
+      __syncwarp();  // all lanes have read need_s / prefix_s (independent thread scheduling)
       if (mine) {
         unsigned int cum = before;
         for (int e = 0; e < 8; ++e) {
