@@ -399,6 +399,10 @@ def run_ours(args):
                 roof["host_link_gbs"] = fl["uva_stream_read_gbs"]
                 roof["uva_row_gather_floor_us"] = fl["uva_gather_3200_rows_us"]
     scan_gbs = kern.get("scan", {}).get("gbs")
+    # the metric's second half: the collision scan's HBM rate against the 8 TB/s B200 figure the north star
+    # names, and against this box's measured copy bandwidth
+    scan_vs = None if scan_gbs is None else {"gbs": scan_gbs, "frac_of_8tbs": round(scan_gbs / 8000.0, 4),
+                                             "frac_of_measured_peak": round(scan_gbs / hbm_peak, 4)}
 
     # ---- CPU oracle baseline (rank 0, N = 1 only) ----
     cpu = None
@@ -422,6 +426,7 @@ def run_ours(args):
                        "cuda_graph": use_graph},
             "roofline": roof,
             "scan_gbs": scan_gbs,
+            "scan_hbm": scan_vs,
             "kernels": kern,
             "encode_us_per_layer": round(enc_ms_layer * 1000.0, 2),
             "encode_gbs": round(batch * N_KV * n_loc * 400 / (enc_ms_layer * 1e-3) / 1e9, 1),
