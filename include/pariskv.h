@@ -135,6 +135,9 @@ typedef struct {
   int32_t* dbg_cand;    /* [batch][n_q][n_cand] candidate ids (global), set semantics, -1 padded      */
   float* dbg_est;       /* [batch][n_q][n_cand] RSQ-IP estimate aligned with dbg_cand                  */
   float* dbg_q_rot;     /* [batch][n_q][D] rotated unit query q~ = R q/||q||               */
+  int64_t n_global;     /* sequence-sharded calls: the global retrieval length n_cand is checked against; */
+                        /* <= 0 takes the communicator's record (pkv_comm_init / pkv_comm_set_global_len). */
+                        /* Ignored by unsharded calls (the index length is used).                        */
 } pkv_retrieve_params;
 
 /* (3) retrieve_topk — per decode step. q: device bf16 [batch][n_q][D] contiguous.
@@ -247,6 +250,25 @@ pkv_status pkv_stream_state(const pkv_stream* s, int64_t* n_retrieval, int32_t* 
  * Errors: UNSUPPORTED if the capacity exceeds 256 chunks (2,097,152 keys), CUDA on allocation failure. */
 pkv_status pkv_index_set_postings(pkv_index* index, int32_t enable, cudaStream_t stream);
 
+/* Degenerate-key accounting (AMB-7; replaces the per-key API error of S:89): keys whose rotated
+ * subspace b has S_b = 0 get the deterministic encoding of e_1 in that subspace (id 0xFF, w_b = 0) and are
+ * counted on the device by the encoder. Counts cover the current index content (encode_keys resets them,
+ * append_decode_keys adds). pkv_index_get_stats enqueues a copy on `stream` and synchronises that stream. */
+typedef struct {
+  int64_t n_keys;                  /* keys per (sequence, KV head) in the retrieval zone (= pkv_index_len)   */
+  int64_t zero_keys;               /* keys (over all sequences and KV heads) that are entirely zero         */
+  int64_t keys_with_zero_subspace; /* keys with at least one subspace of S_b = 0 (includes zero_keys)       */
+  int64_t zero_subspaces;          /* total (key, subspace) pairs with S_b = 0                              */
+} pkv_index_stats;
+pkv_status pkv_index_get_stats(const pkv_index* index, pkv_index_stats* out, cudaStream_t stream);
+
+/* Test hook: when out_f32 != NULL every later attention call on this index (sparse_attend,
+ * retrieve_and_attend[_rows], the sharded paths — shard 0's pointer in the *_sharded_local emulation) also
+ * writes the fp32 attention output, before its bf16 rounding, to out_f32 (device [batch][n_q][D]). The
+ * caller keeps the buffer alive; NULL disables. Lets parity tests check the fp32 accumulation against the
+ * 2e-3 bar apart from the bf16 rounding of `out` (AMB-17). Host-only. */
+pkv_status pkv_index_set_debug_output(pkv_index* index, float* out_f32);
+
 /* Diagnostics: copy metadata of positions [start, start+count) into caller device buffers in the
  * canonical layout: ids uint8 [batch][n_kv][count][16] (subspace order), codes uint8
  * [batch][n_kv][count][64] (coordinate c -> byte c>>1, low nibble for even c; nibble = sign<<3 | idx),
@@ -264,9 +286,24 @@ pkv_status pkv_index_export(const pkv_index* index, int64_t start, int64_t count
  * ------------------------------------------------------------------------------------------------- */
 /* 128-byte NCCL unique id, to be broadcast from rank 0 to all ranks by the caller. */
 pkv_status pkv_nccl_unique_id(uint8_t out[128]);
-/* Attach a communicator to `index` (collective over `world` ranks; call on every rank). */
+/* Attach an NCCL communicator to `index` (collective over `world` ranks; call on every rank; also sums the
+ * ranks' current index lengths into the global length, one synchronous exchange). */
 pkv_status pkv_comm_init(pkv_index* index, const uint8_t id[128], int32_t rank, int32_t world,
                          int64_t shard_offset);
+/* Host-staged transport (for CPU process groups such as gloo, tests, and several ranks sharing one GPU, where
+ * NCCL cannot run): fn performs an all-gather in HOST memory — buf holds `world` slots of bytes_per_rank
+ * bytes, slot `rank` holds this rank's contribution on entry, and on return every slot must hold its rank's
+ * contribution; fn returns 0 on success (any other value -> PKV_ERR_NCCL). Each exchange then copies the
+ * rank's slot to pinned host memory, synchronises the stream, calls fn and copies all slots back: results
+ * are identical to the NCCL transport, but calls synchronise and are not graph-capturable. Collective over
+ * `world` ranks (every rank calls it); it also sums the ranks' current index lengths into the global length. */
+typedef int32_t (*pkv_host_allgather_fn)(void* ctx, void* buf, size_t bytes_per_rank, int32_t rank, int32_t world);
+pkv_status pkv_comm_init_host(pkv_index* index, pkv_host_allgather_fn fn, void* ctx, int32_t rank, int32_t world,
+                              int64_t shard_offset);
+/* Global retrieval length recorded by the communicator (validation of n_cand in sharded calls). pkv_comm_init
+ * and pkv_comm_init_host set it to the sum of the ranks' lengths at attach time; after appends on any rank the
+ * caller updates it here on every rank, or passes pkv_retrieve_params.n_global per call. */
+pkv_status pkv_comm_set_global_len(pkv_index* index, int64_t n_global);
 /* Attach `donor`'s communicator to `index` as well (e.g. one communicator for all layers of a model). The
  * two indices must then be used from the same stream order on every rank. */
 pkv_status pkv_comm_share(pkv_index* index, pkv_index* donor, int64_t shard_offset);

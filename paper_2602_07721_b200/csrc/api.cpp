@@ -111,8 +111,8 @@ pkv_status alloc_workspace(Workspace* ws, int batch, int n_q, int n_kv, int64_t 
       (size_t)std::max<size_t>(bk, 256) * 32 * GMAX * HB * 2,  // warp_hist (scan CTAs <= max(units, SMs))
       (size_t)MAX_RANKS * bq * MAX_SPLITS * PART * 4,    // part
       bk * 4,                                            // ticket
-      (size_t)MAX_RANKS * bq * MAX_TOPK * 4,             // seg_est
-      (size_t)MAX_RANKS * bq * MAX_TOPK * 4,             // seg_idx
+      (size_t)topk_segments(cap) * bq * MAX_TOPK * 4,    // seg_est
+      (size_t)topk_segments(cap) * bq * MAX_TOPK * 4,    // seg_idx
       bk * 4,                                            // ucount
       bk * (size_t)cap * 4,                              // uid
       bk * (size_t)cap * 16};                            // upos
@@ -145,6 +145,7 @@ pkv_status alloc_workspace(Workspace* ws, int batch, int n_q, int n_kv, int64_t 
   ws->ticket = reinterpret_cast<unsigned int*>(take(13));
   ws->seg_est = reinterpret_cast<float*>(take(14));
   ws->seg_idx = reinterpret_cast<int32_t*>(take(15));
+  ws->seg_slots = topk_segments(cap);
   ws->ucount = reinterpret_cast<unsigned int*>(take(16));
   ws->uid = reinterpret_cast<int32_t*>(take(17));
   ws->upos = reinterpret_cast<int32_t*>(take(18));
@@ -240,19 +241,6 @@ pkv_status run_encoder(pkv_index* ix, const void* K, int64_t sb, int64_t sh, int
   return PKV_OK;
 }
 
-pkv_status check_retrieve(const pkv_index* ix, const void* q, const pkv_retrieve_params* p, int64_t n_global,
-                          const int32_t* out_idx, const float* out_est) {
-  if (!ix || !q || !p || !out_idx || !out_est) return set_error(PKV_ERR_INVALID_ARG, "retrieve_topk: null pointer");
-  if (!aligned16(q)) return set_error(PKV_ERR_INVALID_ARG, "retrieve_topk: q must be 16-byte aligned");
-  if (p->probes_T < 1 || p->probes_T > PKV_CENTROIDS)
-    return set_error(PKV_ERR_INVALID_ARG, "retrieve_topk: probes_T out of [1,256]");
-  if (p->top_k < 1 || p->top_k > MAX_TOPK) return set_error(PKV_ERR_INVALID_ARG, "retrieve_topk: top_k out of [1,1024]");
-  if (n_global < 1) return set_error(PKV_ERR_INVALID_ARG, "retrieve_topk: empty retrieval zone");
-  if (p->n_cand < std::min<int64_t>(p->top_k, n_global) || p->n_cand > n_global)
-    return set_error(PKV_ERR_INVALID_ARG, "retrieve_topk: n_cand must be in [min(top_k, n), n]");
-  return PKV_OK;
-}
-
 // Sequence-sharded retrieve_and_attend with the fused T+A exchange: H all-gather, local
 // candidates and top-k, then ONE all-gather of (est, id, logit, v row) + hot partial per head, and a replicated
 // merge + attention. Two collectives per layer instead of three.
@@ -260,10 +248,13 @@ pkv_status retrieve_and_attend_sharded(pkv_index* ix, const void* q, const pkv_r
                                        const void* V, int64_t sb, int64_t sh, int64_t st, const void* K_hot,
                                        const void* V_hot, int32_t n_hot, float scale, int32_t* out_idx,
                                        float* out_est, void* out, float* lse, cudaStream_t stream) {
-  const int64_t n_global = comm_global_n(ix);
+  if (!p) return set_error(PKV_ERR_INVALID_ARG, "retrieve_and_attend: null params");
+  const int64_t n_global = comm_global_n(ix, p);
+  if (n_global < 0) return set_error(PKV_ERR_INVALID_ARG, "retrieve_and_attend: global retrieval length unknown");
   pkv_status st0 = check_retrieve(ix, q, p, n_global, out_idx, out_est);
   if (st0 != PKV_OK) return st0;
-  if (n_hot < 0 || (n_hot > 0 && (!K_hot || !V_hot))) return set_error(PKV_ERR_INVALID_ARG, "bad hot rows");
+  if (n_hot < 0 || (n_hot > 0 && (!K_hot || !V_hot || !aligned16(K_hot) || !aligned16(V_hot))))
+    return set_error(PKV_ERR_INVALID_ARG, "retrieve_and_attend: bad hot rows");
   st0 = check_kv_layout(K, sb, sh, st, "retrieve_and_attend(K)");
   if (st0 == PKV_OK) st0 = check_kv_layout(V, sb, sh, st, "retrieve_and_attend(V)");
   if (st0 != PKV_OK) return st0;
@@ -293,6 +284,33 @@ pkv_status retrieve_and_attend_sharded(pkv_index* ix, const void* q, const pkv_r
 }
 
 }  // namespace
+
+pkv_status check_retrieve(const pkv_index* ix, const void* q, const pkv_retrieve_params* p, int64_t n_global,
+                          const int32_t* out_idx, const float* out_est) {
+  if (!ix || !q || !p || !out_idx || !out_est) return set_error(PKV_ERR_INVALID_ARG, "retrieve_topk: null pointer");
+  if (!aligned16(q)) return set_error(PKV_ERR_INVALID_ARG, "retrieve_topk: q must be 16-byte aligned");
+  if (p->probes_T < 1 || p->probes_T > PKV_CENTROIDS)
+    return set_error(PKV_ERR_INVALID_ARG, "retrieve_topk: probes_T out of [1,256]");
+  if (p->top_k < 1 || p->top_k > MAX_TOPK) return set_error(PKV_ERR_INVALID_ARG, "retrieve_topk: top_k out of [1,1024]");
+  if (n_global < 1) return set_error(PKV_ERR_INVALID_ARG, "retrieve_topk: empty retrieval zone");
+  if (p->n_cand < std::min<int64_t>(p->top_k, n_global) || p->n_cand > n_global)
+    return set_error(PKV_ERR_INVALID_ARG, "retrieve_topk: n_cand must be in [min(top_k, n), n]");
+  return PKV_OK;
+}
+
+pkv_status attend_hot_only(pkv_index* ix, const void* q, const void* K_hot, const void* V_hot, int n_hot,
+                           int hot_rows, int top_k, float scale, int32_t* out_idx, float* out_est, void* out,
+                           float* lse, cudaStream_t stream) {
+  if (n_hot < 1 || hot_rows < n_hot || !K_hot || !V_hot || !aligned16(K_hot) || !aligned16(V_hot) || !aligned16(q))
+    return set_error(PKV_ERR_INVALID_ARG, "attend_hot_only: bad hot rows");
+  const int64_t bq = (int64_t)ix->batch * ix->cfg.n_q_heads;
+  PKV_CUDA(launch_fill_empty_topk(out_idx, out_est, bq * top_k, stream), "fill");
+  AttendArgs a{q, nullptr, nullptr, 0, 0, 0, nullptr, 0, K_hot, V_hot, n_hot, scale, 0, 0, 0, hot_rows};
+  PKV_CUDA(launch_attend_partial(ix, a, plan_attend_splits(ix, n_hot), ix->ws->part, ix->ws->ticket, out, lse, stream),
+           "attend");
+  return PKV_OK;
+}
+
 }  // namespace pkv
 
 using namespace pkv;
@@ -331,7 +349,11 @@ pkv_status pkv_index_create(const pkv_config* cfg, int32_t batch, int64_t capaci
   const size_t units = (size_t)batch * cfg->n_kv_heads;
   cudaError_t e = cudaMalloc(&ix->ids, units * capacity * NB);
   if (e == cudaSuccess) e = cudaMalloc(&ix->rec, units * capacity * ix->dcfg.rec_bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&ix->stats, 4 * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(ix->stats, 0, 4 * sizeof(unsigned long long));
   if (e != cudaSuccess) {
+    cudaFree(ix->stats);
+    cudaFree(ix->rec);
     cudaFree(ix->ids);
     delete ix;
     return cuda_status(e, "index cudaMalloc");
@@ -350,6 +372,7 @@ pkv_status pkv_index_create(const pkv_config* cfg, int32_t batch, int64_t capaci
     release_workspace(ix->ws);
     cudaFree(ix->ids);
     cudaFree(ix->rec);
+    cudaFree(ix->stats);
     delete ix;
     return st;
   }
@@ -367,7 +390,27 @@ pkv_status pkv_index_destroy(pkv_index* ix) {
   cudaFree(ix->post_off);
   cudaFree(ix->post_key);
   cudaFree(ix->enc_fb);
+  cudaFree(ix->stats);
   delete ix;
+  return PKV_OK;
+}
+
+pkv_status pkv_index_get_stats(const pkv_index* ix, pkv_index_stats* out, cudaStream_t stream) {
+  if (!ix || !out) return set_error(PKV_ERR_INVALID_ARG, "pkv_index_get_stats: null pointer");
+  DeviceGuard g(ix->device);
+  unsigned long long h[4] = {0, 0, 0, 0};
+  PKV_CUDA(cudaMemcpyAsync(h, ix->stats, sizeof(h), cudaMemcpyDeviceToHost, stream), "stats copy");
+  PKV_CUDA(cudaStreamSynchronize(stream), "stats sync");
+  out->n_keys = ix->n;
+  out->zero_keys = (int64_t)h[0];
+  out->keys_with_zero_subspace = (int64_t)h[1];
+  out->zero_subspaces = (int64_t)h[2];
+  return PKV_OK;
+}
+
+pkv_status pkv_index_set_debug_output(pkv_index* ix, float* out_f32) {
+  if (!ix) return set_error(PKV_ERR_INVALID_ARG, "pkv_index_set_debug_output: null index");
+  ix->dbg_out_f32 = out_f32;
   return PKV_OK;
 }
 
@@ -426,6 +469,7 @@ pkv_status encode_keys(pkv_index* ix, const void* K, int64_t sb, int64_t sh, int
     if (s != PKV_OK) return s;
   }
   DeviceGuard g(ix->device);
+  PKV_CUDA(cudaMemsetAsync(ix->stats, 0, 4 * sizeof(unsigned long long), stream), "stats reset");
   if (n > 0) {
     pkv_status se = run_encoder(ix, K, sb, sh, st, 0, n, stream);
     if (se != PKV_OK) return se;
@@ -469,8 +513,9 @@ pkv_status pkv_index_export(const pkv_index* ix, int64_t start, int64_t count, u
 pkv_status retrieve_topk(pkv_index* ix, const void* q, const pkv_retrieve_params* p, int32_t* out_idx, float* out_est,
                          cudaStream_t stream) {
   if (!ix) return set_error(PKV_ERR_INVALID_ARG, "retrieve_topk: null index");
-  const int64_t n_global = ix->comm ? comm_global_n(ix) : ix->n;
-  if (n_global < 0) return set_error(PKV_ERR_NCCL, "retrieve_topk: global length exchange failed");
+  if (!p) return set_error(PKV_ERR_INVALID_ARG, "retrieve_topk: null params");
+  const int64_t n_global = ix->comm ? comm_global_n(ix, p) : ix->n;
+  if (n_global < 0) return set_error(PKV_ERR_INVALID_ARG, "retrieve_topk: global retrieval length unknown");
   pkv_status st = check_retrieve(ix, q, p, n_global, out_idx, out_est);
   if (st != PKV_OK) return st;
   DeviceGuard g(ix->device);
@@ -526,7 +571,7 @@ pkv_status sparse_attend(pkv_index* ix, const void* q, const void* K, const void
   const bool last = !ix->comm || ix->rank == ix->world - 1;
   AttendArgs a{q, K, V, sb, sh, st, idx, k, K_hot, V_hot, last ? n_hot : 0, scale,
                ix->comm ? ix->shard_offset : 0, ix->comm ? ix->shard_offset + ix->n : INT64_MAX,
-               ix->comm ? ix->shard_offset : 0};
+               ix->comm ? ix->shard_offset : 0, n_hot};
   Workspace* ws = ix->ws;
   const size_t part_slot = (size_t)ix->batch * ix->cfg.n_q_heads * MAX_SPLITS * PART;
   const int slot = ix->comm ? ix->rank : 0;
@@ -572,6 +617,8 @@ pkv_status retrieve_and_attend_rows(pkv_index* ix, const void* q, const pkv_retr
   if (st0 != PKV_OK) return st0;
   if (n_hot < 0 || (n_hot > 0 && (!K_hot || !V_hot || !aligned16(K_hot) || !aligned16(V_hot))))
     return set_error(PKV_ERR_INVALID_ARG, "retrieve_and_attend: bad hot rows");
+  if (n_hot > 0 && hot_rows < n_hot)
+    return set_error(PKV_ERR_INVALID_ARG, "retrieve_and_attend_rows: hot_rows must be >= n_hot");
   if (n_hot > 16 * 64) return set_error(PKV_ERR_UNSUPPORTED, "retrieve_and_attend: n_hot must be <= 1024");
   DeviceGuard g(ix->device);
   ScanPlan plan;
@@ -598,6 +645,25 @@ pkv_status retrieve_and_attend_rows(pkv_index* ix, const void* q, const pkv_retr
 }
 
 // ---------------------------------------------------------------- single-process sharded emulation
+namespace {
+// The emulation sets each shard's offset for the duration of one call; restored on every return path so a
+// later unsharded call on the same index returns local ids again.
+struct OffsetScope {
+  pkv_index* const* shards;
+  int P;
+  int64_t saved[MAX_RANKS];
+  OffsetScope(pkv_index* const* s, const int64_t* offsets, int p) : shards(s), P(p) {
+    for (int r = 0; r < P; ++r) {
+      saved[r] = shards[r]->shard_offset;
+      shards[r]->shard_offset = offsets[r];
+    }
+  }
+  ~OffsetScope() {
+    for (int r = 0; r < P; ++r) shards[r]->shard_offset = saved[r];
+  }
+};
+}  // namespace
+
 pkv_status pkv_retrieve_topk_sharded_local(pkv_index* const* shards, const int64_t* offsets, int32_t P, const void* q,
                                            const pkv_retrieve_params* p, int32_t* out_idx, float* out_est,
                                            cudaStream_t stream) {
@@ -618,8 +684,8 @@ pkv_status pkv_retrieve_topk_sharded_local(pkv_index* const* shards, const int64
   const size_t hist_slot = (size_t)shards[0]->batch * shards[0]->cfg.n_q_heads * HB;
   const size_t topk_slot = (size_t)shards[0]->batch * shards[0]->cfg.n_q_heads * MAX_TOPK;
   ScanPlan plans[MAX_RANKS];
+  OffsetScope scope(shards, offsets, P);
   for (int r = 0; r < P; ++r) {
-    shards[r]->shard_offset = offsets[r];
     pkv_retrieve_params pr = *p;
     pr.dbg_scores = nullptr;
     pr.dbg_cand = nullptr;
@@ -639,7 +705,6 @@ pkv_status pkv_retrieve_topk_sharded_local(pkv_index* const* shards, const int64
   PKV_CUDA(launch_topk_merge(shards[0], P, p->top_k, w0->topk_est, w0->topk_idx, 2 * topk_slot, out_idx, out_est,
                              stream),
            "merge");
-  for (int r = 0; r < P; ++r) shards[r]->shard_offset = 0;
   return PKV_OK;
 }
 
@@ -652,6 +717,10 @@ pkv_status pkv_sparse_attend_sharded_local(pkv_index* const* shards, const int64
     return set_error(PKV_ERR_INVALID_ARG, "attend_sharded_local: bad arguments");
   if (k < 0 || n_hot < 0 || k > MAX_TOPK || (k == 0 && n_hot == 0))
     return set_error(PKV_ERR_INVALID_ARG, "attend_sharded_local: bad k / n_hot");
+  if (n_hot > 0 && (!K_hot || !V_hot || !aligned16(K_hot) || !aligned16(V_hot)))
+    return set_error(PKV_ERR_INVALID_ARG, "attend_sharded_local: bad hot rows");
+  if (k > 0 && !idx) return set_error(PKV_ERR_INVALID_ARG, "attend_sharded_local: null idx");
+  if (!aligned16(q)) return set_error(PKV_ERR_INVALID_ARG, "attend_sharded_local: q must be 16-byte aligned");
   for (int r = 1; r < P; ++r)
     if (!shards[r] || shards[r]->ws == shards[0]->ws || shards[r]->device != shards[0]->device)
       return set_error(PKV_ERR_INVALID_ARG, "attend_sharded_local: shards need their own workspace");
@@ -667,7 +736,7 @@ pkv_status pkv_sparse_attend_sharded_local(pkv_index* const* shards, const int64
       if (s1 != PKV_OK) return s1;
     }
     AttendArgs a{q, Ks[r], Vs[r], sb, sh, st, idx, k, K_hot, V_hot, r == P - 1 ? n_hot : 0, scale, offsets[r],
-                 offsets[r] + shards[r]->n, offsets[r]};
+                 offsets[r] + shards[r]->n, offsets[r], n_hot};
     PKV_CUDA(launch_attend_partial(shards[r], a, splits, w0->part + r * part_slot, nullptr, nullptr, nullptr, stream),
              "attend");
   }
@@ -684,7 +753,8 @@ pkv_status pkv_retrieve_and_attend_sharded_local(pkv_index* const* shards, const
   if (!shards || !offsets || !Ks || !Vs || P < 1 || P > MAX_RANKS || !q || !p || !out)
     return set_error(PKV_ERR_INVALID_ARG, "retrieve_and_attend_sharded_local: bad arguments");
   if (p->top_k > TA_MAXK) return set_error(PKV_ERR_UNSUPPORTED, "retrieve_and_attend_sharded_local: top_k > 256");
-  if (n_hot < 0 || (n_hot > 0 && (!K_hot || !V_hot))) return set_error(PKV_ERR_INVALID_ARG, "bad hot rows");
+  if (n_hot < 0 || (n_hot > 0 && (!K_hot || !V_hot || !aligned16(K_hot) || !aligned16(V_hot))))
+    return set_error(PKV_ERR_INVALID_ARG, "retrieve_and_attend_sharded_local: bad hot rows");
   int64_t n_global = 0;
   for (int r = 0; r < P; ++r) {
     if (!shards[r] || shards[r]->device != shards[0]->device || shards[r]->batch != shards[0]->batch ||
@@ -710,8 +780,8 @@ pkv_status pkv_retrieve_and_attend_sharded_local(pkv_index* const* shards, const
   pr.dbg_cand = nullptr;
   pr.dbg_est = nullptr;
   pr.dbg_q_rot = nullptr;
+  OffsetScope scope(shards, offsets, P);
   for (int r = 0; r < P; ++r) {
-    shards[r]->shard_offset = offsets[r];
     st0 = phase_scan(shards[r], q, &pr, plans[r], stream);
     if (st0 != PKV_OK) return st0;
     PKV_CUDA(launch_head_hist(shards[r], plans[r], w0->head_hist + r * hist_slot, stream), "head hist");
@@ -726,7 +796,6 @@ pkv_status pkv_retrieve_and_attend_sharded_local(pkv_index* const* shards, const
              "exchange pack");
   }
   PKV_CUDA(launch_ta_merge(shards[0], w0->ta_msg, P, pr.top_k, out_idx, out_est, out, lse, stream), "exchange merge");
-  for (int r = 0; r < P; ++r) shards[r]->shard_offset = 0;
   return PKV_OK;
 }
 
@@ -737,6 +806,19 @@ pkv_status pkv_comm_init(pkv_index* ix, const uint8_t id[128], int32_t rank, int
     return set_error(PKV_ERR_INVALID_ARG, "pkv_comm_init: bad arguments (world must be in [1, 8])");
   DeviceGuard g(ix->device);
   return comm_init(ix, id, rank, world, shard_offset);
+}
+
+pkv_status pkv_comm_init_host(pkv_index* ix, pkv_host_allgather_fn fn, void* ctx, int32_t rank, int32_t world,
+                              int64_t shard_offset) {
+  if (!ix || !fn || world < 1 || world > MAX_RANKS || rank < 0 || rank >= world || shard_offset < 0)
+    return set_error(PKV_ERR_INVALID_ARG, "pkv_comm_init_host: bad arguments (world must be in [1, 8])");
+  DeviceGuard g(ix->device);
+  return comm_init_host(ix, fn, ctx, rank, world, shard_offset);
+}
+
+pkv_status pkv_comm_set_global_len(pkv_index* ix, int64_t n_global) {
+  if (!ix || n_global < 0) return set_error(PKV_ERR_INVALID_ARG, "pkv_comm_set_global_len: bad arguments");
+  return comm_set_global_len(ix, n_global);
 }
 
 pkv_status pkv_comm_share(pkv_index* ix, pkv_index* donor, int64_t shard_offset) {

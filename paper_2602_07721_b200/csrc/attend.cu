@@ -9,6 +9,8 @@
 //                        fetched 4 items at a time (8 x 8-byte loads in flight per lane) to cover UVA latency.
 //                        Emits one partial (m, l, o[128]) per (query head, split).
 // attend_combine_kernel  LSE merge of the partials (all splits, all ranks when sharded) -> bf16 out, natural lse.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace pkv {
@@ -36,7 +38,7 @@ static_assert(AT_BATCH * GMAX == 32, "transpose-reduction maps one (row, head) p
 __global__ void __launch_bounds__(AT_WARPS * 32) attend_partial_kernel(AttendArgs a, int n_q, int n_kv, int G,
                                                                        int items_per_split, float* part,
                                                                        unsigned int* ticket, void* out,
-                                                                       float* lse) {
+                                                                       float* lse, float* out_f32) {
   phase_mark(K_ATTEND, 0);
   __shared__ __align__(16) float sm_x[AT_WARPS][AT_BATCH * GMAX];
   __shared__ float sm_m[AT_WARPS][GMAX], sm_l[AT_WARPS][GMAX];
@@ -71,8 +73,8 @@ __global__ void __launch_bounds__(AT_WARPS * 32) attend_partial_kernel(AttendArg
   const int i1 = min(n_items, i0 + items_per_split);
   const uint16_t* Kb = static_cast<const uint16_t*>(a.K);
   const uint16_t* Vb = static_cast<const uint16_t*>(a.V);
-  const uint16_t* Kh = static_cast<const uint16_t*>(a.K_hot) + ((int64_t)b * n_kv + g) * a.n_hot * D;
-  const uint16_t* Vh = static_cast<const uint16_t*>(a.V_hot) + ((int64_t)b * n_kv + g) * a.n_hot * D;
+  const uint16_t* Kh = static_cast<const uint16_t*>(a.K_hot) + ((int64_t)b * n_kv + g) * a.hot_rows * D;
+  const uint16_t* Vh = static_cast<const uint16_t*>(a.V_hot) + ((int64_t)b * n_kv + g) * a.hot_rows * D;
   bool waited = false;
   for (int base = i0 + warp * AT_BATCH; base < i1; base += AT_WARPS * AT_BATCH) {
     uint2 kr[AT_BATCH], vr[AT_BATCH];
@@ -253,14 +255,17 @@ __global__ void __launch_bounds__(AT_WARPS * 32) attend_partial_kernel(AttendArg
     for (int s = 0; s < nsplits; ++s) O += sm_w[hh][s] * __ldcg(base + (int64_t)s * PART + 2 + d);
     const float L = sm_L[hh];
     const int64_t bhq = (int64_t)b * n_q + g * G + hh;
-    static_cast<__nv_bfloat16*>(out)[bhq * D + d] = __float2bfloat16_rn(L > 0.f ? O / L : 0.f);
+    const float o = L > 0.f ? O / L : 0.f;
+    static_cast<__nv_bfloat16*>(out)[bhq * D + d] = __float2bfloat16_rn(o);
+    if (out_f32) out_f32[bhq * D + d] = o;
     if (lse && d == 0) lse[bhq] = L > 0.f ? (sm_M[hh] + log2f(L)) * 0.6931471805599453f : -INFINITY;
   }
   if (threadIdx.x == 0) ticket[b * n_kv + g] = 0u;  // re-arm for the next launch / graph replay
 }
 
 __global__ void __launch_bounds__(D) attend_combine_kernel(const float* parts, int nsplits, int P,
-                                                            int64_t rank_stride, int n_q, void* out, float* lse) {
+                                                            int64_t rank_stride, int n_q, void* out, float* lse,
+                                                            float* out_f32) {
   const int h = blockIdx.x, b = blockIdx.y, d = threadIdx.x;
   const int64_t bhq = (int64_t)b * n_q + h;
   float M = -INFINITY;
@@ -281,10 +286,26 @@ __global__ void __launch_bounds__(D) attend_combine_kernel(const float* parts, i
   }
   const float o = L > 0.f ? O / L : 0.f;
   static_cast<__nv_bfloat16*>(out)[bhq * D + d] = __float2bfloat16_rn(o);
+  if (out_f32) out_f32[bhq * D + d] = o;
   if (lse && d == 0) lse[bhq] = L > 0.f ? (M + log2f(L)) * 0.6931471805599453f : -INFINITY;
 }
 
+__global__ void fill_empty_topk_kernel(int32_t* idx, float* est, int64_t count) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    idx[i] = -1;
+    est[i] = -INFINITY;
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_fill_empty_topk(int32_t* out_idx, float* out_est, int64_t count, cudaStream_t stream) {
+  if (count <= 0) return cudaSuccess;
+  ProfScope p_(K_DEBUG, stream);
+  fill_empty_topk_kernel<<<(unsigned)std::min<int64_t>(64, (count + 255) / 256), 256, 0, stream>>>(out_idx, out_est,
+                                                                                                  count);
+  return cudaGetLastError();
+}
 
 int plan_attend_splits(const pkv_index* ix, int total_items) {
   // one round of AT_BATCH rows per warp: every row load of a CTA is in flight at once
@@ -303,7 +324,7 @@ cudaError_t launch_attend_partial(const pkv_index* ix, const AttendArgs& a, int 
   dim3 grid(splits, ix->cfg.n_kv_heads, ix->batch);
   ProfScope p_(K_ATTEND, stream);
   return pdl_launch(attend_partial_kernel, grid, dim3(AT_WARPS * 32), 0, stream, a, ix->cfg.n_q_heads,
-                    ix->cfg.n_kv_heads, G, per > 0 ? per : 1, part_out, ticket, out, lse);
+                    ix->cfg.n_kv_heads, G, per > 0 ? per : 1, part_out, ticket, out, lse, ix->dbg_out_f32);
 }
 
 cudaError_t launch_attend_combine(const pkv_index* ix, const float* parts, int nsplits, int P, void* out, float* lse,
@@ -311,7 +332,8 @@ cudaError_t launch_attend_combine(const pkv_index* ix, const float* parts, int n
   dim3 grid(ix->cfg.n_q_heads, ix->batch);
   const int64_t rank_stride = (int64_t)ix->batch * ix->cfg.n_q_heads * MAX_SPLITS * PART;
   ProfScope p_(K_COMBINE, stream);
-  attend_combine_kernel<<<grid, D, 0, stream>>>(parts, nsplits, P, rank_stride, ix->cfg.n_q_heads, out, lse);
+  attend_combine_kernel<<<grid, D, 0, stream>>>(parts, nsplits, P, rank_stride, ix->cfg.n_q_heads, out, lse,
+                                                ix->dbg_out_f32);
   return cudaGetLastError();
 }
 

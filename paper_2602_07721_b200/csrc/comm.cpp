@@ -1,6 +1,12 @@
-// NCCL plumbing for the sequence-sharded retrieval. Three in-place all-gathers per
-// layer and decode step, all on the caller's stream: (H) per-head score histograms, (T) local top-k lists,
-// (A) partial softmax states. The unique id is produced here and broadcast by the caller (torch.distributed).
+// Exchange plumbing for the sequence-sharded retrieval. Per layer and decode step the library
+// all-gathers (H) per-head score histograms and then either (T) local top-k lists and (A) partial softmax
+// states, or the fused T+A message — all in place in one device buffer on the caller's stream.
+// Two transports:
+//   NCCL  (pkv_comm_init): ncclAllGather over NVLink; stream-ordered and CUDA-graph capturable. The unique id
+//         is produced here and broadcast by the caller (torch.distributed).
+//   host  (pkv_comm_init_host): the caller's host all-gather (e.g. a gloo process group): the rank's slot is
+//         copied to pinned host memory, the stream synchronised, the callback run, and all slots copied back.
+//         Synchronous, not capturable — for CPU process groups, tests, and ranks that share one GPU.
 #include <nccl.h>
 
 #include <cstring>
@@ -13,6 +19,12 @@ namespace pkv {
 
 struct Comm {
   ncclComm_t comm = nullptr;
+  pkv_host_allgather_fn host_fn = nullptr;
+  void* host_ctx = nullptr;
+  void* stage = nullptr;  // pinned host staging buffer of the host transport
+  size_t stage_bytes = 0;
+  int rank = 0, world = 1;
+  int64_t global_n = -1;
   int refs = 1;
 };
 
@@ -31,20 +43,91 @@ pkv_status comm_unique_id(uint8_t out[128]) {
   return PKV_OK;
 }
 
+static pkv_status raw_allgather(Comm* c, void* buf, size_t bytes, cudaStream_t stream) {
+  if (c->comm)
+    return nccl_status(ncclAllGather(static_cast<char*>(buf) + c->rank * bytes, buf, bytes, ncclChar, c->comm, stream),
+                       "ncclAllGather");
+  const size_t total = bytes * c->world;
+  if (c->stage_bytes < total) {
+    if (c->stage) cudaFreeHost(c->stage);
+    c->stage = nullptr;
+    c->stage_bytes = 0;
+    if (cudaMallocHost(&c->stage, total) != cudaSuccess) return set_error(PKV_ERR_CUDA, "host exchange staging");
+    c->stage_bytes = total;
+  }
+  char* h = static_cast<char*>(c->stage);
+  cudaError_t e = cudaMemcpyAsync(h + c->rank * bytes, static_cast<char*>(buf) + c->rank * bytes, bytes,
+                                  cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  if (e != cudaSuccess) return cuda_status(e, "host exchange (device to host)");
+  if (c->host_fn(c->host_ctx, h, bytes, c->rank, c->world) != 0)
+    return set_error(PKV_ERR_NCCL, "host all-gather callback failed");
+  e = cudaMemcpyAsync(buf, h, total, cudaMemcpyHostToDevice, stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);  // the staging buffer is reused by the next exchange
+  return cuda_status(e, "host exchange (host to device)");
+}
+
+// Global length at attach time: all-gather of every rank's local length (one synchronous exchange).
+static pkv_status reduce_global_n(Comm* c, int64_t local_n) {
+  int64_t* d = nullptr;
+  cudaStream_t s = nullptr;
+  cudaError_t e = cudaMalloc(&d, sizeof(int64_t) * c->world);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d + c->rank, &local_n, sizeof(int64_t), cudaMemcpyHostToDevice, s);
+  pkv_status st = cuda_status(e, "global length exchange");
+  if (st == PKV_OK) st = raw_allgather(c, d, sizeof(int64_t), s);
+  int64_t h[MAX_RANKS] = {};
+  if (st == PKV_OK) {
+    e = cudaMemcpyAsync(h, d, sizeof(int64_t) * c->world, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    st = cuda_status(e, "global length exchange");
+  }
+  if (st == PKV_OK) {
+    c->global_n = 0;
+    for (int r = 0; r < c->world; ++r) c->global_n += h[r];
+  }
+  if (s) cudaStreamDestroy(s);
+  cudaFree(d);
+  return st;
+}
+
+static void attach(pkv_index* ix, Comm* c, int64_t shard_offset) {
+  comm_destroy(ix->comm);
+  ix->comm = c;
+  ix->rank = c->rank;
+  ix->world = c->world;
+  ix->shard_offset = shard_offset;
+}
+
 pkv_status comm_init(pkv_index* ix, const uint8_t id_bytes[128], int rank, int world, int64_t shard_offset) {
   ncclUniqueId id;
   std::memcpy(&id, id_bytes, 128);
   Comm* c = new Comm();
+  c->rank = rank;
+  c->world = world;
   pkv_status s = nccl_status(ncclCommInitRank(&c->comm, world, id, rank), "ncclCommInitRank");
+  if (s == PKV_OK) s = reduce_global_n(c, ix->n);
   if (s != PKV_OK) {
-    delete c;
+    comm_destroy(c);
     return s;
   }
-  comm_destroy(ix->comm);
-  ix->comm = c;
-  ix->rank = rank;
-  ix->world = world;
-  ix->shard_offset = shard_offset;
+  attach(ix, c, shard_offset);
+  return PKV_OK;
+}
+
+pkv_status comm_init_host(pkv_index* ix, pkv_host_allgather_fn fn, void* ctx, int rank, int world,
+                          int64_t shard_offset) {
+  Comm* c = new Comm();
+  c->host_fn = fn;
+  c->host_ctx = ctx;
+  c->rank = rank;
+  c->world = world;
+  pkv_status s = reduce_global_n(c, ix->n);
+  if (s != PKV_OK) {
+    comm_destroy(c);
+    return s;
+  }
+  attach(ix, c, shard_offset);
   return PKV_OK;
 }
 
@@ -52,6 +135,7 @@ void comm_destroy(Comm* c) {
   if (!c) return;
   if (--c->refs > 0) return;
   if (c->comm) ncclCommDestroy(c->comm);
+  if (c->stage) cudaFreeHost(c->stage);
   delete c;
 }
 
@@ -71,13 +155,18 @@ pkv_status comm_share(pkv_index* ix, pkv_index* donor, int64_t shard_offset) {
 }
 
 pkv_status comm_allgather_u32(pkv_index* ix, uint32_t* buf, size_t slot, cudaStream_t stream) {
-  return nccl_status(ncclAllGather(buf + ix->rank * slot, buf, slot, ncclUint32, ix->comm->comm, stream),
-                     "ncclAllGather");
+  return raw_allgather(ix->comm, buf, slot * sizeof(uint32_t), stream);
 }
 
-int64_t comm_global_n(const pkv_index* ix) {
-  (void)ix;
-  return INT64_MAX;
+int64_t comm_global_n(const pkv_index* ix, const pkv_retrieve_params* p) {
+  if (p && p->n_global > 0) return p->n_global;
+  return ix->comm ? ix->comm->global_n : ix->n;
+}
+
+pkv_status comm_set_global_len(pkv_index* ix, int64_t n_global) {
+  if (!ix->comm) return set_error(PKV_ERR_INVALID_ARG, "pkv_comm_set_global_len: index has no communicator");
+  ix->comm->global_n = n_global;
+  return PKV_OK;
 }
 
 }  // namespace pkv

@@ -54,7 +54,7 @@ __device__ __forceinline__ void fwht128(T v[8], int lane16) {
 __device__ __forceinline__ void encode_one(const uint16_t* __restrict__ K, int64_t sb, int64_t sh, int64_t st,
                                            int64_t t0, int n_kv, int64_t cap, const DevCfg& cfg,
                                            uint8_t* __restrict__ ids, uint8_t* __restrict__ rec, float* sL,
-                                           int bh, int64_t tt, bool live, bool stage) {
+                                           unsigned long long* stats, int bh, int64_t tt, bool live, bool stage) {
   const int lane16 = threadIdx.x & 15;
   const int b = bh / n_kv, h = bh - b * n_kv;
   const int64_t t = t0 + tt;
@@ -120,6 +120,15 @@ __device__ __forceinline__ void encode_one(const uint16_t* __restrict__ K, int64
   uint32_t id = 0, code = 0;
   float dot = 0.f, vn2 = 0.f;
   const bool degenerate = (S == 0.0);
+  // AMB-7 / SURVEY §8(b): zero subspaces and zero keys are encoded deterministically and counted, not rejected.
+  // stats[0] zero keys, [1] keys with at least one zero subspace, [2] zero subspaces (rare: one atomic per key).
+  const unsigned zmask = __ballot_sync(0xffffffffu, degenerate && live) >> (threadIdx.x & 16);
+  if (lane16 == 0 && (zmask & 0xffffu)) {
+    const unsigned z = zmask & 0xffffu;
+    if (z == 0xffffu) atomicAdd(stats + 0, 1ull);
+    atomicAdd(stats + 1, 1ull);
+    atomicAdd(stats + 2, (unsigned long long)__popc(z));
+  }
   // weights in fp32 on y scaled by 2^(119 - emax): |y| < 128 * 2^(emax - 126) so |y * scale| < 1 (ratios only)
   const double scale = __longlong_as_double((long long)(1023 + 119 - emax) << 52);
   const double unscale = __longlong_as_double((long long)(1023 - 119 + emax) << 52);
@@ -195,12 +204,12 @@ __device__ __forceinline__ void encode_one(const uint16_t* __restrict__ K, int64
 __global__ void __launch_bounds__(256, 4) encode_kernel(const uint16_t* __restrict__ K, int64_t sb, int64_t sh,
                                                         int64_t st, int64_t t0, int64_t count, int n_kv,
                                                         int64_t cap, DevCfg cfg, uint8_t* __restrict__ ids,
-                                                        uint8_t* __restrict__ rec) {
+                                                        uint8_t* __restrict__ rec, unsigned long long* stats) {
   __shared__ float sL[8];  // magnitude levels: per-lane indexed (a divergent constant-bank read would serialise)
   int64_t tt = (int64_t)blockIdx.x * KEYS_PER_BLOCK + (threadIdx.x >> 4);
   const bool live = tt < count;
   if (!live) tt = count - 1;  // keep the half-warp shuffles full; results discarded
-  encode_one(K, sb, sh, st, t0, n_kv, cap, cfg, ids, rec, sL, blockIdx.y, tt, live, true);
+  encode_one(K, sb, sh, st, t0, n_kv, cap, cfg, ids, rec, sL, stats, blockIdx.y, tt, live, true);
 }
 
 // The keys list[0 .. *list_n) (entry = bh * count + tt, written by the tensor-core encoder for keys outside its
@@ -208,15 +217,15 @@ __global__ void __launch_bounds__(256, 4) encode_kernel(const uint16_t* __restri
 __global__ void __launch_bounds__(256) encode_list_kernel(const uint16_t* __restrict__ K, int64_t sb, int64_t sh,
                                                           int64_t st, int64_t t0, int64_t count, int n_kv,
                                                           int64_t cap, DevCfg cfg, uint8_t* __restrict__ ids,
-                                                          uint8_t* __restrict__ rec, const int32_t* list,
-                                                          const int32_t* list_n) {
+                                                          uint8_t* __restrict__ rec, unsigned long long* stats,
+                                                          const int32_t* list, const int32_t* list_n) {
   __shared__ float sL[8];
   if (threadIdx.x < 8) sL[threadIdx.x] = cfg.levels[threadIdx.x];
   __syncthreads();
   const int n = *list_n;
   for (int kk = blockIdx.x * KEYS_PER_BLOCK + (threadIdx.x >> 4); kk < n; kk += gridDim.x * KEYS_PER_BLOCK) {
     const int e = list[kk];
-    encode_one(K, sb, sh, st, t0, n_kv, cap, cfg, ids, rec, sL, (int)(e / count), e % count, true, false);
+    encode_one(K, sb, sh, st, t0, n_kv, cap, cfg, ids, rec, sL, stats, (int)(e / count), e % count, true, false);
   }
 }
 
@@ -252,8 +261,8 @@ cudaError_t launch_encode_list(const pkv_index* ix, const void* K, int64_t sb, i
                                int64_t count, const int32_t* list, const int32_t* list_n, cudaStream_t stream) {
   ProfScope p_(K_ENCODE, stream);
   encode_list_kernel<<<ix->num_sms * 2, 256, 0, stream>>>(static_cast<const uint16_t*>(K), sb, sh, st, t0, count,
-                                                     ix->cfg.n_kv_heads, ix->cap, ix->dcfg, ix->ids, ix->rec, list,
-                                                     list_n);
+                                                     ix->cfg.n_kv_heads, ix->cap, ix->dcfg, ix->ids, ix->rec,
+                                                     ix->stats, list, list_n);
   return cudaGetLastError();
 }
 
@@ -263,7 +272,7 @@ cudaError_t launch_encode(const pkv_index* ix, const void* K, int64_t sb, int64_
   const dim3 grid((unsigned)((count + KEYS_PER_BLOCK - 1) / KEYS_PER_BLOCK), ix->batch * ix->cfg.n_kv_heads);
   ProfScope p_(K_ENCODE, stream);
   encode_kernel<<<grid, 256, 0, stream>>>(static_cast<const uint16_t*>(K), sb, sh, st, t0, count,
-                                          ix->cfg.n_kv_heads, ix->cap, ix->dcfg, ix->ids, ix->rec);
+                                          ix->cfg.n_kv_heads, ix->cap, ix->dcfg, ix->ids, ix->rec, ix->stats);
   return cudaGetLastError();
 }
 

@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(TC_KEYS, 1) encode_tc_kernel(const uint16_t* _
         bad |= e != 0 && e < emax - 16;
       }
     }
-    const bool fast = live && !bad;
+    bool fast = live && !bad;  // cleared below for keys with a zero subspace (counted by the half-warp encoder)
 #pragma unroll
     for (int c = 0; c < 16; ++c) {
       uint32_t dg[3][4];
@@ -259,6 +259,7 @@ __global__ void __launch_bounds__(TC_KEYS, 1) encode_tc_kernel(const uint16_t* _
           nib[j] = ((pos ? 1u : 0u) << 3) | (uint32_t)idx;
         }
         const bool degenerate = (S == 0.f);  // all eight y are exactly zero (integers)
+        fast &= !degenerate;                 // AMB-7 keys go to the half-warp encoder, which counts them
         if (!certain && !degenerate) {        // exact fp64 sequence of the oracle for this subspace
           double yd[8], sqd[8];
 #pragma unroll

@@ -55,8 +55,9 @@ struct Workspace {
   float* topk_est = nullptr;      //   its estimates at topk_est + 2r*slot (= ids + slot); slot = batch*n_q*MAX_TOPK
   float* part = nullptr;          // [MAX_RANKS][batch][n_q][MAX_SPLITS][PART] (exchange A)
   unsigned int* ticket = nullptr; // [batch][n_kv] split-completion counters of the fused attention merge
-  float* seg_est = nullptr;       // [MAX_RANKS][batch][n_q][MAX_TOPK] segmented top-k of long candidate lists
+  float* seg_est = nullptr;       // [seg_slots][batch][n_q][MAX_TOPK] segmented top-k of long candidate lists
   int32_t* seg_idx = nullptr;
+  int seg_slots = 1;              // = topk_segments(cap): segment lists a head's candidate list can need
   // GQA-union rerank: per (sequence, KV head) the keys that are a candidate of at least one of
   // its query heads, each with its candidate position in every head's list (-1: not a candidate of that head)
   unsigned int* ucount = nullptr; // [batch][n_kv] union sizes (zeroed by qprep, counted by select)
@@ -70,6 +71,7 @@ struct Workspace {
 };
 
 constexpr int MAX_RANKS = 8;
+constexpr int SEG_SLOTS = 64;  // most segments of one candidate list in the segmented top-k (rerank.cu)
 
 struct Comm;  // comm.cpp
 
@@ -86,6 +88,8 @@ struct pkv_index {
   uint8_t* rec = nullptr;   // [batch][n_kv][cap][rec_bytes]: 64 B nibbles + 16 x fp32 w' (or 16 x fp16 w')
   // inverted lists (pkv_index_set_postings): per (b, kv, chunk of POST_CHUNK keys, subspace)
   // bucket offsets u16 [257] and the chunk's key offsets u16 [POST_CHUNK] sorted by centroid id
+  float* dbg_out_f32 = nullptr;         // optional fp32 copy of every attention output (pkv_index_set_debug_output)
+  unsigned long long* stats = nullptr;  // device [4]: zero keys, keys with a zero subspace, zero subspaces, spare
   int32_t* enc_fb = nullptr;  // [batch*n_kv*cap + 1]: tensor-core encoder fallback list, count at the end
   bool postings = false;
   uint16_t* post_off = nullptr;
@@ -119,6 +123,14 @@ cudaError_t set_phase_rerank(unsigned long long* p);
 cudaError_t set_phase_qprep(unsigned long long* p);
 cudaError_t set_phase_attend(unsigned long long* p);
 cudaError_t set_phase_encode(unsigned long long* p);
+
+// Shared validation / hot-row-only attention (api.cpp), used by the streaming manager (stream.cpp)
+pkv_status check_retrieve(const pkv_index* ix, const void* q, const pkv_retrieve_params* p, int64_t n_global,
+                          const int32_t* out_idx, const float* out_est);
+// Attention over the hot rows alone (empty retrieval zone): out_idx/out_est [batch][n_q][top_k] get -1 / -inf.
+pkv_status attend_hot_only(pkv_index* ix, const void* q, const void* K_hot, const void* V_hot, int n_hot,
+                           int hot_rows, int top_k, float scale, int32_t* out_idx, float* out_est, void* out,
+                           float* lse, cudaStream_t stream);
 
 // Error plumbing (api.cpp)
 pkv_status set_error(pkv_status s, const std::string& msg);
@@ -215,11 +227,14 @@ struct AttendArgs {
   float scale;
   int64_t own_lo, own_hi;  // global ids owned by this shard
   int64_t id_offset;       // local row = id - id_offset
+  int hot_rows;            // row capacity of a (sequence, KV head) block of the hot rows (>= n_hot)
 };
 int plan_attend_splits(const pkv_index* ix, int total_rows);
 // ticket != nullptr: the last CTA of each (sequence, KV head) also does the LSE merge into out/lse.
 cudaError_t launch_attend_partial(const pkv_index* ix, const AttendArgs& a, int splits, float* part_out,
                                   unsigned int* ticket, void* out, float* lse, cudaStream_t stream);
+// out_idx = -1, out_est = -inf for `count` entries (retrieval over an empty zone)
+cudaError_t launch_fill_empty_topk(int32_t* out_idx, float* out_est, int64_t count, cudaStream_t stream);
 cudaError_t launch_attend_combine(const pkv_index* ix, const float* parts, int nsplits, int P, void* out,
                                   float* lse, cudaStream_t stream);
 

@@ -599,17 +599,18 @@ struct AttendEpi {  // gather + attention over the selected rows and the hot row
   void* out;
   float* lse;
   int G;
+  float* out_f32;         // optional fp32 copy of out (pkv_index_set_debug_output), may be null
 };
 
 // Grid (n_q, batch, nseg). nseg == 1: the whole candidate list of a head, output at out_idx + bhq*out_stride.
-// nseg > 1 (very long lists, e.g. 1M-token contexts): CTA z takes candidates [z*BS_CACHE, (z+1)*BS_CACHE) and
+// nseg > 1 (very long lists, e.g. 1M-token contexts): CTA z takes candidates [z*seg_len, (z+1)*seg_len) and
 // writes its local top-k to slot z of out (slot stride seg_stride), to be merged by merge_kernel.
 template <bool ATTEND, bool SELECT = true>
 __global__ void __launch_bounds__(BS_THREADS) topk_kernel(const float* est, const int32_t* cand,
                                                            const int32_t* sel, int n_q,
                                                            int64_t cand_stride, int k, int out_stride,
                                                            int32_t* out_idx, float* out_est, AttendEpi ep,
-                                                           int64_t seg_stride) {
+                                                           int64_t seg_stride, int seg_len) {
   phase_mark(K_TOPK, 0);
   pdl_trigger();
   pdl_wait();
@@ -618,8 +619,8 @@ __global__ void __launch_bounds__(BS_THREADS) topk_kernel(const float* est, cons
     const int h = blockIdx.x, b = blockIdx.y, z = blockIdx.z;
     const int64_t bhq = (int64_t)b * n_q + h;
     const int total = sel[bhq * SEL_STRIDE + 2];
-    const int begin = gridDim.z > 1 ? z * BS_CACHE : 0;
-    const int count = gridDim.z > 1 ? max(0, min(BS_CACHE, total - begin)) : total;
+    const int begin = gridDim.z > 1 ? min(total, z * seg_len) : 0;
+    const int count = gridDim.z > 1 ? max(0, min(seg_len, total - begin)) : total;
     topk_select(est + bhq * cand_stride + begin, cand + bhq * cand_stride + begin, count, k,
                 out_idx + z * seg_stride + bhq * out_stride, out_est + z * seg_stride + bhq * out_stride);
   }
@@ -725,7 +726,9 @@ __global__ void __launch_bounds__(BS_THREADS) topk_kernel(const float* est, cons
           O += cw * sm_o[w * D + d];
         }
       }
-      static_cast<__nv_bfloat16*>(ep.out)[bhq * D + d] = __float2bfloat16_rn(L > 0.f ? O / L : 0.f);
+      const float o = L > 0.f ? O / L : 0.f;
+      static_cast<__nv_bfloat16*>(ep.out)[bhq * D + d] = __float2bfloat16_rn(o);
+      if (ep.out_f32) ep.out_f32[bhq * D + d] = o;
       if (ep.lse && d == 0) ep.lse[bhq] = L > 0.f ? (M + log2f(L)) * 0.6931471805599453f : -INFINITY;
     }
 
@@ -1207,7 +1210,9 @@ __global__ void __launch_bounds__(BS_THREADS) topk_cl_kernel(const float* est, c
           O = fmaf(c, cpart[pr][2 + d], O);
         }
       }
-      static_cast<__nv_bfloat16*>(ep.out)[bhq * D + d] = __float2bfloat16_rn(L > 0.f ? O / L : 0.f);
+      const float o = L > 0.f ? O / L : 0.f;
+      static_cast<__nv_bfloat16*>(ep.out)[bhq * D + d] = __float2bfloat16_rn(o);
+      if (ep.out_f32) ep.out_f32[bhq * D + d] = o;
       if (ep.lse && d == 0) ep.lse[bhq] = L > 0.f ? (M + log2f(L)) * 0.6931471805599453f : -INFINITY;
     }
   }
@@ -1333,7 +1338,8 @@ __global__ void __launch_bounds__(256) ta_pack_kernel(const int32_t* lidx, const
 // merge_kernel) and attend the selected entries' (x, v) plus the P hot partials.
 __global__ void __launch_bounds__(TK_THREADS) ta_merge_kernel(const uint32_t* msg, int P, int64_t rank_stride,
                                                               int64_t SW, int n_q, int k, int32_t* out_idx,
-                                                              float* out_est, void* out, float* lse) {
+                                                              float* out_est, void* out, float* lse,
+                                                              float* out_f32) {
   constexpr int NW = TK_THREADS / 32;
   __shared__ float sm_o[NW][D], sm_ml[NW][2];
   __shared__ unsigned long long s_kth;
@@ -1399,7 +1405,9 @@ __global__ void __launch_bounds__(TK_THREADS) ta_merge_kernel(const uint32_t* ms
         O = fmaf(c, hp[2 + d], O);
       }
     }
-    static_cast<__nv_bfloat16*>(out)[bhq * D + d] = __float2bfloat16_rn(L > 0.f ? O / L : 0.f);
+    const float o = L > 0.f ? O / L : 0.f;
+    static_cast<__nv_bfloat16*>(out)[bhq * D + d] = __float2bfloat16_rn(o);
+    if (out_f32) out_f32[bhq * D + d] = o;
     if (lse && d == 0) lse[bhq] = L > 0.f ? (M + log2f(L)) * 0.6931471805599453f : -INFINITY;
   }
 }
@@ -1444,8 +1452,11 @@ static size_t topk_cluster_smem(int slice, int k) {
   return need > lists ? need : lists;
 }
 
+// Segments of a list too long for one cluster: ceil(C/BS_CACHE) (each cached in smem), at most SEG_SLOTS; beyond
+// that the segments grow and topk_select streams them from global memory (radix path).
 int topk_segments(int64_t C_cap) {
-  return C_cap > (int64_t)CL_MAX * CL_SLICE ? (int)((C_cap + BS_CACHE - 1) / BS_CACHE) : 1;
+  if (C_cap <= (int64_t)CL_MAX * CL_SLICE) return 1;
+  return (int)std::min<int64_t>(SEG_SLOTS, (C_cap + BS_CACHE - 1) / BS_CACHE);
 }
 
 cudaError_t init_rerank_attrs() {
@@ -1533,8 +1544,8 @@ cudaError_t launch_rerank(const pkv_index* ix, int64_t C_cap, int64_t id_offset,
 
 cudaError_t launch_topk(const pkv_index* ix, int64_t C_cap, int k, int32_t* out_idx, float* out_est,
                         int out_stride, cudaStream_t stream) {
-  (void)C_cap;
   const Workspace* ws = ix->ws;
+  C_cap = std::min<int64_t>(C_cap, ws->cap);  // a head's list never exceeds the workspace capacity (sharded: global C)
   dim3 grid(ix->cfg.n_q_heads, ix->batch);
   ProfScope p_(K_TOPK, stream);
   AttendEpi ep{};
@@ -1546,18 +1557,20 @@ cudaError_t launch_topk(const pkv_index* ix, int64_t C_cap, int k, int32_t* out_
                               (const int32_t*)ws->sel, ix->cfg.n_q_heads, ws->cap, k, out_stride, out_idx, out_est,
                               ep, slice);
   const int nseg = topk_segments(C_cap);
-  if (nseg > 1) {  // long candidate lists: per-segment top-k into the exchange slots, then the merge kernel
+  if (nseg > 1) {  // long candidate lists: per-segment top-k into the segment slots, then the merge kernel
+    if (nseg > ws->seg_slots) return cudaErrorInvalidValue;  // the workspace holds seg_slots lists per head
     const size_t slot = (size_t)ix->batch * ix->cfg.n_q_heads * MAX_TOPK;
+    const int seg_len = (int)((C_cap + nseg - 1) / nseg);
     dim3 g3(ix->cfg.n_q_heads, ix->batch, nseg);
     cudaError_t e = pdl_launch(topk_kernel<false>, g3, dim3(BS_THREADS), TK_SMEM, stream, (const float*)ws->est,
                                (const int32_t*)ws->cand, (const int32_t*)ws->sel, ix->cfg.n_q_heads, ws->cap, k,
-                               MAX_TOPK, ws->seg_idx, ws->seg_est, ep, (int64_t)slot);
+                               MAX_TOPK, ws->seg_idx, ws->seg_est, ep, (int64_t)slot, seg_len);
     if (e != cudaSuccess) return e;
     return launch_topk_merge_strided(ix, nseg, k, ws->seg_est, ws->seg_idx, out_idx, out_est, out_stride, stream);
   }
   return pdl_launch(topk_kernel<false>, grid, dim3(BS_THREADS), TK_SMEM, stream, (const float*)ws->est,
                     (const int32_t*)ws->cand, (const int32_t*)ws->sel, ix->cfg.n_q_heads, ws->cap, k, out_stride,
-                    out_idx, out_est, ep, (int64_t)0);
+                    out_idx, out_est, ep, (int64_t)0, 0);
 }
 
 cudaError_t launch_topk_attend(const pkv_index* ix, int64_t C_cap, int k, int32_t* out_idx, float* out_est, const void* q,
@@ -1567,7 +1580,7 @@ cudaError_t launch_topk_attend(const pkv_index* ix, int64_t C_cap, int k, int32_
   const Workspace* ws = ix->ws;
   dim3 grid(ix->cfg.n_q_heads, ix->batch);
   ProfScope p_(K_TOPK, stream);
-  AttendEpi ep{q, K, V, sb, sh, st, scale, K_hot, V_hot, n_hot, hot_rows, out, lse, ix->dcfg.G};
+  AttendEpi ep{q, K, V, sb, sh, st, scale, K_hot, V_hot, n_hot, hot_rows, out, lse, ix->dcfg.G, ix->dbg_out_f32};
   int slice = 0;
   const int R = topk_cluster(ix, C_cap, &slice);
   if (R > 0)
@@ -1577,7 +1590,7 @@ cudaError_t launch_topk_attend(const pkv_index* ix, int64_t C_cap, int k, int32_
                               slice);
   return pdl_launch(topk_kernel<true>, grid, dim3(BS_THREADS), TK_SMEM, stream, (const float*)ws->est,
                     (const int32_t*)ws->cand, (const int32_t*)ws->sel, ix->cfg.n_q_heads, ws->cap, k, k, out_idx,
-                    out_est, ep, (int64_t)0);
+                    out_est, ep, (int64_t)0, 0);
 }
 
 cudaError_t launch_topk_merge(const pkv_index* ix, int P, int k, const float* all_est, const int32_t* all_idx,
@@ -1596,10 +1609,10 @@ cudaError_t launch_topk_attend_rows(const pkv_index* ix, int k, const int32_t* i
   const Workspace* ws = ix->ws;
   dim3 grid(ix->cfg.n_q_heads, ix->batch);
   ProfScope p_(K_ATTEND, stream);
-  AttendEpi ep{q, K, V, sb, sh, st, scale, K_hot, V_hot, n_hot, hot_rows, out, lse, ix->dcfg.G};
+  AttendEpi ep{q, K, V, sb, sh, st, scale, K_hot, V_hot, n_hot, hot_rows, out, lse, ix->dcfg.G, ix->dbg_out_f32};
   return pdl_launch(topk_kernel<true, false>, grid, dim3(BS_THREADS), TK_SMEM, stream, (const float*)ws->est,
                     (const int32_t*)ws->cand, (const int32_t*)ws->sel, ix->cfg.n_q_heads, ws->cap, k, k,
-                    const_cast<int32_t*>(idx), (float*)nullptr, ep, (int64_t)0);
+                    const_cast<int32_t*>(idx), (float*)nullptr, ep, (int64_t)0, 0);
 }
 
 cudaError_t launch_topk_merge_strided(const pkv_index* ix, int P, int k, const float* all_est, const int32_t* all_idx,
@@ -1631,7 +1644,8 @@ cudaError_t launch_ta_merge(const pkv_index* ix, const uint32_t* msg, int P, int
   ProfScope p_(K_MERGE, stream);
   const int64_t SW = ta_slot_words(k);
   return pdl_launch(ta_merge_kernel, grid, dim3(TK_THREADS), TK_SMEM, stream, msg, P,
-                    (int64_t)ix->batch * ix->cfg.n_q_heads * SW, SW, ix->cfg.n_q_heads, k, out_idx, out_est, out, lse);
+                    (int64_t)ix->batch * ix->cfg.n_q_heads * SW, SW, ix->cfg.n_q_heads, k, out_idx, out_est, out, lse,
+                    ix->dbg_out_f32);
 }
 
 cudaError_t launch_dbg_cand(const pkv_index* ix, int64_t C, int32_t* dbg_cand, float* dbg_est, cudaStream_t stream) {

@@ -165,8 +165,13 @@ pkv_status pkv_stream_prefill(pkv_stream* s, const void* K, const void* V, int64
 pkv_status pkv_stream_decode(pkv_stream* s, const void* q, const void* k_new, const void* v_new,
                              const pkv_retrieve_params* params, float scale, int32_t* out_idx, float* out_est,
                              void* out, float* lse, cudaStream_t stream) {
-  if (!s || !q || !k_new || !v_new || !params) return set_error(PKV_ERR_INVALID_ARG, "pkv_stream_decode: null pointer");
+  // Every argument is validated, for the state this step will produce, before anything is enqueued or changed:
+  // a failing call leaves the regions and the index as they were (header contract).
+  if (!s || !q || !k_new || !v_new || !params || !out_idx || !out_est || !out)
+    return set_error(PKV_ERR_INVALID_ARG, "pkv_stream_decode: null pointer");
   if (!s->prefilled) return set_error(PKV_ERR_INVALID_ARG, "pkv_stream_decode: prefill first");
+  if (params->top_k < 1 || params->top_k > MAX_TOPK)
+    return set_error(PKV_ERR_INVALID_ARG, "pkv_stream_decode: top_k out of [1,1024]");
   pkv_index* ix = s->ix;
   const int sink = s->cfg.sink, L = s->cfg.local_size, U = s->cfg.update_size;
   const int batch = ix->batch, n_kv = ix->cfg.n_kv_heads;
@@ -174,6 +179,25 @@ pkv_status pkv_stream_decode(pkv_stream* s, const void* q, const void* k_new, co
   const int evict = flush ? std::max(0, s->n_local + U - L) : 0;
   if (flush && ix->n + evict > ix->cap)
     return set_error(PKV_ERR_CAPACITY, "pkv_stream_decode: flush would exceed the index capacity");
+  const int64_t n_after = ix->n + evict;                                   // retrieval zone after this step
+  const int keep = flush ? s->n_local + s->n_buf + 1 - evict : s->n_local;  // Local after this step
+  const int buf_after = flush ? 0 : s->n_buf + 1;
+  const int n_hot = sink + keep + buf_after;
+  pkv_retrieve_params p = *params;
+  if (n_after > 0 && (p.probes_T <= 0 || p.n_cand <= 0)) {  // schedule for the post-flush retrieval length
+    int32_t T = 0;
+    int64_t C = 0;
+    pkv_status r = pkv_schedule(n_after, p.top_k, &T, &C);
+    if (r != PKV_OK) return r;
+    if (p.probes_T <= 0) p.probes_T = T;
+    if (p.n_cand <= 0) p.n_cand = C;
+  }
+  if (n_after > 0) {
+    pkv_status r = check_retrieve(ix, q, &p, n_after, out_idx, out_est);
+    if (r != PKV_OK) return r;
+  } else if (n_hot < 1 || (reinterpret_cast<uintptr_t>(q) & 15u)) {
+    return set_error(PKV_ERR_INVALID_ARG, "pkv_stream_decode: nothing to attend / misaligned q");
+  }
   Guard g(ix->device);
   const int64_t hb = (int64_t)n_kv * s->rows * D;  // elements per sequence in the hot buffer
   const int64_t row = sink + s->n_local + s->n_buf;
@@ -198,7 +222,6 @@ pkv_status pkv_stream_decode(pkv_stream* s, const void* q, const void* k_new, co
                       n_kv, stream);
     }
     // (3) the newest local_size rows become Local (ii)
-    const int keep = s->n_local + s->n_buf - evict;
     if (e == cudaSuccess && evict > 0 && keep > 0) {
       for (uint16_t* H : {s->Kh, s->Vh}) {
         const uint16_t* src = H + (int64_t)(sink + evict) * D;
@@ -217,17 +240,10 @@ pkv_status pkv_stream_decode(pkv_stream* s, const void* q, const void* k_new, co
     s->n_local = keep;
     s->n_buf = 0;
   }
-  // (4) retrieval over the updated index + attention over Sink U Local U Update and the retrieved rows
-  pkv_retrieve_params p = *params;
-  if (p.probes_T <= 0 || p.n_cand <= 0) {
-    int32_t T = 0;
-    int64_t C = 0;
-    pkv_status r = pkv_schedule(ix->n, p.top_k, &T, &C);
-    if (r != PKV_OK) return r;
-    if (p.probes_T <= 0) p.probes_T = T;
-    if (p.n_cand <= 0) p.n_cand = C;
-  }
-  const int n_hot = sink + s->n_local + s->n_buf;
+  // (4) retrieval over the updated index + attention over Sink U Local U Update and the retrieved rows; a still
+  // empty retrieval zone (prompt <= sink + local_size, no eviction yet) attends the hot rows alone
+  if (n_after == 0)
+    return attend_hot_only(ix, q, s->Kh, s->Vh, n_hot, s->rows, p.top_k, scale, out_idx, out_est, out, lse, stream);
   return retrieve_and_attend_rows(ix, q, &p, s->Ks, s->Vs, (int64_t)n_kv * ix->cap * D, ix->cap * D, D, s->Kh, s->Vh,
                                   n_hot, s->rows, scale, out_idx, out_est, out, lse, stream);
 }

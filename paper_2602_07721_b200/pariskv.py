@@ -42,7 +42,17 @@ class StreamConfig(ctypes.Structure):
 class RetrieveParams(ctypes.Structure):
     _fields_ = [("probes_T", ctypes.c_int32), ("n_cand", ctypes.c_int64), ("top_k", ctypes.c_int32),
                 ("dbg_scores", ctypes.c_void_p), ("dbg_cand", ctypes.c_void_p), ("dbg_est", ctypes.c_void_p),
-                ("dbg_q_rot", ctypes.c_void_p)]
+                ("dbg_q_rot", ctypes.c_void_p), ("n_global", ctypes.c_int64)]
+
+
+class IndexStats(ctypes.Structure):
+    _fields_ = [("n_keys", ctypes.c_int64), ("zero_keys", ctypes.c_int64),
+                ("keys_with_zero_subspace", ctypes.c_int64), ("zero_subspaces", ctypes.c_int64)]
+
+
+# int32 fn(void* ctx, void* host_buf, size_t bytes_per_rank, int32 rank, int32 world)
+HostAllgatherFn = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int32,
+                                   ctypes.c_int32)
 
 
 _vp, _i32, _i64, _f32 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_float
@@ -69,6 +79,10 @@ _sigs = {
     "pkv_stream_state": [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i32), ctypes.POINTER(_i32),
                          ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp)],
     "pkv_index_export": [_vp, _i64, _i64, _vp, _vp, _vp, _vp],
+    "pkv_index_get_stats": [_vp, ctypes.POINTER(IndexStats), _vp],
+    "pkv_index_set_debug_output": [_vp, _vp],
+    "pkv_comm_init_host": [_vp, HostAllgatherFn, _vp, _i32, _i32, _i64],
+    "pkv_comm_set_global_len": [_vp, _i64],
     "pkv_nccl_unique_id": [_vp],
     "pkv_comm_init": [_vp, _vp, _i32, _i32, _i64],
     "pkv_comm_share": [_vp, _vp, _i64],
@@ -184,6 +198,20 @@ class Index:
         """Inverted-list collision variant: same results, buckets of probed centroids only."""
         _check(_lib.pkv_index_set_postings(self.handle, int(enable), _stream(stream)))
 
+    def stats(self, stream=None) -> dict:
+        """Degenerate-key counters of the current content (AMB-7; synchronises the stream)."""
+        s = IndexStats()
+        _check(_lib.pkv_index_get_stats(self.handle, ctypes.byref(s), _stream(stream)))
+        return {f: int(getattr(s, f)) for f, _ in IndexStats._fields_}
+
+    def set_debug_output(self, out_f32: torch.Tensor | None):
+        """fp32 copy [batch, n_q, 128] of every later attention output on this index (None disables)."""
+        if out_f32 is not None:
+            assert out_f32.dtype == torch.float32 and out_f32.is_contiguous()
+            assert tuple(out_f32.shape) == (self.batch, self.n_q, D)
+        self._dbg_out = out_f32  # kept alive while the library holds the pointer
+        _check(_lib.pkv_index_set_debug_output(self.handle, _ptr(out_f32)))
+
     def share_workspace(self, donor: "Index"):
         _check(_lib.pkv_index_share_workspace(self.handle, donor.handle))
 
@@ -232,7 +260,7 @@ def retrieve_topk(index: Index, q: torch.Tensor, top_k: int, probes_T: int | Non
         out_idx = torch.empty(index.batch, index.n_q, top_k, dtype=torch.int32, device=dev)
     if out_est is None:
         out_est = torch.empty(index.batch, index.n_q, top_k, dtype=torch.float32, device=dev)
-    p = RetrieveParams(T, C, top_k, None, None, None, None)
+    p = RetrieveParams(T, C, top_k, None, None, None, None, 0 if n_global is None else n_global)
     dbg = None
     if debug:
         nl = len(index)
@@ -278,12 +306,12 @@ def sparse_attend(index: Index, q: torch.Tensor, K: torch.Tensor | None, V: torc
 def retrieve_and_attend(index: Index, q: torch.Tensor, K, V, top_k: int, K_hot=None, V_hot=None,
                         scale: float | None = None, probes_T: int | None = None, n_cand: int | None = None,
                         out_idx=None, out_est=None, out=None, lse=None, strides=None, K_ptr=None, V_ptr=None,
-                        stream=None):
+                        n_global: int | None = None, stream=None):
     """(3)+(4) in one call: retrieval and attention of one decode step and layer, with the hot-row attention
     overlapped with the retrieval and the final top-k fused with the gather/attention. Returns
     (idx, est, out, lse)."""
     assert q.dtype == torch.bfloat16 and q.is_contiguous() and q.shape[-1] == D
-    n = len(index)
+    n = len(index) if n_global is None else n_global
     T0, C0 = schedule(n, top_k)
     T = T0 if probes_T is None else probes_T
     C = C0 if n_cand is None else n_cand
@@ -303,7 +331,7 @@ def retrieve_and_attend(index: Index, q: torch.Tensor, K, V, top_k: int, K_hot=N
         sb, sh, st = strides
     n_hot = 0 if K_hot is None else K_hot.shape[2]
     scale = 1.0 / np.sqrt(D) if scale is None else scale
-    p = RetrieveParams(T, C, top_k, None, None, None, None)
+    p = RetrieveParams(T, C, top_k, None, None, None, None, 0 if n_global is None else n_global)
     _check(_lib.retrieve_and_attend(index.handle, _ptr(q), ctypes.byref(p), _vp(K_ptr), _vp(V_ptr), sb, sh, st,
                                     _ptr(K_hot), _ptr(V_hot), n_hot, scale, _ptr(out_idx), _ptr(out_est), _ptr(out),
                                     _ptr(lse), _stream(stream)))
@@ -407,6 +435,27 @@ def nccl_unique_id() -> bytes:
 def comm_init(index: Index, uid: bytes, rank: int, world: int, shard_offset: int):
     buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
     _check(_lib.pkv_comm_init(index.handle, buf, rank, world, shard_offset))
+
+
+def comm_init_host(index: Index, allgather, rank: int, world: int, shard_offset: int):
+    """Attach the host-staged transport: allgather(buf: numpy uint8 [world, bytes_per_rank]) must fill every row
+    with that rank's bytes in place (row `rank` holds this rank's on entry), e.g. a gloo all_gather."""
+    def _fn(ctx, buf, nbytes, r, w):
+        try:
+            arr = np.ctypeslib.as_array(ctypes.cast(buf, ctypes.POINTER(ctypes.c_uint8)), shape=(w * nbytes,))
+            allgather(arr.reshape(w, nbytes))
+            return 0
+        except Exception:  # noqa: BLE001 — reported to the library as a failed exchange
+            import traceback
+            traceback.print_exc()
+            return 1
+    cb = HostAllgatherFn(_fn)
+    index._allgather_cb = cb  # the library keeps the pointer: keep the trampoline alive with the index
+    _check(_lib.pkv_comm_init_host(index.handle, cb, None, rank, world, shard_offset))
+
+
+def comm_set_global_len(index: Index, n_global: int):
+    _check(_lib.pkv_comm_set_global_len(index.handle, n_global))
 
 
 def comm_share(index: Index, donor: Index, shard_offset: int):

@@ -84,3 +84,20 @@ def oracle_retrieval(meta, q_f64, T, C, k):
     qt, qn = rerank.rotated_unit_query(q_f64, SB)
     est = rerank.estimate(meta, cand, qt, qn)
     return dict(score=score, cand=cand, est=est, qt=qt, qnorm=qn)
+
+
+ATT_F32 = 2e-3  # the north-star 2e-3 absolute, applied to the fp32 output alone (before the bf16 rounding of out)
+
+
+def check_attention(out_bf16, o_oracle, out_f32=None, lse=None, lse_oracle=None, what=""):
+    """AMB-17 on one (sequence, query head): the bf16 output within 2e-3 + one bf16 rounding (2^-8 |o|) of the
+    fp64 oracle; the fp32 output of pkv_index_set_debug_output (when given) within 2e-3 absolute; lse within
+    1e-3 relative (floor 1)."""
+    og = np.asarray(out_bf16, dtype=np.float64)
+    err = np.abs(og - o_oracle)
+    assert np.all(err <= ATT_ABS + 2.0 ** -8 * np.abs(o_oracle)), f"{what} attn err {err.max()}"
+    if out_f32 is not None:
+        e32 = np.abs(np.asarray(out_f32, dtype=np.float64) - o_oracle)
+        assert np.all(e32 <= ATT_F32), f"{what} fp32 attn err {e32.max()}"
+    if lse is not None:
+        assert abs(float(lse) - lse_oracle) <= 1e-3 * max(1.0, abs(lse_oracle)), f"{what} lse"

@@ -451,3 +451,65 @@ def test_p8_complement_symmetry_of_ranking():
         assert not np.any(np.signbit(s[s == 0]))
         rank = codebook.rank_centroids(s)
         assert np.array_equal(rank[255 - c], 255 - rank[c])
+
+
+# ---------------------------------------------------------------- helpers that were unpinned in round 1
+def test_eq4_blockwise_ip_equals_plain_inner_product():
+    """Eq. 4: sum_b r_b^k r_b^q <u_b^k, u_b^q> = <k~, q~>. Pinned against numpy's dot of the
+    unsplit rotated vectors (the identity the paper uses), including zero-radius subspaces (u := e_1, r = 0,
+    AMB-7), which must contribute nothing."""
+    rng = np.random.default_rng(31)
+    k = rng.standard_normal((50, 128))
+    q = rng.standard_normal((50, 128))
+    k[3, 16:24] = 0.0          # one zero subspace of the key
+    q[7, :8] = 0.0             # and of a query
+    for x, y in ((k, q), (transform.rotate_unscaled(k, SB), transform.rotate_unscaled(q, SB))):
+        rk, uk = transform.polar(transform.split(x, 16))
+        rq, uq = transform.polar(transform.split(y, 16))
+        got = transform.blockwise_ip(rk, uk, rq, uq)
+        want = np.einsum("nd,nd->n", x, y)
+        assert np.allclose(got, want, rtol=1e-12, atol=1e-10)
+    # a transposed operand (blocks of k against blocks of a different key) must not pass
+    rk, uk = transform.polar(transform.split(k, 16))
+    rq, uq = transform.polar(transform.split(q, 16))
+    assert not np.allclose(transform.blockwise_ip(rk, uk, rq[::-1], uq[::-1]), np.einsum("nd,nd->n", k, q))
+
+
+def test_dequantize_matches_code_semantics():
+    """P:400 ("dequantizes to v"), AMB-4/AMB-6: unpacking the stored nibbles and dequantising gives unit
+    subspace vectors whose signs are the sign bits, whose magnitudes are the Prop. 1 levels of the idx bits
+    (closed-form values A.1 in tests/golden), and whose inner product with u_b is the stored alpha wherever
+    the 1e-3 floor is inactive (Eq. 7)."""
+    rng = np.random.default_rng(32)
+    K = _bf16(rng.standard_normal((40, 128)))
+    meta = quantizer.encode_keys(K, SB, L32, MSQ)
+    v = quantizer.dequantize(quantizer.unpack_codes(meta["codes"]), L32)
+    assert v.shape == (40, 16, 8)
+    assert np.allclose(np.linalg.norm(v, axis=-1), 1.0, atol=1e-12)
+    nib = quantizer.unpack_codes(meta["codes"]).reshape(40, 16, 8).astype(np.int64)
+    y = meta["y"].reshape(40, 16, 8)
+    assert np.array_equal(v > 0, (nib >> 3) == 1)
+    assert np.array_equal((nib >> 3) == 1, y >= 0)                    # sign bit = sign of y (AMB-3)
+    # |v_j| / |v_0| = L[idx_j] / L[idx_0] with the printed A.1 levels
+    Lp = np.array([0.03072799, 0.09277686, 0.15670372, 0.22414131, 0.29752234, 0.38118776, 0.48522534, 0.65992414])
+    ratio = np.abs(v) / np.abs(v[..., :1])
+    assert np.allclose(ratio, Lp[nib & 7] / Lp[nib[..., :1] & 7], rtol=2e-7)
+    dots = np.sum(v * meta["u"], axis=-1)
+    live = dots > 1e-3
+    assert live.mean() > 0.99 and np.allclose(dots[live], meta["alpha"][live], rtol=1e-12)
+
+
+def test_attention_weights_are_the_softmax():
+    """Eq. 2: weights = exp(logit - lse) of the same logits (scipy softmax), sum to one,
+    a singleton gets weight 1 and equal logits give 1/n."""
+    rng = np.random.default_rng(33)
+    K = rng.standard_normal((77, 128))
+    q = rng.standard_normal(128)
+    sc = 1 / np.sqrt(128)
+    p = attention.attention_weights(q, K, sc)
+    assert np.allclose(p, scipy.special.softmax(K @ q * sc), rtol=1e-12)
+    _, lse = attention.full_attention(q, K, np.zeros((77, 1)), sc)
+    assert np.allclose(p, np.exp(K @ q * sc - lse), rtol=1e-12)
+    assert abs(p.sum() - 1) < 1e-12
+    assert np.allclose(attention.attention_weights(q, K[:1], sc), [1.0])
+    assert np.allclose(attention.attention_weights(q, np.tile(K[:1], (5, 1)), sc), 0.2)

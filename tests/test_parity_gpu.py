@@ -11,8 +11,8 @@ import torch
 
 import synth
 from oracle import attention, coarse, pipeline, sharded
-from tests.gpu_helpers import (ATT_ABS, SB, bf16_f64, check_encode, check_topk, oracle_meta, oracle_retrieval,
-                               w16_bound)
+from tests.gpu_helpers import (ATT_ABS, SB, bf16_f64, check_attention, check_encode, check_topk, oracle_meta,
+                               oracle_retrieval, w16_bound)
 
 pytestmark = pytest.mark.gpu
 
@@ -49,7 +49,10 @@ def run_and_check(pkv, K, q, V, k, T=None, C=None, n_hot=0, check_all_heads=True
     if n_hot:
         Kh = synth.isotropic(91, (batch, n_kv, n_hot, 128), device="cuda")
         Vh = synth.isotropic(92, (batch, n_kv, n_hot, 128), device="cuda")
+    out32 = torch.full((batch, n_q, 128), float("nan"), device="cuda")
+    ix.set_debug_output(out32)
     out, lse = pkv.sparse_attend(ix, q, K, V, idx, Kh, Vh)
+    ix.set_debug_output(None)
     ids_g, codes_g, w_g = [t.cpu().numpy() for t in ix.export()]
     torch.cuda.synchronize()
     Tn, Cn = dbg["T"], dbg["C"]
@@ -88,9 +91,7 @@ def run_and_check(pkv, K, q, V, k, T=None, C=None, n_hot=0, check_all_heads=True
                 o, l = pipeline.attend(qf, Kf, bf16_f64(V[b, g]), ig,
                                        None if Kh is None else bf16_f64(Kh[b, g]),
                                        None if Vh is None else bf16_f64(Vh[b, g]))
-                og = out[b, h].float().cpu().numpy()
-                assert np.all(np.abs(og - o) <= ATT_ABS + 2.0 ** -8 * np.abs(o)), f"attn err {np.max(np.abs(og - o))}"
-                assert abs(float(lse[b, h]) - l) <= 1e-3 * max(1.0, abs(l))
+                check_attention(out[b, h].float().cpu().numpy(), o, out32[b, h].cpu().numpy(), lse[b, h], l)
     return ix, idx, est, dbg
 
 
@@ -276,9 +277,22 @@ def test_sequence_sharded_local_equals_unsharded(pkv, P):
     offs = [a for a, _ in bounds]
     i1, e1 = pkv.retrieve_topk_sharded_local(shards, offs, q, 100, n)
     assert torch.equal(i0, i1) and torch.equal(e0, e1)
+    out32 = torch.full((1, 8, 128), float("nan"), device="cuda")
+    shards[0].set_debug_output(out32)
     o1, l1 = pkv.sparse_attend_sharded_local(shards, offs, q, Ks, Vs, i1, Kh, Vh)
-    assert torch.allclose(o0.float(), o1.float(), atol=2e-3, rtol=1e-2)
-    assert torch.allclose(l0, l1, atol=1e-4, rtol=1e-5)
+    torch.cuda.synchronize()
+    # the sharded attention (per-shard partials + LSE merge) against the oracle's Eq. 2-3 over the same rows
+    for h in range(8):
+        g = h // 4
+        o, l = pipeline.attend(bf16_f64(q[0, h]), bf16_f64(K[0, g]), bf16_f64(V[0, g]), i1[0, h].cpu().numpy(),
+                               bf16_f64(Kh[0, g]), bf16_f64(Vh[0, g]))
+        check_attention(o1[0, h].float().cpu().numpy(), o, out32[0, h].cpu().numpy(), l1[0, h], l, f"P={P} h={h}")
+    # the emulation restores each shard's offset: an unsharded call on a shard returns its local ids again
+    loc = pkv.Index(cfg, 1, bounds[-1][1] - bounds[-1][0])
+    pkv.encode_keys(loc, Ks[-1])
+    ia, ea, _ = pkv.retrieve_topk(loc, q, 100)
+    ib, eb, _ = pkv.retrieve_topk(shards[-1], q, 100)
+    assert torch.equal(ia, ib) and torch.equal(ea, eb)
 
 
 @pytest.mark.slow
@@ -303,11 +317,19 @@ def test_fused_exchange_sharded_local(pkv, P, n_hot):
         shards.append(ix)
         Ks.append(K[:, :, lo:hi].contiguous())
         Vs.append(V[:, :, lo:hi].contiguous())
+    out32 = torch.full((batch, n_q, 128), float("nan"), device="cuda")
+    shards[0].set_debug_output(out32)
     i1, e1, o1, l1 = pkv.retrieve_and_attend_sharded_local(shards, bounds[:P], q, Ks, Vs, k,
                                                            Kh if n_hot else None, Vh if n_hot else None)
     torch.cuda.synchronize()
     assert torch.equal(i0, i1) and torch.equal(e0, e1)
-    assert torch.allclose(o0.float(), o1.float(), atol=4e-3) and torch.allclose(l0, l1, atol=1e-4)
+    for b in range(batch):
+        for h in range(n_q):
+            g = h // (n_q // n_kv)
+            o, l = pipeline.attend(bf16_f64(q[b, h]), bf16_f64(K[b, g]), bf16_f64(V[b, g]), i1[b, h].cpu().numpy(),
+                                   bf16_f64(Kh[b, g]) if n_hot else None, bf16_f64(Vh[b, g]) if n_hot else None)
+            check_attention(o1[b, h].float().cpu().numpy(), o, out32[b, h].cpu().numpy(), l1[b, h], l,
+                            f"fused P={P} b={b} h={h}")
 
 
 def test_full_size_128k_sampled_head(pkv):
@@ -479,13 +501,16 @@ def test_retrieve_and_attend_matches_two_calls(pkv, n, n_hot, k):
         assert abs(float(l1[0, h]) - lse) <= 1e-3 * max(1.0, abs(lse))
 
 
-@pytest.mark.parametrize("n,C", [(60000, 40000), (150000, 140000)])
+@pytest.mark.parametrize("n,C", [(60000, 40000), (150000, 140000), (330000, 320000)])
 def test_segmented_topk_long_candidate_list(pkv, n, C):
     """Long candidate lists (the 1M-token regime): C = 40000 takes the cluster top-k (several CTAs per head),
-    C = 140000 > 8 x 16384 the per-segment top-k + merge. Both must equal the oracle top-k up to ties, and
-    retrieve_and_attend must take the same ids."""
+    C = 140000 and 320000 > 8 x 16384 the per-segment top-k (9 and 20 segment lists, more than the 8 rank slots
+    round 1 sized them by) + merge. The newest key is planted as every head's best match, so it sits in the LAST
+    segment; all must equal the oracle top-k up to ties, and retrieve_and_attend must take the same ids."""
     K, q, V = make_problem(17, 1, 4, 1, n)
-    run_and_check(pkv, K, q, V, k=100, C=C, check_all_heads=False)
+    K[0, 0, n - 1] = (q[0, 0].float() * 16.0).to(torch.bfloat16)
+    ix, idx, est, dbg = run_and_check(pkv, K, q, V, k=100, C=C, check_all_heads=False)
+    assert int(idx[0, 0, 0]) == n - 1
     cfg = pkv.config_init(4, 1, SB)
     ix = pkv.Index(cfg, 1, n)
     pkv.encode_keys(ix, K)
@@ -493,9 +518,15 @@ def test_segmented_topk_long_candidate_list(pkv, n, C):
     Kh = synth.isotropic(97, (1, 1, 40, 128), device="cuda")
     Vh = synth.isotropic(98, (1, 1, 40, 128), device="cuda")
     o0, l0 = pkv.sparse_attend(ix, q, K, V, i0, Kh, Vh)
+    out32 = torch.full((1, 4, 128), float("nan"), device="cuda")
+    ix.set_debug_output(out32)
     i1, e1, o1, l1 = pkv.retrieve_and_attend(ix, q, K, V, 100, Kh, Vh, n_cand=C)
+    torch.cuda.synchronize()
     assert torch.equal(i0, i1) and torch.equal(e0, e1)
-    assert torch.allclose(o0.float(), o1.float(), atol=4e-3) and torch.allclose(l0, l1, atol=1e-4)
+    for h in range(4):
+        o, l = pipeline.attend(bf16_f64(q[0, h]), bf16_f64(K[0, 0]), bf16_f64(V[0, 0]), i1[0, h].cpu().numpy(),
+                               bf16_f64(Kh[0, 0]), bf16_f64(Vh[0, 0]))
+        check_attention(o1[0, h].float().cpu().numpy(), o, out32[0, h].cpu().numpy(), l1[0, h], l, f"seg h={h}")
 
 
 def test_topk_massive_estimate_ties(pkv):
@@ -603,3 +634,64 @@ def test_gqa_union_rerank(pkv, monkeypatch):
     run_and_check(pkv, K, q, V, k=32)
     K, q, V = make_problem(94, 1, 8, 2, 4000)
     run_and_check(pkv, K, q, V, k=64, cfg=w16_cfg(pkv, 8, 2))
+
+
+def test_degenerate_key_stats(pkv):
+    """SURVEY §8(b), AMB-7: zero subspaces / zero keys are encoded deterministically and counted on the device;
+    the counts equal the oracle's (S_b == 0 of its exact y'); encode_keys resets them, appends add."""
+    K, q, V = make_problem(24, 2, 4, 2, 1500, plant=False)
+    K[0, 0, 5] = 0
+    K[1, 1, 6] = 0
+    K[0, 1, 7, 16:24] = 0
+    K[1, 0, 9, :64] = 0
+    K[0, 0, 30:40, 100:108] = 0
+    cfg = pkv.config_init(4, 2, SB)
+    ix = pkv.Index(cfg, 2, 3000)
+
+    def oracle_counts(Kt):
+        zk = kz = zs = 0
+        for b in range(Kt.shape[0]):
+            for g in range(Kt.shape[1]):
+                S = oracle_meta(bf16_f64(Kt[b, g]))["S"]
+                z = S == 0
+                zk += int(np.sum(z.all(axis=1)))
+                kz += int(np.sum(z.any(axis=1)))
+                zs += int(np.sum(z))
+        return zk, kz, zs
+
+    pkv.encode_keys(ix, K)
+    st = ix.stats()
+    assert (st["zero_keys"], st["keys_with_zero_subspace"], st["zero_subspaces"]) == oracle_counts(K)
+    assert st["zero_keys"] == 2 and st["n_keys"] == 1500
+    K2 = K[:, :, :700].clone()
+    K2[0, 0, 3] = 0
+    pkv.append_decode_keys(ix, K2)
+    st = ix.stats()
+    a, b = oracle_counts(K), oracle_counts(K2)
+    assert (st["zero_keys"], st["keys_with_zero_subspace"], st["zero_subspaces"]) == tuple(x + y for x, y in zip(a, b))
+    pkv.encode_keys(ix, K[:, :, 10:])  # replaces the content: counts restart
+    st = ix.stats()
+    assert (st["zero_keys"], st["keys_with_zero_subspace"], st["zero_subspaces"]) == oracle_counts(K[:, :, 10:])
+
+
+def test_hot_rows_capacity_validated(pkv):
+    """retrieve_and_attend_rows refuses hot_rows < n_hot (rows of one KV head would read the next head's)."""
+    import ctypes
+    K, q, V = make_problem(25, 1, 8, 2, 500, plant=False)
+    cfg = pkv.config_init(8, 2, SB)
+    ix = pkv.Index(cfg, 1, 500)
+    pkv.encode_keys(ix, K)
+    Kh = synth.isotropic(26, (1, 2, 64, 128), device="cuda")
+    T, C = pkv.schedule(500, 16)
+    p = pkv.RetrieveParams(T, C, 16, None, None, None, None, 0)
+    idx = torch.empty(1, 8, 16, dtype=torch.int32, device="cuda")
+    est = torch.empty(1, 8, 16, device="cuda")
+    out = torch.empty(1, 8, 128, dtype=torch.bfloat16, device="cuda")
+    sb, sh, st = K.stride(0), K.stride(1), K.stride(2)
+    vp = ctypes.c_void_p
+    args = lambda n_hot, rows: (ix.handle, vp(q.data_ptr()), ctypes.byref(p), vp(K.data_ptr()), vp(V.data_ptr()), sb,
+                                sh, st, vp(Kh.data_ptr()), vp(Kh.data_ptr()), n_hot, rows, 0.088, vp(idx.data_ptr()),
+                                vp(est.data_ptr()), vp(out.data_ptr()), None, vp(torch.cuda.current_stream().cuda_stream))
+    assert pkv._lib.retrieve_and_attend_rows(*args(64, 32)) == pkv.PKV_ERR_INVALID_ARG
+    assert pkv._lib.retrieve_and_attend_rows(*args(32, 64)) == pkv.PKV_OK
+    torch.cuda.synchronize()

@@ -13,7 +13,8 @@ import torch
 
 import synth
 from oracle import pipeline
-from tests.gpu_helpers import ATT_ABS, SB, bf16_f64, check_encode, check_topk, oracle_meta, oracle_retrieval
+from tests.gpu_helpers import (ATT_ABS, SB, bf16_f64, check_attention, check_encode, check_topk, oracle_meta,
+                               oracle_retrieval)
 
 pytestmark = pytest.mark.gpu
 
@@ -63,6 +64,8 @@ def test_stream_regions_and_outputs(pkv, sink, L, U, offload):
     st.prefill(K[:, :, :N].contiguous(), V[:, :, :N].contiguous())
     model = region_model(N, steps, sink, L, U)
     ref = pkv.Index(cfg, batch, N + steps)
+    out32 = torch.full((batch, n_q, 128), float("nan"), device="cuda")
+    ix.set_debug_output(out32)
     for s in range(steps):
         t = N + s  # token generated at this step
         q = qs[s % 4]
@@ -87,14 +90,21 @@ def test_stream_regions_and_outputs(pkv, sink, L, U, offload):
         pkv.encode_keys(ref, Kr)
         for a, b in zip(ix.export(), ref.export()):
             assert torch.equal(a, b), "index metadata"
-        # the decode output equals retrieve_and_attend over the same regions
+        # the decode output: Eq. 2-3 of the oracle over Sink U Local U Update U its retrieved rows (AMB-17)
+        o32 = out32.cpu().numpy()
+        for b in range(batch):
+            for h in range(n_q):
+                g = h // (n_q // n_kv)
+                o, l = pipeline.attend(bf16_f64(q[b, h]), bf16_f64(Kr[b, g]), bf16_f64(Vr[b, g]),
+                                       idx[b, h].cpu().numpy(), bf16_f64(Kx[b, g]), bf16_f64(Vx[b, g]))
+                check_attention(out[b, h].float().cpu().numpy(), o, o32[b, h], lse[b, h], l, f"step {s} b{b} h{h}")
+        # and its retrieval equals retrieve_and_attend over the same regions (bit-exact ids and estimates)
         i1, e1, o1, l1 = pkv.retrieve_and_attend(ref, q, Kr, Vr, k, Kx, Vx)
         i2, e2, _ = pkv.retrieve_topk(ix, q, k)
         bad = (i1 != idx).any(-1)
         assert torch.equal(i1, idx) and torch.equal(e1, est), (
             f"retrieval: step {s} n_r {n_r} heads {bad.nonzero().tolist()} stream-vs-topk "
             f"{torch.equal(i2, idx)} ref-vs-topk {torch.equal(i2, i1)} est {(e1 - est).abs().max().item()}")
-        assert torch.allclose(o1.float(), out.float(), atol=4e-3) and torch.allclose(l1, lse, atol=1e-4)
 
 
 def test_stream_decode_matches_oracle(pkv):
@@ -157,3 +167,44 @@ def test_stream_capacity_and_args(pkv):
         st.decode(qs[0], K[:, :, t].contiguous(), V[:, :, t].contiguous(), 16)
     assert e.value.status == pkv.PKV_ERR_CAPACITY
     assert st.state() == (300, 32, 7)
+
+
+@pytest.mark.parametrize("n_prompt", [16, 50, 80])
+def test_stream_short_prompt_empty_retrieval_zone(pkv, n_prompt):
+    """A prompt of at most sink + local_size tokens leaves the retrieval zone empty until the first flush: those
+    steps attend the hot rows alone (ids -1, estimates -inf), later steps retrieve; every output against the
+    oracle (Eq. 2-3 over all tokens so far while nothing is evicted). A refused call changes nothing."""
+    batch, n_q, n_kv, k = 1, 4, 1, 16
+    sink, L, U = 16, 64, 32
+    steps = 80
+    K, V, qs = make_tokens(71 + n_prompt, batch, n_q, n_kv, n_prompt + steps)
+    cfg = pkv.config_init(n_q, n_kv, SB)
+    ix = pkv.Index(cfg, batch, n_prompt + steps)
+    st = pkv.Stream(ix, sink=sink, local_size=L, update_size=U)
+    st.prefill(K[:, :, :n_prompt].contiguous(), V[:, :, :n_prompt].contiguous())
+    assert st.state() == (0, n_prompt - sink, 0)
+    model = region_model(n_prompt, steps, sink, L, U)
+    out32 = torch.full((batch, n_q, 128), float("nan"), device="cuda")
+    ix.set_debug_output(out32)
+    for s in range(steps):
+        t = n_prompt + s
+        kn, vn = K[:, :, t].contiguous(), V[:, :, t].contiguous()
+        if s == 3:  # invalid top_k: refused before any state change
+            with pytest.raises(pkv.PkvError) as e:
+                st.decode(qs[0], kn, vn, 0)
+            assert e.value.status == pkv.PKV_ERR_INVALID_ARG and st.state() == model[s - 1]
+        idx, est, out, lse = st.decode(qs[s % 4], kn, vn, k)
+        assert st.state() == model[s]
+        n_r = model[s][0]
+        torch.cuda.synchronize()
+        hot_tok = list(range(sink)) + list(range(sink + n_r, t + 1))
+        for h in range(n_q):
+            qf = bf16_f64(qs[s % 4][0, h])
+            ig = idx[0, h].cpu().numpy()
+            if n_r == 0:
+                assert np.all(ig == -1) and np.all(np.isneginf(est[0, h].cpu().numpy()))
+            o, l = pipeline.attend(qf, bf16_f64(K[0, 0, sink:sink + n_r]), bf16_f64(V[0, 0, sink:sink + n_r]), ig,
+                                   bf16_f64(K[0, 0, hot_tok]), bf16_f64(V[0, 0, hot_tok]))
+            check_attention(out[0, h].float().cpu().numpy(), o, out32[0, h].cpu().numpy(), lse[0, h], l,
+                            f"step {s} h{h}")
+    assert model[-1][0] > 0  # the run crossed at least one flush
