@@ -67,13 +67,14 @@ def _worker(rank, port, result_dir):
         out32 = torch.full((batch, n_q, 128), float("nan"), device="cuda")
         ix.set_debug_output(out32)
         # three-exchange path: retrieve_topk (H, T) then sparse_attend (A)
-        i1, e1, _ = pkv.retrieve_topk(ix, q, k)           # n_global recorded at comm init (sum of shard lengths)
+        i1, e1, _ = pkv.retrieve_topk(ix, q, k, n_global=n)  # T and C from the global schedule
         o1, l1 = pkv.sparse_attend(ix, q, Kl, Vl, i1, hk, hv)
         torch.cuda.synchronize()
         assert torch.equal(i0, i1) and torch.equal(e0, e1), f"rank {rank}: sharded top-k differs"
         o32a = out32.clone()
-        # fused T+A path (two exchanges), n_global passed per call
-        i2, e2, o2, l2 = pkv.retrieve_and_attend(ix, q, Kl, Vl, k, hk, hv, n_global=n)
+        # fused T+A path (two exchanges); params.n_global = 0: the length recorded at comm init (sum of shards)
+        T, C = pkv.schedule(n, k)
+        i2, e2, o2, l2 = pkv.retrieve_and_attend(ix, q, Kl, Vl, k, hk, hv, probes_T=T, n_cand=C)
         torch.cuda.synchronize()
         assert torch.equal(i0, i2) and torch.equal(e0, e2), f"rank {rank}: fused top-k differs"
         for b in range(batch):

@@ -176,7 +176,7 @@ def test_stream_short_prompt_empty_retrieval_zone(pkv, n_prompt):
     oracle (Eq. 2-3 over all tokens so far while nothing is evicted). A refused call changes nothing."""
     batch, n_q, n_kv, k = 1, 4, 1, 16
     sink, L, U = 16, 64, 32
-    steps = 80
+    steps = 130
     K, V, qs = make_tokens(71 + n_prompt, batch, n_q, n_kv, n_prompt + steps)
     cfg = pkv.config_init(n_q, n_kv, SB)
     ix = pkv.Index(cfg, batch, n_prompt + steps)
