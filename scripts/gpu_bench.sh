@@ -3,6 +3,8 @@ cd $GRAFT_REPO_ROOT
 tag=${1:-b}; shift
 mkdir -p gpurun_out
 python -m paper_2602_07721_b200.build > gpurun_out/build_$tag.log 2>&1 || { tail -30 gpurun_out/build_$tag.log; exit 1; }
-/usr/bin/time -v timeout 1500 python bench.py "$@" > gpurun_out/bench_$tag.log 2> gpurun_out/bench_${tag}_err.log
-tail -c 600 gpurun_out/bench_$tag.log; echo
-grep -E "Elapsed|Maximum resident" gpurun_out/bench_${tag}_err.log
+start=$(date +%s)
+timeout 1500 python bench.py "$@" > gpurun_out/bench_$tag.log 2> gpurun_out/bench_${tag}_err.log
+echo "rc=$? wall_s=$(( $(date +%s) - start ))"
+tail -c 3000 gpurun_out/bench_$tag.log; echo
+tail -5 gpurun_out/bench_${tag}_err.log
