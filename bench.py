@@ -396,7 +396,9 @@ def measure(args, config: str) -> dict:
         kern[name] = ent
     dom = max((k for k in kern if k in alg), key=lambda k: prof[k][1])
     traffic = None
-    tr_file = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    # per-kernel DRAM bytes from the latest committed `ncu --set full` capture (this round's, else round 1's)
+    tr_file = next((f for f in (os.path.join(ROOT, "profiles", r, "ncu_traffic.json") for r in ("r02", "r01"))
+                    if os.path.exists(f)), "")
     if os.path.exists(tr_file):
         try:
             traffic = json.load(open(tr_file)).get(config, {}).get(dom)
@@ -404,7 +406,7 @@ def measure(args, config: str) -> dict:
             traffic = None
     roof = {"bound": "hbm", "kernel": dom, "achieved": kern[dom]["gbs"], "peak": hbm_peak, "unit": "GB/s",
             "frac": round(kern[dom]["gbs"] / hbm_peak, 4), "traffic": traffic, "peak_source": peak_kind}
-    fl_file = os.path.join(ROOT, "profiles", "floors_r01.json")
+    fl_file = os.path.join(ROOT, "profiles", "r01", "floors_r01.json")
     if uva and fused and dom == "topk" and os.path.exists(fl_file):
         # at 1M the fused top-k is bound by its UVA gather of the k selected rows (SURVEY §8(d) "host link"):
         # its roofline is the measured host-link read rate, over the bytes that cross the link
@@ -414,7 +416,7 @@ def measure(args, config: str) -> dict:
         roof = {"bound": "host_link", "kernel": dom, "achieved": ach, "peak": link, "unit": "GB/s",
                 "frac": round(ach / link, 4), "traffic": traffic, "peak_source": "measured (scripts/uva_bw.cu)",
                 "host_bytes_per_launch": host_bytes}
-    # context: measured data-movement floors of the two gathers (profiles/floors_r01.json, scripts/hbm_gather.cu,
+    # context: measured data-movement floors of the two gathers (profiles/r01/floors_r01.json, scripts/hbm_gather.cu,
     # scripts/uva_bw.cu) — the rerank's random 128 B record gather from HBM and, at 1M, the UVA row gather
     if os.path.exists(fl_file) and world == 1 and not args.w16:
         try:
@@ -434,7 +436,7 @@ def measure(args, config: str) -> dict:
                                              "frac_of_measured_peak": round(scan_gbs / hbm_peak, 4),
                                              "timing": "CUDA events around eager launches (breaks PDL overlap)"}
     # the same kernel timed by ncu (warm launch list committed under profiles/, serialised, no PDL overlap)
-    warm_file = os.path.join(ROOT, "profiles", "ncu_warm_r02.json")
+    warm_file = os.path.join(ROOT, "profiles", "r02", "ncu_warm.json")
     if scan_vs is not None and os.path.exists(warm_file):
         try:
             wu = json.load(open(warm_file)).get(config, {}).get("scan_us")
@@ -443,7 +445,7 @@ def measure(args, config: str) -> dict:
         if wu:
             g2 = round(alg["scan"] / (wu * 1e-6) / 1e9, 1)
             scan_vs.update({"ncu_warm_us": wu, "ncu_gbs": g2, "ncu_frac_of_8tbs": round(g2 / 8000.0, 4),
-                            "ncu_frac_of_measured_peak": round(g2 / hbm_peak, 4), "ncu_source": "profiles/ncu_warm_r02.json"})
+                            "ncu_frac_of_measured_peak": round(g2 / hbm_peak, 4), "ncu_source": "profiles/r02/ncu_warm.json"})
 
     res = None
     if rank == 0:
