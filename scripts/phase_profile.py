@@ -32,13 +32,22 @@ if os.environ.get("PHASE_UVA") == "1":  # K/V rows read through UVA from pinned 
 for _ in range(3):
     pkv.retrieve_and_attend(ix, q, K, V, 100, Kh, Vh)
 torch.cuda.synchronize()
+# replay one layer's five kernels from a CUDA graph, as bench.py does (eager launches add host-side gaps)
+graph = torch.cuda.CUDAGraph()
+st = torch.cuda.Stream()
+with torch.cuda.stream(st):
+    pkv.retrieve_and_attend(ix, q, K, V, 100, Kh, Vh)
+    st.synchronize()
+    with torch.cuda.graph(graph, stream=st):
+        pkv.retrieve_and_attend(ix, q, K, V, 100, Kh, Vh)
+torch.cuda.synchronize()
 buf = torch.zeros(256 + 8192, dtype=torch.int64, device=dev)
 pkv._lib.pkv_phase_profile(ctypes.c_void_p(buf.data_ptr()))
 names = {1: "qprep", 2: "scan", 3: "select", 5: "rerank", 6: "topk+attend", 8: "hot attend"}
 for rep in range(3):
     buf.zero_()
     torch.cuda._sleep(20_000_000)
-    pkv.retrieve_and_attend(ix, q, K, V, 100, Kh, Vh)
+    graph.replay()
     torch.cuda.synchronize()
     allb = buf.cpu().tolist()
     b = [allb[16 * i:16 * i + 16] for i in range(16)]
