@@ -228,6 +228,14 @@ def measure(args, config: str) -> dict:
         for ly in layers:
             ly["ix"].set_postings(True)
         torch.cuda.synchronize()
+    rho_keys = 0
+    if args.key_fraction:  # rho as a fraction of keys (AMB-8b): occupancy counts, per-subspace probes
+        if world > 1:
+            raise SystemExit("--key-fraction is single-GPU (the occupancy counts are not exchanged)")
+        rho_keys = pkv.schedule_key_fraction(n)
+        for ly in layers:
+            ly["ix"].set_occupancy(True)
+        torch.cuda.synchronize()
     if uva and not args.k_hbm:  # the device copies were only needed to build the summaries
         for d in data:
             d["Kd"] = None
@@ -249,10 +257,10 @@ def measure(args, config: str) -> dict:
         if fused:  # one decode step of one layer: retrieval + attention scheduled as one unit
             pkv.retrieve_and_attend(ly["ix"], ly["q"], ly["K"], ly["V"], TOP_K, ly["Kh"], ly["Vh"], probes_T=T,
                                     n_cand=C, n_global=n, out_idx=ly["idx"], out_est=ly["est"], out=ly["out"],
-                                    lse=ly["lse"])
+                                    lse=ly["lse"], rho_keys=rho_keys)
         else:
             pkv.retrieve_topk(ly["ix"], ly["q"], TOP_K, probes_T=T, n_cand=C, n_global=n, out_idx=ly["idx"],
-                              out_est=ly["est"])
+                              out_est=ly["est"], rho_keys=rho_keys)
             pkv.sparse_attend(ly["ix"], ly["q"], ly["K"], ly["V"], ly["idx"], ly["Kh"], ly["Vh"], out=ly["out"],
                               lse=ly["lse"])
 
@@ -460,6 +468,7 @@ def measure(args, config: str) -> dict:
                        "l2": "inputs > L2: 32 layer-distinct indices + K/V touched per step",
                        "rerank_weights": "fp16 (96 B records)" if args.w16 else "fp32 (128 B records)",
                        "collision_scan": "inverted lists" if args.inverted else "dense",
+                       "rho_reading": f"key fraction, rho_keys={rho_keys}" if rho_keys else f"centroid fraction, T={T}",
                        "kv_placement": ("K in HBM, V in pinned host (UVA)" if args.k_hbm else "K, V in pinned host (UVA)")
                        if uva else "HBM",
                        "cuda_graph": use_graph},
@@ -627,6 +636,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--w16", action="store_true", help="fp16 rerank weights (96-byte records, AMB-20 / SURVEY f2)")
     ap.add_argument("--inverted", action="store_true", help="inverted-list collision scan (SURVEY f4)")
+    ap.add_argument("--key-fraction", action="store_true",
+                    help="rho as a fraction of keys (AMB-8b, SURVEY f4): per-subspace probes from occupancy counts")
     ap.add_argument("--k-hbm", action="store_true",
                     help="1M variant: keys in HBM, only values in pinned host memory (half the UVA bytes)")
     args = ap.parse_args()

@@ -138,6 +138,13 @@ typedef struct {
   int64_t n_global;     /* sequence-sharded calls: the global retrieval length n_cand is checked against; */
                         /* <= 0 takes the communicator's record (pkv_comm_init / pkv_comm_set_global_len). */
                         /* Ignored by unsharded calls (the index length is used).                        */
+  int64_t rho_keys;     /* 0: rho read as a fraction of CENTROIDS, T = probes_T probes per subspace      */
+                        /* (AMB-8). > 0: the KEY-fraction reading (AMB-8b, "only let the     */
+                        /* top-rho fraction contribute a non-zero bonus", "scales with rho n"): per */
+                        /* (query head, subspace) the centroids are probed in rank order until they hold */
+                        /* >= rho_keys indexed keys (pkv_schedule_key_fraction gives ceil(rho n)); the 6 */
+                        /* tiers split that subspace's probe count T_b as AMB-10 splits T. Needs         */
+                        /* pkv_index_set_occupancy(index, 1); in [0, n]; UNSUPPORTED when sharded.       */
 } pkv_retrieve_params;
 
 /* (3) retrieve_topk — per decode step. q: device bf16 [batch][n_q][D] contiguous.
@@ -249,6 +256,15 @@ pkv_status pkv_stream_state(const pkv_stream* s, int64_t* n_retrieval, int32_t* 
  * results are identical to the dense scan's. enable = 0 returns to the dense scan (buffers are kept).
  * Errors: UNSUPPORTED if the capacity exceeds 256 chunks (2,097,152 keys), CUDA on allocation failure. */
 pkv_status pkv_index_set_postings(pkv_index* index, int32_t enable, cudaStream_t stream);
+
+/* Key-fraction reading of rho: enable = 1 allocates the per-(sequence, KV head,
+ * subspace) centroid occupancy histogram (16 x 256 u32 counts: how many indexed keys carry each centroid id),
+ * counts the current retrieval zone on `stream`, and keeps it current on every later encode_keys /
+ * append_decode_keys; enable = 0 frees it. Required by retrieve calls with rho_keys > 0. */
+pkv_status pkv_index_set_occupancy(pkv_index* index, int32_t enable, cudaStream_t stream);
+
+/* rho_keys = ceil(rho * n) with rho from the same (rho, beta) schedule as pkv_schedule (AMB-11). */
+pkv_status pkv_schedule_key_fraction(int64_t n, int64_t* rho_keys);
 
 /* Degenerate-key accounting (AMB-7; replaces the per-key API error of S:89): keys whose rotated
  * subspace b has S_b = 0 get the deterministic encoding of e_1 in that subspace (id 0xFF, w_b = 0) and are

@@ -5,6 +5,9 @@
 * collision_scores      score_i = sum_b bonus_b(id_{i,b})  in [0, B * max bonus]
 * bucket_topk           C = ceil(beta n) highest integer scores by counting (P:478, P:509, P:525);
                         ties in the threshold bucket: newest (larger index) first (AMB-12)
+* key-fraction reading of rho (AMB-8b): occupancy, key_fraction_target,
+  key_fraction_probes, query_bonus_tables_keys — "only let the top-rho fraction contribute a non-zero bonus"
+   read as a fraction of KEYS, so that "collision processing scales with rho n"
 """
 from __future__ import annotations
 
@@ -110,3 +113,50 @@ def bucket_topk_by_sort(score: np.ndarray, C: int) -> np.ndarray:
     score = np.asarray(score, dtype=np.int64)
     order = sorted(range(len(score)), key=lambda i: (-score[i], -i))
     return np.sort(np.array(order[:C], dtype=np.int64))
+
+
+# ---------------------------------------------------------------- key-fraction reading of rho (AMB-8b)
+def occupancy(ids: np.ndarray, n_centroids: int = 256) -> np.ndarray:
+    """occ[b, c] = number of keys whose subspace-b centroid id is c (per-subspace occupancy histogram)."""
+    ids = np.asarray(ids).astype(np.int64)
+    n, B = ids.shape
+    occ = np.zeros((B, n_centroids), dtype=np.int64)
+    for b in range(B):
+        for c in ids[:, b]:
+            occ[b, c] += 1
+    return occ
+
+
+def key_fraction_target(n: int, table=SCHEDULE_BP) -> int:
+    """rho_keys = ceil(rho n): keys each subspace's probed centroids must hold (rho of the AMB-11 schedule)."""
+    rho_bp = table[0][1]
+    for min_len, r_bp, _ in table:
+        if n >= min_len:
+            rho_bp = r_bp
+    return int((rho_bp * n + 9999) // 10000)
+
+
+def key_fraction_probes(rank: np.ndarray, occ_b: np.ndarray, rho_keys: int) -> int:
+    """T_b: probe centroids in rank order (best first, AMB-9) until the probed ones hold >= rho_keys keys —
+    the top-rho fraction of the keys by their centroid's query score gets a bonus, whole centroids."""
+    order = np.argsort(np.asarray(rank))  # order[r] = the centroid of rank r
+    held, T = 0, 0
+    while held < rho_keys:
+        held += int(occ_b[order[T]])
+        T += 1
+    return T
+
+
+def query_bonus_tables_keys(q: np.ndarray, rot_sign_bits: np.ndarray, occ: np.ndarray, rho_keys: int,
+                            B: int = 16, tier_bonus=(6, 5, 4, 3, 2, 1)):
+    """(bonus[b, c], T_b[b]) for one query under the key-fraction reading: per subspace the same ranking and
+    tiers as query_bonus_tables (AMB-9/10) with that subspace's own probe count T_b."""
+    y = transform.rotate_unscaled(q, rot_sign_bits)
+    yb = transform.split(y, B)
+    out = np.zeros((B, 2 ** yb.shape[-1]), dtype=np.int64)
+    Tb = np.zeros(B, dtype=np.int64)
+    for b in range(B):
+        rank = codebook.rank_centroids(codebook.centroid_scores(yb[b]))
+        Tb[b] = key_fraction_probes(rank, occ[b], rho_keys)
+        out[b] = codebook.tier_bonus_of_rank(rank, int(Tb[b]), tier_bonus)
+    return out, Tb

@@ -17,17 +17,23 @@ from . import attention, coarse, quantizer, rerank
 
 
 def decode_step(meta: dict, Q: np.ndarray, rot_sign_bits: np.ndarray, top_k: int,
-                tier_bonus=(6, 5, 4, 3, 2, 1), T: int | None = None, C: int | None = None) -> list:
+                tier_bonus=(6, 5, 4, 3, 2, 1), T: int | None = None, C: int | None = None,
+                rho_keys: int | None = None) -> list:
     """Retrieval for the query heads Q [G, D] against the encoded retrieval zone `meta`.
+    rho_keys: the key-fraction reading of rho (AMB-8b) instead of T probes per subspace.
 
     Returns one dict per query head: bonus, score, cand, est, idx, topk_est, T, C."""
     n = meta["ids"].shape[0]
     T0, C0 = coarse.schedule(n, top_k)
     T = T0 if T is None else T
     C = C0 if C is None else C
+    occ = coarse.occupancy(meta["ids"]) if rho_keys else None
     out = []
     for q in np.asarray(Q, dtype=np.float64):
-        bonus = coarse.query_bonus_tables(q, rot_sign_bits, T, tier_bonus=tier_bonus)
+        if rho_keys:
+            bonus, _ = coarse.query_bonus_tables_keys(q, rot_sign_bits, occ, rho_keys, tier_bonus=tier_bonus)
+        else:
+            bonus = coarse.query_bonus_tables(q, rot_sign_bits, T, tier_bonus=tier_bonus)
         score = coarse.collision_scores(meta["ids"], bonus)
         cand = coarse.bucket_topk(score, C)
         qt, qn = rerank.rotated_unit_query(q, rot_sign_bits)

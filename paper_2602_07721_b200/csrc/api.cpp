@@ -190,7 +190,7 @@ pkv_status check_kv_layout(const void* K, int64_t sb, int64_t sh, int64_t st, co
 // -------------------------------------------------------------- retrieval phases (shared by all modes)
 pkv_status phase_scan(pkv_index* ix, const void* q, const pkv_retrieve_params* p, ScanPlan& plan, cudaStream_t s) {
   const int64_t n = ix->n;
-  PKV_CUDA(launch_qprep(ix, q, p->probes_T, p->dbg_q_rot, s), "qprep");
+  PKV_CUDA(launch_qprep(ix, q, p->probes_T, p->rho_keys, p->dbg_q_rot, s), "qprep");
   plan = plan_scan(ix, n > 0 ? n : 1);
   if (n > 0 && ix->postings) {
     PKV_CUDA(launch_postings_scan(ix, n, score_stride(ix), s), "postings scan");
@@ -295,6 +295,12 @@ pkv_status check_retrieve(const pkv_index* ix, const void* q, const pkv_retrieve
   if (n_global < 1) return set_error(PKV_ERR_INVALID_ARG, "retrieve_topk: empty retrieval zone");
   if (p->n_cand < std::min<int64_t>(p->top_k, n_global) || p->n_cand > n_global)
     return set_error(PKV_ERR_INVALID_ARG, "retrieve_topk: n_cand must be in [min(top_k, n), n]");
+  if (p->rho_keys < 0 || p->rho_keys > n_global)
+    return set_error(PKV_ERR_INVALID_ARG, "retrieve_topk: rho_keys must be in [0, n]");
+  if (p->rho_keys > 0 && !ix->occ)
+    return set_error(PKV_ERR_INVALID_ARG, "retrieve_topk: rho_keys needs pkv_index_set_occupancy(index, 1)");
+  if (p->rho_keys > 0 && ix->world > 1)
+    return set_error(PKV_ERR_UNSUPPORTED, "retrieve_topk: the key-fraction reading is not sequence-sharded");
   return PKV_OK;
 }
 
@@ -387,6 +393,7 @@ pkv_status pkv_index_destroy(pkv_index* ix) {
   release_workspace(ix->ws);
   cudaFree(ix->ids);
   cudaFree(ix->rec);
+  cudaFree(ix->occ);
   cudaFree(ix->post_off);
   cudaFree(ix->post_key);
   cudaFree(ix->enc_fb);
@@ -440,6 +447,27 @@ pkv_status pkv_index_set_postings(pkv_index* ix, int32_t enable, cudaStream_t st
   return PKV_OK;
 }
 
+pkv_status pkv_index_set_occupancy(pkv_index* ix, int32_t enable, cudaStream_t stream) {
+  if (!ix) return set_error(PKV_ERR_INVALID_ARG, "pkv_index_set_occupancy: null index");
+  DeviceGuard g(ix->device);
+  if (!enable) {
+    cudaFree(ix->occ);
+    ix->occ = nullptr;
+    return PKV_OK;
+  }
+  const size_t bytes = (size_t)ix->batch * ix->cfg.n_kv_heads * NB * NC * 4;
+  if (!ix->occ) {
+    cudaError_t e = cudaMalloc(&ix->occ, bytes);
+    if (e != cudaSuccess) {
+      ix->occ = nullptr;
+      return cuda_status(e, "pkv_index_set_occupancy");
+    }
+  }
+  PKV_CUDA(cudaMemsetAsync(ix->occ, 0, bytes, stream), "occupancy clear");
+  PKV_CUDA(launch_occupancy(ix, 0, ix->n, stream), "occupancy");
+  return PKV_OK;
+}
+
 pkv_status pkv_index_len(const pkv_index* ix, int64_t* n_out) {
   if (!ix || !n_out) return set_error(PKV_ERR_INVALID_ARG, "pkv_index_len: null pointer");
   *n_out = ix->n;
@@ -476,6 +504,11 @@ pkv_status encode_keys(pkv_index* ix, const void* K, int64_t sb, int64_t sh, int
   }
   ix->n = n;
   if (ix->postings) PKV_CUDA(launch_postings_build(ix, 0, (n + POST_CHUNK - 1) / POST_CHUNK, stream), "postings");
+  if (ix->occ) {
+    PKV_CUDA(cudaMemsetAsync(ix->occ, 0, (size_t)ix->batch * ix->cfg.n_kv_heads * NB * NC * 4, stream),
+             "occupancy clear");
+    PKV_CUDA(launch_occupancy(ix, 0, n, stream), "occupancy");
+  }
   return PKV_OK;
 }
 
@@ -494,6 +527,7 @@ pkv_status append_decode_keys(pkv_index* ix, const void* K, int64_t sb, int64_t 
     if (se != PKV_OK) return se;
   }
   const int64_t first = ix->n / POST_CHUNK;  // the partial chunk and the new ones are rebuilt
+  if (ix->occ && t > 0) PKV_CUDA(launch_occupancy(ix, ix->n, ix->n + t, stream), "occupancy(append)");
   ix->n += t;
   if (ix->postings && t > 0)
     PKV_CUDA(launch_postings_build(ix, first, (ix->n + POST_CHUNK - 1) / POST_CHUNK, stream), "postings(append)");

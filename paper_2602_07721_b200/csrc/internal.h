@@ -95,6 +95,7 @@ struct pkv_index {
   unsigned long long* stats = nullptr;  // device [4]: zero keys, keys with a zero subspace, zero subspaces, spare
   int32_t* enc_fb = nullptr;  // [batch*n_kv*cap + 1]: tensor-core encoder fallback list, count at the end
   bool postings = false;
+  uint32_t* occ = nullptr;  // [batch][n_kv][16][256] centroid occupancy (pkv_index_set_occupancy); null = off
   uint16_t* post_off = nullptr;
   uint16_t* post_key = nullptr;
   pkv::Workspace* ws = nullptr;
@@ -155,7 +156,9 @@ cudaError_t launch_encode(const pkv_index* ix, const void* K, int64_t sb, int64_
                           int64_t count, cudaStream_t stream);
 cudaError_t launch_export(const pkv_index* ix, int64_t start, int64_t count, uint8_t* ids, uint8_t* codes,
                           float* w, cudaStream_t stream);
-cudaError_t launch_qprep(const pkv_index* ix, const void* q, int T, float* dbg_q_rot, cudaStream_t stream);
+cudaError_t launch_qprep(const pkv_index* ix, const void* q, int T, int64_t rho_keys, float* dbg_q_rot,
+                         cudaStream_t stream);
+cudaError_t launch_occupancy(const pkv_index* ix, int64_t t0, int64_t t1, cudaStream_t stream);
 
 constexpr int POST_CHUNK = 8192;  // keys per inverted-list chunk (u16 offsets)
 

@@ -75,17 +75,33 @@ extern "C" pkv_status pkv_config_init(pkv_config* cfg, int32_t n_q_heads, int32_
   return PKV_OK;
 }
 
+// (min_length, rho, beta) in basis points — reading AMB-11
+static void schedule_bp(int64_t n, int64_t* rho, int64_t* beta) {
+  static const int64_t table[4][3] = {{0, 1500, 1000}, {20000, 1200, 800}, {60000, 1000, 600}, {200000, 800, 500}};
+  *rho = table[0][1];
+  *beta = table[0][2];
+  for (auto& r : table)
+    if (n >= r[0]) {
+      *rho = r[1];
+      *beta = r[2];
+    }
+}
+
+// Key-fraction reading of rho (AMB-8b): rho_keys = ceil(rho n) keys per subspace must be covered by
+// the probed centroids.
+extern "C" pkv_status pkv_schedule_key_fraction(int64_t n, int64_t* rho_keys) {
+  if (n < 0 || !rho_keys) return pkv::set_error(PKV_ERR_INVALID_ARG, "pkv_schedule_key_fraction: bad argument");
+  int64_t rho, beta;
+  schedule_bp(n, &rho, &beta);
+  *rho_keys = (rho * n + 9999) / 10000;
+  return PKV_OK;
+}
+
 extern "C" pkv_status pkv_schedule(int64_t n, int32_t top_k, int32_t* probes_T, int64_t* n_cand) {
   if (n < 0 || top_k < 1 || !probes_T || !n_cand)
     return pkv::set_error(PKV_ERR_INVALID_ARG, "pkv_schedule: bad argument");
-  // (min_length, rho, beta) in basis points — reading AMB-11
-  static const int64_t table[4][3] = {{0, 1500, 1000}, {20000, 1200, 800}, {60000, 1000, 600}, {200000, 800, 500}};
-  int64_t rho = table[0][1], beta = table[0][2];
-  for (auto& r : table)
-    if (n >= r[0]) {
-      rho = r[1];
-      beta = r[2];
-    }
+  int64_t rho, beta;
+  schedule_bp(n, &rho, &beta);
   *probes_T = (int32_t)((rho * PKV_CENTROIDS + 9999) / 10000);
   int64_t c = (beta * n + 9999) / 10000;
   const int64_t lo = top_k < n ? top_k : n;

@@ -42,7 +42,8 @@ __device__ __forceinline__ void ce(KV& mine, const KV& o, int p, int k, int j) {
 __global__ void __launch_bounds__(QP_THREADS) qprep_kernel(const uint16_t* q, int T, DevCfg cfg,
                                                           uint32_t* lut, float* rtab,
                                                           float* qnorm, float* qrot,
-                                                          float* dbg_q_rot, unsigned int* ucount) {
+                                                          float* dbg_q_rot, unsigned int* ucount,
+                                                          const uint32_t* occ, int64_t rho_keys) {
   __shared__ unsigned long long sk[2][NC / 2];
   __shared__ uint32_t si[2][NC / 2];
   phase_mark(K_QPREP, 0);
@@ -215,6 +216,54 @@ __global__ void __launch_bounds__(QP_THREADS) qprep_kernel(const uint16_t* q, in
     }
   }
   phase_mark(K_QPREP, 3);
+  // Key-fraction reading of rho (AMB-8b): this subspace probes its centroids in rank order until the
+  // probed ones hold >= rho_keys indexed keys: T_b = 1 + the first rank whose inclusive occupancy prefix reaches
+  // rho_keys. Ranks 0..127 are the sorted leaders (rank p at thread p/2), ranks 128..255 their complements in
+  // reverse (rank 255 - p), so the prefix before complement rank 255 - p is (all leaders) + (complements of the
+  // leaders after p). Two block scans over the 64 threads of each subspace (the pair's halves are independent).
+  if (occ != nullptr) {
+    __shared__ uint32_t s_wsum[4][2];  // per warp: leader total, complement total
+    __shared__ int s_T[2];
+    const uint32_t* ob = occ + (((int64_t)b * cfg.n_kv + g) * NB + sb) * NC;
+    uint32_t oL[2], oC[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      oL[i] = ob[e[i].id];
+      oC[i] = ob[NC - 1 - e[i].id];
+    }
+    const uint32_t sL = oL[0] + oL[1], sC = oC[0] + oC[1];
+    uint32_t iL = sL, iC = sC;  // inclusive scans over this warp's lanes
+#pragma unroll
+    for (int x = 1; x < 32; x <<= 1) {
+      const uint32_t a = __shfl_up_sync(0xffffffffu, iL, x), c = __shfl_up_sync(0xffffffffu, iC, x);
+      if (lane >= x) {
+        iL += a;
+        iC += c;
+      }
+    }
+    if (lane == 31) {
+      s_wsum[warp][0] = iL;
+      s_wsum[warp][1] = iC;
+    }
+    if (tl == 0) s_T[half] = 0;  // rho_keys == 0 would probe nothing (never reached: rho_keys >= 1 here)
+    __syncthreads();
+    const int w0 = 2 * half;  // the two warps of this subspace: w0 (threads 0..31 of the half), w0 + 1
+    const bool upper = (warp & 1) != 0;
+    const uint32_t TL = s_wsum[w0][0] + s_wsum[w0 + 1][0], TC = s_wsum[w0][1] + s_wsum[w0 + 1][1];
+    const uint32_t exL = (upper ? s_wsum[w0][0] : 0u) + iL - sL;  // leaders before rank 2tl
+    const uint32_t exC = (upper ? s_wsum[w0][1] : 0u) + iC - sC;  // complements of leaders before 2tl
+    const uint64_t tgt = (uint64_t)rho_keys;
+    // (rank, keys before it, keys through it)
+    const uint32_t rk[4] = {(uint32_t)(2 * tl), (uint32_t)(2 * tl + 1), (uint32_t)(NC - 1 - 2 * tl),
+                            (uint32_t)(NC - 2 - 2 * tl)};
+    const uint32_t bef[4] = {exL, exL + oL[0], TL + TC - exC - oC[0], TL + TC - exC - oC[0] - oC[1]};
+    const uint32_t thr[4] = {oL[0], oL[1], oC[0], oC[1]};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if ((uint64_t)bef[i] < tgt && (uint64_t)bef[i] + thr[i] >= tgt) s_T[half] = (int)rk[i] + 1;
+    __syncthreads();
+    T = s_T[half];
+  }
   // position p = 2*tl + i == rank of leader e[i].id, 255 - p == rank of its complement; write this head's bonus
   // byte of the packed LUT entry of both
   const int chunk = max(1, T / cfg.n_tiers);
@@ -236,12 +285,14 @@ __global__ void __launch_bounds__(QP_THREADS) qprep_kernel(const uint16_t* q, in
 
 }  // namespace
 
-cudaError_t launch_qprep(const pkv_index* ix, const void* q, int T, float* dbg_q_rot, cudaStream_t stream) {
+cudaError_t launch_qprep(const pkv_index* ix, const void* q, int T, int64_t rho_keys, float* dbg_q_rot,
+                         cudaStream_t stream) {
   const Workspace* ws = ix->ws;
   dim3 grid(NB / 2, ix->cfg.n_q_heads, ix->batch);
   ProfScope p_(K_QPREP, stream);
   return pdl_launch(qprep_kernel, grid, dim3(QP_THREADS), 0, stream, static_cast<const uint16_t*>(q), T, ix->dcfg,
-                    ws->lut, ws->rtab, ws->qnorm, ws->qrot, dbg_q_rot, ws->ucount);
+                    ws->lut, ws->rtab, ws->qnorm, ws->qrot, dbg_q_rot, ws->ucount,
+                    rho_keys > 0 ? (const uint32_t*)ix->occ : (const uint32_t*)nullptr, rho_keys);
 }
 
 cudaError_t set_phase_qprep(unsigned long long* p) { return set_phase_ptr_tu(p); }

@@ -42,7 +42,7 @@ class StreamConfig(ctypes.Structure):
 class RetrieveParams(ctypes.Structure):
     _fields_ = [("probes_T", ctypes.c_int32), ("n_cand", ctypes.c_int64), ("top_k", ctypes.c_int32),
                 ("dbg_scores", ctypes.c_void_p), ("dbg_cand", ctypes.c_void_p), ("dbg_est", ctypes.c_void_p),
-                ("dbg_q_rot", ctypes.c_void_p), ("n_global", ctypes.c_int64)]
+                ("dbg_q_rot", ctypes.c_void_p), ("n_global", ctypes.c_int64), ("rho_keys", ctypes.c_int64)]
 
 
 class IndexStats(ctypes.Structure):
@@ -64,6 +64,8 @@ _sigs = {
     "pkv_index_len": [_vp, ctypes.POINTER(_i64)],
     "pkv_index_share_workspace": [_vp, _vp],
     "pkv_index_set_postings": [_vp, _i32, _vp],
+    "pkv_index_set_occupancy": [_vp, _i32, _vp],
+    "pkv_schedule_key_fraction": [_i64, ctypes.POINTER(_i64)],
     "encode_keys": [_vp, _vp, _i64, _i64, _i64, _i64, _vp],
     "append_decode_keys": [_vp, _vp, _i64, _i64, _i64, _i64, _vp],
     "retrieve_topk": [_vp, _vp, ctypes.POINTER(RetrieveParams), _vp, _vp, _vp],
@@ -164,6 +166,13 @@ def schedule(n: int, top_k: int):
     return int(T.value), int(C.value)
 
 
+def schedule_key_fraction(n: int) -> int:
+    """rho_keys = ceil(rho n) for the key-fraction reading of rho (AMB-8b)."""
+    r = _i64(0)
+    _check(_lib.pkv_schedule_key_fraction(n, ctypes.byref(r)))
+    return int(r.value)
+
+
 class Index:
     """Owns a pkv_index (GPU-resident key summaries of the retrieval zone)."""
 
@@ -197,6 +206,10 @@ class Index:
     def set_postings(self, enable: bool = True, stream=None):
         """Inverted-list collision variant: same results, buckets of probed centroids only."""
         _check(_lib.pkv_index_set_postings(self.handle, int(enable), _stream(stream)))
+
+    def set_occupancy(self, enable: bool = True, stream=None):
+        """Per-subspace centroid occupancy counts, needed by retrievals with rho_keys > 0 (AMB-8b)."""
+        _check(_lib.pkv_index_set_occupancy(self.handle, int(enable), _stream(stream)))
 
     def stats(self, stream=None) -> dict:
         """Degenerate-key counters of the current content (AMB-7; synchronises the stream)."""
@@ -247,7 +260,8 @@ def append_decode_keys(index: Index, K: torch.Tensor, t: int | None = None, stre
 
 
 def retrieve_topk(index: Index, q: torch.Tensor, top_k: int, probes_T: int | None = None, n_cand: int | None = None,
-                  n_global: int | None = None, out_idx=None, out_est=None, debug: bool = False, stream=None):
+                  n_global: int | None = None, out_idx=None, out_est=None, debug: bool = False, rho_keys: int = 0,
+                  stream=None):
     """(3) q bf16 [batch, n_q, 128] -> (idx int32 [batch, n_q, k], est f32 [batch, n_q, k], dbg dict|None).
     probes_T / n_cand default to the library schedule on the (global) retrieval length."""
     assert q.dtype == torch.bfloat16 and q.is_contiguous() and q.shape[-1] == D
@@ -260,7 +274,7 @@ def retrieve_topk(index: Index, q: torch.Tensor, top_k: int, probes_T: int | Non
         out_idx = torch.empty(index.batch, index.n_q, top_k, dtype=torch.int32, device=dev)
     if out_est is None:
         out_est = torch.empty(index.batch, index.n_q, top_k, dtype=torch.float32, device=dev)
-    p = RetrieveParams(T, C, top_k, None, None, None, None, 0 if n_global is None else n_global)
+    p = RetrieveParams(T, C, top_k, None, None, None, None, 0 if n_global is None else n_global, rho_keys)
     dbg = None
     if debug:
         nl = len(index)
@@ -306,7 +320,7 @@ def sparse_attend(index: Index, q: torch.Tensor, K: torch.Tensor | None, V: torc
 def retrieve_and_attend(index: Index, q: torch.Tensor, K, V, top_k: int, K_hot=None, V_hot=None,
                         scale: float | None = None, probes_T: int | None = None, n_cand: int | None = None,
                         out_idx=None, out_est=None, out=None, lse=None, strides=None, K_ptr=None, V_ptr=None,
-                        n_global: int | None = None, stream=None):
+                        n_global: int | None = None, rho_keys: int = 0, stream=None):
     """(3)+(4) in one call: retrieval and attention of one decode step and layer, with the hot-row attention
     overlapped with the retrieval and the final top-k fused with the gather/attention. Returns
     (idx, est, out, lse)."""
@@ -331,7 +345,7 @@ def retrieve_and_attend(index: Index, q: torch.Tensor, K, V, top_k: int, K_hot=N
         sb, sh, st = strides
     n_hot = 0 if K_hot is None else K_hot.shape[2]
     scale = 1.0 / np.sqrt(D) if scale is None else scale
-    p = RetrieveParams(T, C, top_k, None, None, None, None, 0 if n_global is None else n_global)
+    p = RetrieveParams(T, C, top_k, None, None, None, None, 0 if n_global is None else n_global, rho_keys)
     _check(_lib.retrieve_and_attend(index.handle, _ptr(q), ctypes.byref(p), _vp(K_ptr), _vp(V_ptr), sb, sh, st,
                                     _ptr(K_hot), _ptr(V_hot), n_hot, scale, _ptr(out_idx), _ptr(out_est), _ptr(out),
                                     _ptr(lse), _stream(stream)))

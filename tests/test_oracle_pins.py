@@ -513,3 +513,93 @@ def test_attention_weights_are_the_softmax():
     assert abs(p.sum() - 1) < 1e-12
     assert np.allclose(attention.attention_weights(q, K[:1], sc), [1.0])
     assert np.allclose(attention.attention_weights(q, np.tile(K[:1], (5, 1)), sc), 0.2)
+
+
+# ---------------------------------------------------------------- P15 key-fraction reading of rho (AMB-8b, f4)
+def _rand_ids(seed, n, B=16, skew=True):
+    """Centroid ids with a skewed occupancy (a few crowded centroids, many empty ones), like LLM keys."""
+    rng = np.random.default_rng(seed)
+    if not skew:
+        return rng.integers(0, 256, size=(n, B))
+    p = rng.dirichlet(np.full(256, 0.08), size=B)
+    return np.stack([rng.choice(256, size=n, p=p[b]) for b in range(B)], axis=1)
+
+
+def test_p15_occupancy_is_a_count():
+    ids = _rand_ids(150, 700)
+    occ = coarse.occupancy(ids)
+    assert occ.shape == (16, 256) and np.all(occ.sum(axis=1) == 700)
+    for b in (0, 7, 15):  # numpy's own counter as the independent check
+        assert np.array_equal(occ[b], np.bincount(ids[:, b], minlength=256))
+
+
+@pytest.mark.parametrize("rho_keys", [1, 37, 350, 699, 700])
+def test_p15_probes_equal_bruteforce_key_sort(rho_keys):
+    """Independent formulation: sort the KEYS by the rank of their centroid; the rho_keys-th key's centroid is
+    the last probed one, so T_b = its rank + 1 — whole centroids, the minimal prefix of the centroid order."""
+    ids = _rand_ids(151, 700)
+    occ = coarse.occupancy(ids)
+    rng = np.random.default_rng(152)
+    for b in range(16):
+        y = _bf16(rng.normal(size=8))
+        rank = codebook.rank_centroids(codebook.centroid_scores(y))
+        key_ranks = np.sort(rank[ids[:, b]])
+        T = coarse.key_fraction_probes(rank, occ[b], rho_keys)
+        assert T == key_ranks[rho_keys - 1] + 1
+        probed = rank < T
+        assert occ[b][probed].sum() >= rho_keys                      # covers the target ...
+        last = np.argmax(rank == T - 1)
+        assert occ[b][probed].sum() - occ[b][last] < rho_keys        # ... and is minimal
+        assert occ[b][last] > 0                                      # a prefix never ends on an empty centroid
+
+
+def test_p15_uniform_occupancy_reduces_to_centroid_fraction():
+    """With every centroid holding the same number of keys, a key fraction is a centroid fraction:
+    rho_keys = T * m keys -> exactly T probes, and the bonus tables equal the AMB-8 (centroid) reading."""
+    m = 3
+    rng = np.random.default_rng(153)
+    ids = np.stack([rng.permutation(np.repeat(np.arange(256), m)) for _ in range(16)], axis=1)
+    occ = coarse.occupancy(ids)
+    q = _bf16(rng.normal(size=128))
+    for T in (1, 5, 26, 39, 256):
+        bonus_k, Tb = coarse.query_bonus_tables_keys(q, SB, occ, T * m)
+        assert np.all(Tb == T)
+        assert np.array_equal(bonus_k, coarse.query_bonus_tables(q, SB, T))
+
+
+def test_p15_key_fraction_scores_equal_naive_per_key_loop():
+    """The key-mode scores from the bonus tables equal a naive per-key loop that ranks each key's centroid against
+    all 256 and counts how many keys' centroids rank strictly before it (pure Python, tiny n)."""
+    n, rho_keys = 300, 45
+    ids = _rand_ids(154, n)
+    rng = np.random.default_rng(155)
+    q = _bf16(rng.normal(size=128))
+    occ = coarse.occupancy(ids)
+    bonus, Tb = coarse.query_bonus_tables_keys(q, SB, occ, rho_keys)
+    score = coarse.collision_scores(ids, bonus)
+    y = transform.rotate_unscaled(q, SB)
+    W = codebook.all_centroids(8) * np.sqrt(8)
+    naive = np.zeros(n, dtype=np.int64)
+    for b in range(16):
+        sc = W @ y[8 * b:8 * b + 8]
+        rk = [int(np.sum(sc > sc[c]) + np.sum((sc == sc[c]) & (np.arange(256) < c))) for c in range(256)]
+        # T_b by scanning ranks: keys held by centroids of rank < r
+        held_before = {r: sum(1 for i in range(n) if rk[ids[i, b]] < r) for r in range(257)}
+        T = min(r for r in range(257) if held_before[r] >= rho_keys)
+        assert T == Tb[b]
+        chunk = max(1, T // 6)
+        for i in range(n):
+            r = rk[ids[i, b]]
+            if r < T:
+                naive[i] += (6, 5, 4, 3, 2, 1)[min(r // chunk, 5)]
+    assert np.array_equal(score, naive)
+    # every subspace hands a non-zero bonus to at least rho_keys keys (P:477's top-rho fraction)
+    for b in range(16):
+        assert np.sum(bonus[b][ids[:, b]] > 0) >= rho_keys
+
+
+def test_p15_key_fraction_target_schedule():
+    assert coarse.key_fraction_target(0) == 0
+    assert coarse.key_fraction_target(130800) == 13080          # rho = 10% at 128K (S:329 row 60000)
+    assert coarse.key_fraction_target(1048304) == 83865         # ceil(0.08 * 1048304)
+    assert coarse.key_fraction_target(4096) == 615              # ceil(0.15 * 4096)

@@ -10,7 +10,7 @@ import pytest
 import torch
 
 import synth
-from oracle import attention, coarse, pipeline, sharded
+from oracle import attention, coarse, pipeline, rerank, sharded
 from tests.gpu_helpers import (ATT_ABS, SB, bf16_f64, check_attention, check_encode, check_topk, oracle_meta,
                                oracle_retrieval, w16_bound)
 
@@ -695,3 +695,64 @@ def test_hot_rows_capacity_validated(pkv):
     assert pkv._lib.retrieve_and_attend_rows(*args(64, 32)) == pkv.PKV_ERR_INVALID_ARG
     assert pkv._lib.retrieve_and_attend_rows(*args(32, 64)) == pkv.PKV_OK
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("rho_mode", ["schedule", "one", "all"])
+def test_key_fraction_reading_of_rho(pkv, rho_mode):
+    """rho as a fraction of KEYS. The occupancy counts are built at
+    pkv_index_set_occupancy and kept by a later append; scores and candidate sets bit-exact against the oracle's
+    key-mode bonus tables, estimates / top-k / attention at the usual bars."""
+    batch, n_q, n_kv, n, n_app, k = 2, 8, 2, 9000, 1500, 100
+    K, q, V = make_problem(201, batch, n_q, n_kv, n)
+    cfg = pkv.config_init(n_q, n_kv, SB)
+    ix = pkv.Index(cfg, batch, n)
+    pkv.encode_keys(ix, K[:, :, :n - n_app].contiguous())
+    ix.set_occupancy(True)
+    pkv.append_decode_keys(ix, K[:, :, n - n_app:].contiguous())
+    rho = {"schedule": pkv.schedule_key_fraction(n), "one": 1, "all": n}[rho_mode]
+    idx, est, dbg = pkv.retrieve_topk(ix, q, k, debug=True, rho_keys=rho)
+    out32 = torch.full((batch, n_q, 128), float("nan"), device="cuda")
+    ix.set_debug_output(out32)
+    idx2, est2, out, lse = pkv.retrieve_and_attend(ix, q, K, V, k, rho_keys=rho)
+    ix.set_debug_output(None)
+    torch.cuda.synchronize()
+    assert torch.equal(idx, idx2) and torch.equal(est, est2)
+    C = dbg["C"]
+    G = n_q // n_kv
+    for b in range(batch):
+        for g in range(n_kv):
+            Kf = bf16_f64(K[b, g])
+            meta = oracle_meta(Kf)
+            occ = coarse.occupancy(meta["ids"])
+            for hh in range(G):
+                h = g * G + hh
+                qf = bf16_f64(q[b, h])
+                bonus, Tb = coarse.query_bonus_tables_keys(qf, SB, occ, rho)
+                score = coarse.collision_scores(meta["ids"], bonus)
+                assert np.array_equal(dbg["scores"][b, h].cpu().numpy().astype(np.int64), score), "scores"
+                cand = coarse.bucket_topk(score, C)
+                cg = dbg["cand"][b, h].cpu().numpy()
+                assert np.array_equal(np.sort(cg[cg >= 0]), cand), "candidate set"
+                qt, qn = rerank.rotated_unit_query(qf, SB)
+                eo = rerank.estimate(meta, cand, qt, qn)
+                check_topk(idx[b, h].cpu().numpy(), est[b, h].cpu().numpy(), cand, eo,
+                           dict(zip(range(n), meta["knorm"].tolist())), qn, k)
+                o, l = pipeline.attend(qf, Kf, bf16_f64(V[b, g]), idx[b, h].cpu().numpy())
+                check_attention(out[b, h].float().cpu().numpy(), o, out32[b, h].cpu().numpy(), lse[b, h], l)
+                if rho_mode == "all":  # every key is covered: the last probed centroid is the worst-ranked used one
+                    assert np.all(Tb >= 1)
+
+
+def test_key_fraction_needs_occupancy(pkv):
+    K, q, V = make_problem(202, 1, 4, 1, 500, plant=False)
+    ix = pkv.Index(pkv.config_init(4, 1, SB), 1, 500)
+    pkv.encode_keys(ix, K)
+    with pytest.raises(pkv.PkvError):
+        pkv.retrieve_topk(ix, q, 10, rho_keys=50)  # occupancy not enabled
+    ix.set_occupancy(True)
+    with pytest.raises(pkv.PkvError):
+        pkv.retrieve_topk(ix, q, 10, rho_keys=501)  # more keys than the zone holds
+    pkv.retrieve_topk(ix, q, 10, rho_keys=50)
+    ix.set_occupancy(False)
+    with pytest.raises(pkv.PkvError):
+        pkv.retrieve_topk(ix, q, 10, rho_keys=50)
