@@ -489,6 +489,7 @@ pkv_status pkv_index_share_workspace(pkv_index* ix, pkv_index* donor) {
 
 pkv_status encode_keys(pkv_index* ix, const void* K, int64_t sb, int64_t sh, int64_t st, int64_t n,
                        cudaStream_t stream) {
+  NvtxRange nvtx_("pkv:encode_keys");
   if (!ix) return set_error(PKV_ERR_INVALID_ARG, "encode_keys: null index");
   if (n < 0) return set_error(PKV_ERR_INVALID_ARG, "encode_keys: n < 0");
   if (n > ix->cap) return set_error(PKV_ERR_CAPACITY, "encode_keys: n exceeds capacity");
@@ -514,6 +515,7 @@ pkv_status encode_keys(pkv_index* ix, const void* K, int64_t sb, int64_t sh, int
 
 pkv_status append_decode_keys(pkv_index* ix, const void* K, int64_t sb, int64_t sh, int64_t st, int64_t t,
                               cudaStream_t stream) {
+  NvtxRange nvtx_("pkv:append_decode_keys");
   if (!ix) return set_error(PKV_ERR_INVALID_ARG, "append_decode_keys: null index");
   if (t < 0) return set_error(PKV_ERR_INVALID_ARG, "append_decode_keys: t < 0");
   if (ix->n + t > ix->cap) return set_error(PKV_ERR_CAPACITY, "append_decode_keys: capacity exceeded");
@@ -546,6 +548,7 @@ pkv_status pkv_index_export(const pkv_index* ix, int64_t start, int64_t count, u
 
 pkv_status retrieve_topk(pkv_index* ix, const void* q, const pkv_retrieve_params* p, int32_t* out_idx, float* out_est,
                          cudaStream_t stream) {
+  NvtxRange nvtx_("pkv:retrieve_topk");
   if (!ix) return set_error(PKV_ERR_INVALID_ARG, "retrieve_topk: null index");
   if (!p) return set_error(PKV_ERR_INVALID_ARG, "retrieve_topk: null params");
   const int64_t n_global = ix->comm ? comm_global_n(ix, p) : ix->n;
@@ -586,6 +589,7 @@ pkv_status retrieve_topk(pkv_index* ix, const void* q, const pkv_retrieve_params
 pkv_status sparse_attend(pkv_index* ix, const void* q, const void* K, const void* V, int64_t sb, int64_t sh, int64_t st,
                          const int32_t* idx, int32_t k, const void* K_hot, const void* V_hot, int32_t n_hot,
                          float scale, void* out, float* lse, cudaStream_t stream) {
+  NvtxRange nvtx_("pkv:sparse_attend");
   if (!ix || !q || !out) return set_error(PKV_ERR_INVALID_ARG, "sparse_attend: null pointer");
   if (k < 0 || n_hot < 0 || k > MAX_TOPK) return set_error(PKV_ERR_INVALID_ARG, "sparse_attend: bad k / n_hot");
   if (k > 0) {
@@ -633,7 +637,25 @@ pkv_status retrieve_and_attend_rows(pkv_index* ix, const void* q, const pkv_retr
                                     const void* V, int64_t sb, int64_t sh, int64_t st, const void* K_hot,
                                     const void* V_hot, int32_t n_hot, int32_t hot_rows, float scale, int32_t* out_idx,
                                     float* out_est, void* out, float* lse, cudaStream_t stream) {
+  return pkv::retrieve_and_attend_rows_after(ix, q, p, K, V, sb, sh, st, K_hot, V_hot, n_hot, hot_rows, scale,
+                                             out_idx, out_est, out, lse, nullptr, stream);
+}
+
+}  // extern "C"
+
+namespace pkv {
+
+// retrieve_and_attend_rows whose row gather (the last kernel) also waits for `attend_after` (may be null): the
+// streaming manager's asynchronous offload of evicted K/V rows must land in the store before those rows can be
+// gathered, while query prep, scan, select and rerank of the same step run alongside it.
+pkv_status retrieve_and_attend_rows_after(pkv_index* ix, const void* q, const pkv_retrieve_params* p, const void* K,
+                                          const void* V, int64_t sb, int64_t sh, int64_t st, const void* K_hot,
+                                          const void* V_hot, int32_t n_hot, int32_t hot_rows, float scale,
+                                          int32_t* out_idx, float* out_est, void* out, float* lse,
+                                          cudaEvent_t attend_after, cudaStream_t stream) {
+  NvtxRange nvtx_("pkv:retrieve_and_attend");
   if (!ix) return set_error(PKV_ERR_INVALID_ARG, "retrieve_and_attend: null index");
+  if (attend_after && ix->comm) return set_error(PKV_ERR_UNSUPPORTED, "retrieve_and_attend: ordered gather when sharded");
   if (ix->comm) {  // sequence-sharded: one fused T+A exchange when k fits its slots, else the two calls
     if (hot_rows != n_hot) return set_error(PKV_ERR_UNSUPPORTED, "retrieve_and_attend: strided hot rows when sharded");
     if (p && p->top_k <= TA_MAXK && out)
@@ -664,6 +686,7 @@ pkv_status retrieve_and_attend_rows(pkv_index* ix, const void* q, const pkv_retr
   if (st0 != PKV_OK) return st0;
   // The hot rows (sink + local + buffer) are attended by the last kernel: in the cluster top-k kernel ahead of
   // its dependency wait (overlapping the rerank kernel's drain); after the segmented top-k for very long lists.
+  if (attend_after) PKV_CUDA(cudaStreamWaitEvent(stream, attend_after, 0), "wait for the offload");
   if (!clustered) {
     PKV_CUDA(launch_topk(ix, p->n_cand, p->top_k, out_idx, out_est, p->top_k, stream), "topk");
     PKV_CUDA(launch_topk_attend_rows(ix, p->top_k, out_idx, q, K, V, sb, sh, st, scale, K_hot, V_hot, n_hot, hot_rows,
@@ -677,6 +700,10 @@ pkv_status retrieve_and_attend_rows(pkv_index* ix, const void* q, const pkv_retr
   if (p->dbg_cand || p->dbg_est) PKV_CUDA(launch_dbg_cand(ix, p->n_cand, p->dbg_cand, p->dbg_est, stream), "dbg cand");
   return PKV_OK;
 }
+
+}  // namespace pkv
+
+extern "C" {
 
 // ---------------------------------------------------------------- single-process sharded emulation
 namespace {

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <atomic>
 #include <cstdint>
@@ -108,6 +109,15 @@ struct pkv_index {
 
 namespace pkv {
 
+// NVTX range around one public call (nsys / ncu timelines: "pkv:retrieve_and_attend" etc.); header-only NVTX 3,
+// a no-op unless a tool is attached
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 // Kernel kinds for launch accounting / optional event timing (profile.cpp)
 enum KernelKind { K_ENCODE, K_QPREP, K_SCAN, K_SELECT, K_UNUSED4, K_RERANK, K_TOPK, K_MERGE, K_ATTEND,
                   K_COMBINE, K_HEADHIST, K_EXPORT, K_DEBUG, K_NUM_KINDS };
@@ -129,6 +139,11 @@ cudaError_t set_phase_attend(unsigned long long* p);
 cudaError_t set_phase_encode(unsigned long long* p);
 
 // Shared validation / hot-row-only attention (api.cpp), used by the streaming manager (stream.cpp)
+pkv_status retrieve_and_attend_rows_after(pkv_index* ix, const void* q, const pkv_retrieve_params* p, const void* K,
+                                          const void* V, int64_t sb, int64_t sh, int64_t st, const void* K_hot,
+                                          const void* V_hot, int32_t n_hot, int32_t hot_rows, float scale,
+                                          int32_t* out_idx, float* out_est, void* out, float* lse,
+                                          cudaEvent_t attend_after, cudaStream_t stream);
 pkv_status check_retrieve(const pkv_index* ix, const void* q, const pkv_retrieve_params* p, int64_t n_global,
                           const int32_t* out_idx, const float* out_est);
 // Attention over the hot rows alone (empty retrieval zone): out_idx/out_est [batch][n_q][top_k] get -1 / -inf.

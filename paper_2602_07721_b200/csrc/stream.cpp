@@ -31,6 +31,14 @@ struct pkv_stream {
   uint16_t* Vs = nullptr;
   void* Ks_host = nullptr;  // host allocation when offloaded
   void* Vs_host = nullptr;
+  // asynchronous offload of evicted rows ("offloading the corresponding full-precision KV pairs
+  // asynchronously"): a flush copies the evicted rows to device staging buffers on the caller's stream, a side
+  // stream moves them to the store (over the host link when offloaded) while the step's retrieval kernels run,
+  // and only the step's row gather waits for it (ev_join)
+  uint16_t* Kst = nullptr;  // staging [batch][n_kv][update_size][128]
+  uint16_t* Vst = nullptr;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 namespace {
@@ -93,6 +101,11 @@ pkv_status pkv_stream_create(pkv_index* ix, const pkv_stream_config* c, pkv_stre
   if (e == cudaSuccess) e = cudaMalloc(&s->Vh, hot);
   if (e == cudaSuccess && c->local_size > 0)
     e = cudaMalloc(&s->scratch, (size_t)heads * c->local_size * ROWB);
+  if (e == cudaSuccess) e = cudaMalloc(&s->Kst, (size_t)heads * c->update_size * ROWB);
+  if (e == cudaSuccess) e = cudaMalloc(&s->Vst, (size_t)heads * c->update_size * ROWB);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming);
   if (e == cudaSuccess) {
     if (c->offload_host) {
       e = cudaHostAlloc(&s->Ks_host, store, cudaHostAllocMapped);
@@ -118,6 +131,12 @@ pkv_status pkv_stream_destroy(pkv_stream* s) {
   cudaFree(s->Kh);
   cudaFree(s->Vh);
   cudaFree(s->scratch);
+  if (s->side) cudaStreamSynchronize(s->side);  // an offload still in flight finishes before its buffers go
+  cudaFree(s->Kst);
+  cudaFree(s->Vst);
+  if (s->ev_fork) cudaEventDestroy(s->ev_fork);
+  if (s->ev_join) cudaEventDestroy(s->ev_join);
+  if (s->side) cudaStreamDestroy(s->side);
   if (s->cfg.offload_host) {
     cudaFreeHost(s->Ks_host);
     cudaFreeHost(s->Vs_host);
@@ -131,6 +150,7 @@ pkv_status pkv_stream_destroy(pkv_stream* s) {
 
 pkv_status pkv_stream_prefill(pkv_stream* s, const void* K, const void* V, int64_t sb, int64_t sh, int64_t st,
                               int64_t n_tokens, cudaStream_t stream) {
+  NvtxRange nvtx_("pkv:stream_prefill");
   if (!s || !K || !V) return set_error(PKV_ERR_INVALID_ARG, "pkv_stream_prefill: null pointer");
   pkv_index* ix = s->ix;
   const int sink = s->cfg.sink;
@@ -165,6 +185,7 @@ pkv_status pkv_stream_prefill(pkv_stream* s, const void* K, const void* V, int64
 pkv_status pkv_stream_decode(pkv_stream* s, const void* q, const void* k_new, const void* v_new,
                              const pkv_retrieve_params* params, float scale, int32_t* out_idx, float* out_est,
                              void* out, float* lse, cudaStream_t stream) {
+  NvtxRange nvtx_("pkv:stream_decode");
   // Every argument is validated, for the state this step will produce, before anything is enqueued or changed:
   // a failing call leaves the regions and the index as they were (header contract).
   if (!s || !q || !k_new || !v_new || !params || !out_idx || !out_est || !out)
@@ -213,13 +234,25 @@ pkv_status pkv_stream_decode(pkv_stream* s, const void* q, const void* k_new, co
     // (2) evict the oldest rows of Local U Update into Retrieval: encode + append (iii), K/V to the store (i)
     const int64_t n0 = ix->n;
     if (evict > 0) {
-      pkv_status r = append_decode_keys(ix, s->Kh + (int64_t)sink * D, hb, (int64_t)s->rows * D, D, evict, stream);
-      if (r != PKV_OK) return r;
-      e = copy_rows(s->Ks, ix->cap, n0, s->Kh + (int64_t)sink * D, hb, (int64_t)s->rows * D, D, evict, batch, n_kv,
+      // (i) evicted rows -> staging (device, this stream), then -> the store on the side stream, asynchronously
+      const int64_t sh_st = (int64_t)U * D, sb_st = (int64_t)n_kv * U * D;
+      e = copy_rows(s->Kst, U, 0, s->Kh + (int64_t)sink * D, hb, (int64_t)s->rows * D, D, evict, batch, n_kv,
                     stream);
       if (e == cudaSuccess)
-        e = copy_rows(s->Vs, ix->cap, n0, s->Vh + (int64_t)sink * D, hb, (int64_t)s->rows * D, D, evict, batch,
-                      n_kv, stream);
+        e = copy_rows(s->Vst, U, 0, s->Vh + (int64_t)sink * D, hb, (int64_t)s->rows * D, D, evict, batch, n_kv,
+                      stream);
+      if (e == cudaSuccess) e = cudaEventRecord(s->ev_fork, stream);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(s->side, s->ev_fork, 0);
+      if (e == cudaSuccess) e = copy_rows(s->Ks, ix->cap, n0, s->Kst, sb_st, sh_st, D, evict, batch, n_kv, s->side);
+      if (e == cudaSuccess) e = copy_rows(s->Vs, ix->cap, n0, s->Vst, sb_st, sh_st, D, evict, batch, n_kv, s->side);
+      if (e == cudaSuccess) e = cudaEventRecord(s->ev_join, s->side);
+      if (e != cudaSuccess) return cuda_status(e, "pkv_stream_decode(offload)");
+      // (iii) encode and index the evicted keys (read in place, before the Local shift below)
+      pkv_status r = append_decode_keys(ix, s->Kh + (int64_t)sink * D, hb, (int64_t)s->rows * D, D, evict, stream);
+      if (r != PKV_OK) {
+        cudaStreamWaitEvent(stream, s->ev_join, 0);  // join the side stream (capture-safe) before reporting
+        return r;
+      }
     }
     // (3) the newest local_size rows become Local (ii)
     if (e == cudaSuccess && evict > 0 && keep > 0) {
@@ -244,8 +277,12 @@ pkv_status pkv_stream_decode(pkv_stream* s, const void* q, const void* k_new, co
   // empty retrieval zone (prompt <= sink + local_size, no eviction yet) attends the hot rows alone
   if (n_after == 0)
     return attend_hot_only(ix, q, s->Kh, s->Vh, n_hot, s->rows, p.top_k, scale, out_idx, out_est, out, lse, stream);
-  return retrieve_and_attend_rows(ix, q, &p, s->Ks, s->Vs, (int64_t)n_kv * ix->cap * D, ix->cap * D, D, s->Kh, s->Vh,
-                                  n_hot, s->rows, scale, out_idx, out_est, out, lse, stream);
+  const bool offloading = flush && evict > 0;
+  pkv_status r = retrieve_and_attend_rows_after(ix, q, &p, s->Ks, s->Vs, (int64_t)n_kv * ix->cap * D, ix->cap * D, D,
+                                                s->Kh, s->Vh, n_hot, s->rows, scale, out_idx, out_est, out, lse,
+                                                offloading ? s->ev_join : nullptr, stream);
+  if (r != PKV_OK && offloading) cudaStreamWaitEvent(stream, s->ev_join, 0);
+  return r;
 }
 
 pkv_status pkv_stream_state(const pkv_stream* s, int64_t* n_retrieval, int32_t* n_local, int32_t* n_buffer,
