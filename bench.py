@@ -114,6 +114,9 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("PKV_BENCH_GLOO") == "1":  # several ranks per GPU (functional checks, see run_ours)
+        import torch
+        local = local % max(1, torch.cuda.device_count())
     return world, rank, local
 
 
@@ -126,10 +129,16 @@ def run_ours(args):
     pbuild.build()
 
     world, rank, local = dist_env()
+    # PKV_BENCH_GLOO=1: gloo plumbing and every rank on the visible GPU(s) modulo their count — a functional check
+    # of the sharded paths with several ranks on one GPU (peer transport); timings are then meaningless
+    gloo = os.environ.get("PKV_BENCH_GLOO") == "1"
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if gloo:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     res = measure(args, args.config)
     # the metric names both contexts: the default run also measures the 1M configuration (BASELINE configs[4],
     # K/V in pinned host memory) in the same process and reports it as configs["1m"]
@@ -207,7 +216,16 @@ def measure(args, config: str) -> dict:
                            out=torch.empty(batch, N_Q, D, dtype=torch.bfloat16, device=dev),
                            lse=torch.empty(batch, N_Q, dtype=torch.float32, device=dev)))
     torch.cuda.synchronize()
-    if world > 1:
+    if world > 1 and args.transport == "peer":  # one-shot all-gather kernels over NVLink peer memory
+        handle, _ = layers[0]["ix"].comm_init_peer(rank, world, lo)
+        handles = [None] * world
+        dist.all_gather_object(handles, handle)
+        layers[0]["ix"].comm_peer_connect(handles)
+        pkv.comm_set_global_len(layers[0]["ix"], n)
+        for ly in layers[1:]:
+            pkv.comm_share(ly["ix"], layers[0]["ix"], lo)
+        dist.barrier()
+    elif world > 1:
         uid = [pkv.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         pkv.comm_init(layers[0]["ix"], uid[0], rank, world, lo)
@@ -311,7 +329,7 @@ def measure(args, config: str) -> dict:
             dist.barrier()
         ms = a.elapsed_time(b)
         if world > 1:
-            t = torch.tensor([ms], device=dev)
+            t = torch.tensor([ms], device="cpu" if dist.get_backend() == "gloo" else dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
         return ms
@@ -465,6 +483,7 @@ def measure(args, config: str) -> dict:
             "config": {"workload": cfgw["workload"], "batch": batch, "context": ctx, "retrieval_n": n,
                        "hot_rows": n_hot, "top_k": TOP_K, "probes_T": T, "n_cand": C, "layers": L,
                        "parallelism": f"seq-shard{world}" if world > 1 else "single",
+                       "exchange": (args.transport if world > 1 else None),
                        "l2": "inputs > L2: 32 layer-distinct indices + K/V touched per step",
                        "rerank_weights": "fp16 (96 B records)" if args.w16 else "fp32 (128 B records)",
                        "collision_scan": "inverted lists" if args.inverted else "dense",
@@ -636,6 +655,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--w16", action="store_true", help="fp16 rerank weights (96-byte records, AMB-20 / SURVEY f2)")
     ap.add_argument("--inverted", action="store_true", help="inverted-list collision scan (SURVEY f4)")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "peer"],
+                    help="sharded exchanges (N > 1): NCCL all-gathers, or one-shot peer-memory all-gather kernels")
     ap.add_argument("--key-fraction", action="store_true",
                     help="rho as a fraction of keys (AMB-8b, SURVEY f4): per-subspace probes from occupancy counts")
     ap.add_argument("--k-hbm", action="store_true",

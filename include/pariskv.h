@@ -316,6 +316,24 @@ pkv_status pkv_comm_init(pkv_index* index, const uint8_t id[128], int32_t rank, 
 typedef int32_t (*pkv_host_allgather_fn)(void* ctx, void* buf, size_t bytes_per_rank, int32_t rank, int32_t world);
 pkv_status pkv_comm_init_host(pkv_index* index, pkv_host_allgather_fn fn, void* ctx, int32_t rank, int32_t world,
                               int64_t shard_offset);
+/* Peer transport: the exchanges become one-shot all-gather kernels over peer memory — each rank
+ * stores its slot straight into every peer's symmetric "arena" (NVLink stores on an NVSwitch system), raises
+ * per-CTA flags there and waits for the peers' flags in its own arena: no NCCL call and no host involvement per
+ * exchange, stream-ordered and CUDA-graph capturable (peer.cu). Two steps, both on every rank:
+ *   pkv_comm_init_peer: allocates this rank's arena (arena_bytes >= 8192 + 2 * world * the largest exchange
+ *     message; 64 MB covers batch 8 x 32 query heads) and attaches the communicator; returns the arena's
+ *     CUDA IPC handle (ipc_handle, 64 bytes, may be NULL) and its device pointer (arena, may be NULL);
+ *   pkv_comm_peer_connect: opens the peers' IPC handles (ipc_handles = world x 64 bytes, this rank's ignored),
+ *     for ranks in different processes; or pkv_comm_peer_connect_local with the world arena pointers, for
+ *     ranks in one process.
+ * The global retrieval length is not exchanged at attach: set it with pkv_comm_set_global_len or pass
+ * pkv_retrieve_params.n_global. Every rank must issue the same sequence of sharded calls (the exchanges
+ * pair up by order); ranks that share one GPU must run their streams concurrently and keep grids small enough
+ * to co-reside (the exchange kernel of one rank spins until the others arrive). */
+pkv_status pkv_comm_init_peer(pkv_index* index, int32_t rank, int32_t world, int64_t shard_offset,
+                              size_t arena_bytes, uint8_t ipc_handle[64], void** arena);
+pkv_status pkv_comm_peer_connect(pkv_index* index, const uint8_t* ipc_handles);
+pkv_status pkv_comm_peer_connect_local(pkv_index* index, void* const* arenas);
 /* Global retrieval length recorded by the communicator (validation of n_cand in sharded calls). pkv_comm_init
  * and pkv_comm_init_host set it to the sum of the ranks' lengths at attach time; after appends on any rank the
  * caller updates it here on every rank, or passes pkv_retrieve_params.n_global per call. */

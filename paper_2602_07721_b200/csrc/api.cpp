@@ -869,6 +869,26 @@ pkv_status pkv_comm_init(pkv_index* ix, const uint8_t id[128], int32_t rank, int
   return comm_init(ix, id, rank, world, shard_offset);
 }
 
+pkv_status pkv_comm_init_peer(pkv_index* ix, int32_t rank, int32_t world, int64_t shard_offset, size_t arena_bytes,
+                              uint8_t ipc_handle[64], void** arena) {
+  if (!ix || world < 1 || world > MAX_RANKS || rank < 0 || rank >= world || shard_offset < 0)
+    return set_error(PKV_ERR_INVALID_ARG, "pkv_comm_init_peer: bad arguments (world must be in [1, 8])");
+  DeviceGuard g(ix->device);
+  return comm_init_peer(ix, rank, world, shard_offset, arena_bytes, ipc_handle, arena);
+}
+
+pkv_status pkv_comm_peer_connect(pkv_index* ix, const uint8_t* ipc_handles) {
+  if (!ix || !ipc_handles) return set_error(PKV_ERR_INVALID_ARG, "pkv_comm_peer_connect: null pointer");
+  DeviceGuard g(ix->device);
+  return comm_peer_connect(ix, ipc_handles, nullptr);
+}
+
+pkv_status pkv_comm_peer_connect_local(pkv_index* ix, void* const* arenas) {
+  if (!ix || !arenas) return set_error(PKV_ERR_INVALID_ARG, "pkv_comm_peer_connect_local: null pointer");
+  DeviceGuard g(ix->device);
+  return comm_peer_connect(ix, nullptr, arenas);
+}
+
 pkv_status pkv_comm_init_host(pkv_index* ix, pkv_host_allgather_fn fn, void* ctx, int32_t rank, int32_t world,
                               int64_t shard_offset) {
   if (!ix || !fn || world < 1 || world > MAX_RANKS || rank < 0 || rank >= world || shard_offset < 0)

@@ -7,6 +7,8 @@
 //   host  (pkv_comm_init_host): the caller's host all-gather (e.g. a gloo process group): the rank's slot is
 //         copied to pinned host memory, the stream synchronised, the callback run, and all slots copied back.
 //         Synchronous, not capturable — for CPU process groups, tests, and ranks that share one GPU.
+//   peer  (pkv_comm_init_peer + pkv_comm_peer_connect[_local]): a one-shot all-gather kernel that stores the
+//         rank's slot straight into every peer's symmetric arena over NVLink (peer.cu).
 #include <nccl.h>
 
 #include <cstring>
@@ -26,7 +28,17 @@ struct Comm {
   int rank = 0, world = 1;
   int64_t global_n = -1;
   int refs = 1;
+  // peer transport
+  char* arena = nullptr;            // this rank's symmetric arena (cudaMalloc)
+  size_t arena_bytes = 0;
+  char* peers[MAX_RANKS] = {};      // every rank's arena as seen from this process (peers[rank] == arena)
+  bool opened[MAX_RANKS] = {};      // peers[r] came from cudaIpcOpenMemHandle
+  bool connected = false;
 };
+
+cudaError_t launch_peer_allgather(char* const* arenas, int rank, int world, uint32_t* buf, size_t words, size_t half,
+                                  cudaStream_t stream);
+size_t peer_header_bytes();
 
 static pkv_status nccl_status(ncclResult_t r, const char* what) {
   if (r == ncclSuccess) return PKV_OK;
@@ -44,6 +56,15 @@ pkv_status comm_unique_id(uint8_t out[128]) {
 }
 
 static pkv_status raw_allgather(Comm* c, void* buf, size_t bytes, cudaStream_t stream) {
+  if (c->arena) {
+    if (!c->connected) return set_error(PKV_ERR_INVALID_ARG, "peer exchange: pkv_comm_peer_connect first");
+    const size_t half = (c->arena_bytes - peer_header_bytes()) / 2;
+    if ((bytes & 3) || bytes * c->world > half)
+      return set_error(PKV_ERR_CAPACITY, "peer exchange: message larger than the arena (pkv_comm_init_peer)");
+    return cuda_status(launch_peer_allgather(c->peers, c->rank, c->world, static_cast<uint32_t*>(buf), bytes / 4, half,
+                                             stream),
+                       "peer all-gather");
+  }
   if (c->comm)
     return nccl_status(ncclAllGather(static_cast<char*>(buf) + c->rank * bytes, buf, bytes, ncclChar, c->comm, stream),
                        "ncclAllGather");
@@ -131,9 +152,59 @@ pkv_status comm_init_host(pkv_index* ix, pkv_host_allgather_fn fn, void* ctx, in
   return PKV_OK;
 }
 
+pkv_status comm_init_peer(pkv_index* ix, int rank, int world, int64_t shard_offset, size_t arena_bytes,
+                          uint8_t ipc_handle[64], void** arena_out) {
+  if (arena_bytes < peer_header_bytes() + 2 * 4096)
+    return set_error(PKV_ERR_INVALID_ARG, "pkv_comm_init_peer: arena too small");
+  Comm* c = new Comm();
+  c->rank = rank;
+  c->world = world;
+  c->arena_bytes = arena_bytes;
+  cudaError_t e = cudaMalloc(&c->arena, arena_bytes);
+  if (e == cudaSuccess) e = cudaMemset(c->arena, 0, peer_header_bytes());  // flags and epochs start at 0
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  cudaIpcMemHandle_t h{};
+  if (e == cudaSuccess && ipc_handle) e = cudaIpcGetMemHandle(&h, c->arena);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    comm_destroy(c);
+    return cuda_status(e, "pkv_comm_init_peer");
+  }
+  if (ipc_handle) std::memcpy(ipc_handle, &h, 64);
+  if (arena_out) *arena_out = c->arena;
+  c->peers[rank] = c->arena;
+  attach(ix, c, shard_offset);
+  return PKV_OK;
+}
+
+pkv_status comm_peer_connect(pkv_index* ix, const uint8_t* handles, void* const* arenas) {
+  Comm* c = ix->comm;
+  if (!c || !c->arena) return set_error(PKV_ERR_INVALID_ARG, "pkv_comm_peer_connect: pkv_comm_init_peer first");
+  for (int r = 0; r < c->world; ++r) {
+    if (r == c->rank) continue;
+    if (arenas) {
+      c->peers[r] = static_cast<char*>(arenas[r]);
+    } else {
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, handles + 64 * r, 64);
+      void* p = nullptr;
+      cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess) return cuda_status(e, "pkv_comm_peer_connect: cudaIpcOpenMemHandle");
+      c->peers[r] = static_cast<char*>(p);
+      c->opened[r] = true;
+    }
+    if (!c->peers[r]) return set_error(PKV_ERR_INVALID_ARG, "pkv_comm_peer_connect: null peer arena");
+  }
+  c->connected = true;
+  return PKV_OK;
+}
+
 void comm_destroy(Comm* c) {
   if (!c) return;
   if (--c->refs > 0) return;
+  for (int r = 0; r < MAX_RANKS; ++r)
+    if (c->opened[r]) cudaIpcCloseMemHandle(c->peers[r]);
+  if (c->arena) cudaFree(c->arena);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->stage) cudaFreeHost(c->stage);
   delete c;

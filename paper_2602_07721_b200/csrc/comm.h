@@ -9,6 +9,9 @@ pkv_status comm_unique_id(uint8_t out[128]);
 pkv_status comm_init(pkv_index* ix, const uint8_t id[128], int rank, int world, int64_t shard_offset);
 pkv_status comm_init_host(pkv_index* ix, pkv_host_allgather_fn fn, void* ctx, int rank, int world,
                           int64_t shard_offset);
+pkv_status comm_init_peer(pkv_index* ix, int rank, int world, int64_t shard_offset, size_t arena_bytes,
+                          uint8_t ipc_handle[64], void** arena_out);
+pkv_status comm_peer_connect(pkv_index* ix, const uint8_t* handles, void* const* arenas);
 void comm_destroy(Comm* c);
 pkv_status comm_share(pkv_index* ix, pkv_index* donor, int64_t shard_offset);
 // In-place all-gather of `slot` u32 words per rank: buf[r*slot .. (r+1)*slot) is rank r's contribution.

@@ -65,6 +65,9 @@ _sigs = {
     "pkv_index_share_workspace": [_vp, _vp],
     "pkv_index_set_postings": [_vp, _i32, _vp],
     "pkv_index_set_occupancy": [_vp, _i32, _vp],
+    "pkv_comm_init_peer": [_vp, _i32, _i32, _i64, ctypes.c_size_t, _vp, ctypes.POINTER(_vp)],
+    "pkv_comm_peer_connect": [_vp, _vp],
+    "pkv_comm_peer_connect_local": [_vp, _vp],
     "pkv_schedule_key_fraction": [_i64, ctypes.POINTER(_i64)],
     "encode_keys": [_vp, _vp, _i64, _i64, _i64, _i64, _vp],
     "append_decode_keys": [_vp, _vp, _i64, _i64, _i64, _i64, _vp],
@@ -206,6 +209,23 @@ class Index:
     def set_postings(self, enable: bool = True, stream=None):
         """Inverted-list collision variant: same results, buckets of probed centroids only."""
         _check(_lib.pkv_index_set_postings(self.handle, int(enable), _stream(stream)))
+
+    def comm_init_peer(self, rank: int, world: int, shard_offset: int, arena_bytes: int = 64 << 20):
+        """Peer transport: allocate this rank's exchange arena; returns (ipc_handle bytes, arena ptr)."""
+        h = (ctypes.c_uint8 * 64)()
+        a = _vp()
+        _check(_lib.pkv_comm_init_peer(self.handle, rank, world, shard_offset, arena_bytes, h, ctypes.byref(a)))
+        return bytes(h), int(a.value)
+
+    def comm_peer_connect(self, handles):
+        """Open the peers' arenas from their IPC handles (list of `world` 64-byte strings, ranks in other processes)."""
+        buf = (ctypes.c_uint8 * (64 * len(handles))).from_buffer_copy(b"".join(handles))
+        _check(_lib.pkv_comm_peer_connect(self.handle, buf))
+
+    def comm_peer_connect_local(self, arenas):
+        """Connect to the other ranks' arenas by device pointer (ranks in this process)."""
+        arr = (ctypes.c_void_p * len(arenas))(*arenas)
+        _check(_lib.pkv_comm_peer_connect_local(self.handle, arr))
 
     def set_occupancy(self, enable: bool = True, stream=None):
         """Per-subspace centroid occupancy counts, needed by retrievals with rho_keys > 0 (AMB-8b)."""
