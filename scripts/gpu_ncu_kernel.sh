@@ -5,7 +5,7 @@ tag=$1; cfg=$2; kre=$3; shift 3
 mkdir -p gpurun_out
 for v in "$@"; do
   lib=$v; [ $v = base ] && lib=
-  PKV_LIB=$lib timeout 900 ncu --set full --import-source on --clock-control none -k regex:"$kre" -s 8 -c 1 \
+  PKV_LIB=$lib timeout 900 ncu --set full --import-source on --clock-control none -k regex:"$kre" -s ${SKIP:-8} -c 1 \
     -o gpurun_out/ncu_${tag}_$v python bench.py --config $cfg --steps 1 --warmup 3 --no-cpu --no-dense --no-1m \
     --layers 4 --no-graph > gpurun_out/ncu_${tag}_$v.log 2>&1
   ncu -i gpurun_out/ncu_${tag}_$v.ncu-rep --page raw --csv > gpurun_out/ncu_${tag}_${v}_raw.csv 2>/dev/null

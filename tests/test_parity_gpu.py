@@ -756,3 +756,4 @@ def test_key_fraction_needs_occupancy(pkv):
     ix.set_occupancy(False)
     with pytest.raises(pkv.PkvError):
         pkv.retrieve_topk(ix, q, 10, rho_keys=50)
+
