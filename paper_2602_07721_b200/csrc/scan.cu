@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(
   __shared__ uint32_t Hg[GMAX][HB];   // global cumulative counts
   __shared__ uint32_t Hl[GMAX][HB];   // this rank's cumulative counts
   __shared__ int s_star[GMAX], gt_local[GMAX], take_local[GMAX];
-  __shared__ int p_gt_off[GMAX], p_tie_off[GMAX], p_take[GMAX], p_eq[GMAX], p_gt_cnt[GMAX];
+  __shared__ int p_base[GMAX], p_take[GMAX], p_eq[GMAX];
   __shared__ uint32_t wcnt[32][2 * GMAX];
   extern __shared__ uint2 sel_list[];  // per-warp compaction lists (VB * 128 entries each), SEL_SMEM bytes
   pdl_trigger();
@@ -361,7 +361,10 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(
       take_local[hh] = take;
     }
     __syncwarp();
-    // A3: this chunk's offsets: prefix of #(> s*) over older chunks, suffix of ties over newer chunks
+    // A3: this chunk's offsets. A head's candidate list holds its selected keys (score > s*, and the taken s*
+    // ties) in key order, chunk after chunk. Ties are handed out newest first, so the chunks after this one take
+    // min(tl, eq_after) of them, this chunk min(eq, rest), the older chunks what remains:
+    //   base = #(> s*) in older chunks + max(0, tl - eq_after - eq)
     const int st = s_star[hh];
     uint32_t gt_before = 0, eq_after = 0;
     int my_gt = 0, my_eq = 0;
@@ -387,11 +390,10 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(
       const int tl = take_local[hh];
       const int taken_after = (int)eq_after < tl ? (int)eq_after : tl;
       const int rem = tl - taken_after;
-      p_gt_off[hh] = (int)gt_before;
-      p_tie_off[hh] = gt_local[hh] + taken_after;
       p_take[hh] = rem < my_eq ? rem : my_eq;
       p_eq[hh] = my_eq;
-      p_gt_cnt[hh] = my_gt;
+      p_base[hh] = (int)gt_before + max(0, tl - (int)eq_after - my_eq);
+      (void)my_gt;
       if (j == 0) {
         int32_t* o = sel + ((int64_t)b * n_q + g * G + hh) * SEL_STRIDE;
         o[0] = st;
@@ -489,15 +491,18 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(
   __syncthreads();
   // per-head running state in registers (the entry loop below is the select's hot loop; 1024-thread CTAs leave
   // 64 registers per thread, so nothing in it is re-read from shared memory or the parameter bank):
-  //   gtp: list position of the next key with score > s*;  eqe: distance from the end of the s* bucket of the
-  //   next key with score == s* (the bucket is handed out newest first: taken iff eqe < take)
-  int gtp[GMAX], eqe[GMAX], take[GMAX], toff[GMAX];
+  //   base: list position of this warp's next selected key; the chunk's tie quota goes to its newest warps
+  //   first, so this warp takes tw of its ew ties: all of them, none, or (one warp per chunk and head) the
+  //   newest tw, for which es counts the ties already passed
+  int base[GMAX], ew[GMAX], tw[GMAX], es[GMAX];
 #pragma unroll
   for (int hh = 0; hh < GMAX; ++hh) {
-    gtp[hh] = p_gt_off[hh] + (int)wcnt[warp][2 * hh];
-    eqe[hh] = p_eq[hh] - 1 - (int)wcnt[warp][2 * hh + 1];
-    take[hh] = p_take[hh];
-    toff[hh] = p_tie_off[hh];
+    const int pre_gt = (int)wcnt[warp][2 * hh], pre_eq = (int)wcnt[warp][2 * hh + 1];
+    ew[hh] = (warp < 31 ? (int)wcnt[warp + 1][2 * hh + 1] : p_eq[hh]) - pre_eq;
+    const int suf = p_eq[hh] - pre_eq;  // ties in this warp and the newer ones
+    base[hh] = p_base[hh] + pre_gt + max(0, p_take[hh] - suf);
+    tw[hh] = min(ew[hh], max(0, p_take[hh] - (suf - ew[hh])));
+    es[hh] = 0;
   }
   int32_t* const cd0 = cand + ((int64_t)b * n_q + g * G) * cand_stride;
   const int cs = (int)cand_stride;  // the group's lists span < 4 * capacity < 2^31 entries: 32-bit offsets
@@ -558,13 +563,20 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(
       for (int hh = 0; hh < GMAX; ++hh) {
         const bool fg = (ent.y & (0x80u << (8 * hh))) != 0u;
         const bool fe = (ent.y & (0x40u << (8 * hh))) != 0u;
-        const uint32_t mg = __ballot_sync(0xffffffffu, fg);
-        const uint32_t me = __ballot_sync(0xffffffffu, fe);
-        const int fend = eqe[hh] - __popc(me & lt);
-        pos[hh] = fg ? gtp[hh] + __popc(mg & lt) : (fe && fend < take[hh]) ? toff[hh] + fend : -1;
-        if (pos[hh] >= 0) cd0[hh * cs + pos[hh]] = gid;
-        gtp[hh] += __popc(mg);
-        eqe[hh] -= __popc(me);
+        bool pick;
+        if (tw[hh] == 0) {  // warp-uniform: none of this warp's ties is taken
+          pick = fg;
+        } else if (tw[hh] == ew[hh]) {  // all of them
+          pick = fg | fe;
+        } else {  // the chunk's tie boundary: a tie is taken iff fewer than tw ties of this warp are newer
+          const uint32_t me = __ballot_sync(0xffffffffu, fe);
+          pick = fg | (fe && ew[hh] - 1 - (es[hh] + __popc(me & lt)) < tw[hh]);
+          es[hh] += __popc(me);
+        }
+        const uint32_t m = __ballot_sync(0xffffffffu, pick);
+        pos[hh] = pick ? base[hh] + __popc(m & lt) : -1;
+        if (pick) cd0[hh * cs + pos[hh]] = gid;
+        base[hh] += __popc(m);
       }
       if (do_union) {  // union entry: the key once, with its position in every head's candidate list
         const bool any = (pos[0] & pos[1] & pos[2] & pos[3]) != -1;  // positions >= 0, or -1

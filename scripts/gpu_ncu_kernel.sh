@@ -11,5 +11,6 @@ for v in "$@"; do
   ncu -i gpurun_out/ncu_${tag}_$v.ncu-rep --page raw --csv > gpurun_out/ncu_${tag}_${v}_raw.csv 2>/dev/null
   ncu -i gpurun_out/ncu_${tag}_$v.ncu-rep --page details --csv > gpurun_out/ncu_${tag}_${v}_det.csv 2>/dev/null
   ncu -i gpurun_out/ncu_${tag}_$v.ncu-rep --page source --csv --print-source sass > gpurun_out/ncu_${tag}_${v}_sass.csv 2>/dev/null
+  ncu -i gpurun_out/ncu_${tag}_$v.ncu-rep --page source --csv --print-source cuda > gpurun_out/ncu_${tag}_${v}_cuda.csv 2>/dev/null
   echo "$v: $(grep -c . gpurun_out/ncu_${tag}_${v}_raw.csv) raw lines"
 done
