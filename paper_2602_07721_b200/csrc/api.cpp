@@ -216,19 +216,22 @@ pkv_status phase_select_rerank(pkv_index* ix, const pkv_retrieve_params* p, cons
   return PKV_OK;
 }
 
-// Key encoder: by default the half-warp kernel (encode.cu, 464 us per 1M keys at 128K); PKV_ENCODER=tc selects the
-// tensor-core kernel (encode_tc.cu: exact 8-bit-digit GEMMs, 3.5x slower in round 1 — its digit split and the
-// integer recombination cost more ALU work than the butterflies they replace) with the half-warp kernel for the
-// keys it hands back. Read at every call (tests switch it).
-bool use_tc_encoder() {
+// Key encoder. Default: the thread-per-key kernel (encode_fast.cu: exact int32 butterflies, fp32 decisions
+// certified against the oracle's fp64 sequence) with the exact half-warp kernel (encode.cu) for the keys it hands
+// back. PKV_ENCODER=half: the half-warp kernel alone (round 1's default); PKV_ENCODER=tc: the tensor-core kernel
+// (encode_tc.cu, exact 8-bit-digit GEMMs) + the same fallback. fp16 weights always take the half-warp kernel.
+// Read at every call (tests switch it).
+static std::string encoder_kind() {
   const char* e = getenv("PKV_ENCODER");
-  return e && std::string(e) == "tc";
+  return e ? std::string(e) : std::string("fast");
 }
+bool use_tc_encoder() { return encoder_kind() == "tc"; }
 
 pkv_status run_encoder(pkv_index* ix, const void* K, int64_t sb, int64_t sh, int64_t st, int64_t t0, int64_t count,
                        cudaStream_t stream) {
   if (count <= 0) return PKV_OK;
-  if (!use_tc_encoder()) {
+  const std::string kind = encoder_kind();
+  if (kind == "half" || ix->dcfg.w16 || (kind != "tc" && kind != "fast") || (kind == "fast" && !ef_buckets_ok(ix->dcfg))) {
     PKV_CUDA(launch_encode(ix, K, sb, sh, st, t0, count, stream), "encode");
     return PKV_OK;
   }
@@ -236,7 +239,10 @@ pkv_status run_encoder(pkv_index* ix, const void* K, int64_t sb, int64_t sh, int
   if (!ix->enc_fb) PKV_CUDA(cudaMalloc(&ix->enc_fb, (size_t)(units * ix->cap + 1) * 4), "encoder list");
   int32_t* fb_n = ix->enc_fb + units * ix->cap;
   PKV_CUDA(cudaMemsetAsync(fb_n, 0, 4, stream), "encoder list reset");
-  PKV_CUDA(launch_encode_tc(ix, K, sb, sh, st, t0, count, ix->enc_fb, fb_n, stream), "encode (tensor cores)");
+  if (kind == "tc")
+    PKV_CUDA(launch_encode_tc(ix, K, sb, sh, st, t0, count, ix->enc_fb, fb_n, stream), "encode (tensor cores)");
+  else
+    PKV_CUDA(launch_encode_fast(ix, K, sb, sh, st, t0, count, ix->enc_fb, fb_n, stream), "encode (thread per key)");
   PKV_CUDA(launch_encode_list(ix, K, sb, sh, st, t0, count, ix->enc_fb, fb_n, stream), "encode (fallback)");
   return PKV_OK;
 }
@@ -357,7 +363,10 @@ pkv_status pkv_index_create(const pkv_config* cfg, int32_t batch, int64_t capaci
   if (e == cudaSuccess) e = cudaMalloc(&ix->rec, units * capacity * ix->dcfg.rec_bytes);
   if (e == cudaSuccess) e = cudaMalloc(&ix->stats, 4 * sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMemset(ix->stats, 0, 4 * sizeof(unsigned long long));
+  // the encoders' hand-back list (4 B per key + count): allocated here, not inside a (timed, capturable) encode
+  if (e == cudaSuccess) e = cudaMalloc(&ix->enc_fb, (units * capacity + 1) * 4);
   if (e != cudaSuccess) {
+    cudaFree(ix->enc_fb);
     cudaFree(ix->stats);
     cudaFree(ix->rec);
     cudaFree(ix->ids);

@@ -223,9 +223,14 @@ __global__ void __launch_bounds__(256) encode_list_kernel(const uint16_t* __rest
   if (threadIdx.x < 8) sL[threadIdx.x] = cfg.levels[threadIdx.x];
   __syncthreads();
   const int n = *list_n;
-  for (int kk = blockIdx.x * KEYS_PER_BLOCK + (threadIdx.x >> 4); kk < n; kk += gridDim.x * KEYS_PER_BLOCK) {
-    const int e = list[kk];
-    encode_one(K, sb, sh, st, t0, n_kv, cap, cfg, ids, rec, sL, stats, (int)(e / count), e % count, true, false);
+  // both half-warps of a warp run the same number of rounds (encode_one shuffles over the full warp): the round
+  // count is taken over the warp's pair of entries, and a half whose entry is past the list encodes a dummy key
+  // (the list's first entry) without storing it
+  for (int k0 = blockIdx.x * KEYS_PER_BLOCK + ((threadIdx.x >> 5) << 1); k0 < n; k0 += gridDim.x * KEYS_PER_BLOCK) {
+    const int kk = k0 + ((threadIdx.x >> 4) & 1);
+    const bool live = kk < n;
+    const int e = list[live ? kk : 0];
+    encode_one(K, sb, sh, st, t0, n_kv, cap, cfg, ids, rec, sL, stats, (int)(e / count), e % count, live, false);
   }
 }
 

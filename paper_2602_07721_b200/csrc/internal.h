@@ -94,7 +94,7 @@ struct pkv_index {
   // bucket offsets u16 [257] and the chunk's key offsets u16 [POST_CHUNK] sorted by centroid id
   float* dbg_out_f32 = nullptr;         // optional fp32 copy of every attention output (pkv_index_set_debug_output)
   unsigned long long* stats = nullptr;  // device [4]: zero keys, keys with a zero subspace, zero subspaces, spare
-  int32_t* enc_fb = nullptr;  // [batch*n_kv*cap + 1]: tensor-core encoder fallback list, count at the end
+  int32_t* enc_fb = nullptr;  // [batch*n_kv*cap + 1]: keys handed back by the fast / tensor-core encoder, count at the end
   bool postings = false;
   uint32_t* occ = nullptr;  // [batch][n_kv][16][256] centroid occupancy (pkv_index_set_occupancy); null = off
   uint16_t* post_off = nullptr;
@@ -165,6 +165,9 @@ cudaError_t init_encode_tc_attrs();
 cudaError_t launch_encode_tc(const pkv_index* ix, const void* K, int64_t sb, int64_t sh, int64_t st, int64_t t0,
                              int64_t count, int32_t* fb_list, int32_t* fb_count, cudaStream_t stream);
 // half-warp encoder over a device list (entries bh * count + tt)
+bool ef_buckets_ok(const DevCfg& c);
+cudaError_t launch_encode_fast(const pkv_index* ix, const void* K, int64_t sb, int64_t sh, int64_t st, int64_t t0,
+                               int64_t count, int32_t* list, int32_t* list_n, cudaStream_t stream);
 cudaError_t launch_encode_list(const pkv_index* ix, const void* K, int64_t sb, int64_t sh, int64_t st, int64_t t0,
                                int64_t count, const int32_t* list, const int32_t* list_n, cudaStream_t stream);
 cudaError_t launch_encode(const pkv_index* ix, const void* K, int64_t sb, int64_t sh, int64_t st, int64_t t0,

@@ -757,3 +757,35 @@ def test_key_fraction_needs_occupancy(pkv):
     with pytest.raises(pkv.PkvError):
         pkv.retrieve_topk(ix, q, 10, rho_keys=50)
 
+
+
+def test_encoder_kinds_agree(pkv, monkeypatch):
+    """The default thread-per-key encoder (encode_fast.cu: exact int32 butterflies, fp32 decisions certified against
+    the oracle's fp64 sequence, uncertain keys handed to the exact half-warp kernel) against the half-warp kernel on
+    ~300K LLM-like keys plus wide-range / zero / subnormal / tiny keys: ids and codes identical, stored weights within
+    2e-6 relative; the oracle check of the same keys runs in the other parity tests."""
+    K, q, V = make_problem(95, 2, 8, 2, 150000, plant=False)
+    K[0, 0, 5] = 0
+    K[0, 0, 6, 16:24] = 0
+    K[1, 1, 10:40, 3] = 1e-9
+    K[1, 0, 40:60, 100] = 3e-30
+    K[0, 1, 60:70, :] = torch.randn(10, 128, device="cuda").to(torch.bfloat16) * 1e-20
+    cfg = pkv.config_init(8, 2, SB)
+    out = {}
+    for kind in ("fast", "half"):
+        monkeypatch.setenv("PKV_ENCODER", kind)
+        ix = pkv.Index(cfg, 2, 150000)
+        pkv.encode_keys(ix, K)
+        out[kind] = [t.cpu().numpy() for t in ix.export()]
+        out[kind + "_stats"] = ix.stats()
+    assert np.array_equal(out["fast"][0], out["half"][0]), "ids"
+    assert np.array_equal(out["fast"][1], out["half"][1]), "codes"
+    wf, wh = out["fast"][2].astype(np.float64), out["half"][2].astype(np.float64)
+    assert np.all(np.abs(wf - wh) <= 2e-6 * np.abs(wh) + 1e-30), "weights"
+    assert out["fast_stats"] == out["half_stats"]
+
+
+def test_half_warp_encoder_still_exact(pkv, monkeypatch):
+    monkeypatch.setenv("PKV_ENCODER", "half")
+    K, q, V = make_problem(96, 2, 8, 2, 3001)
+    run_and_check(pkv, K, q, V, k=64, n_hot=16)
