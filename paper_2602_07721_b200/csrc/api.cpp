@@ -359,7 +359,7 @@ pkv_status pkv_index_create(const pkv_config* cfg, int32_t batch, int64_t capaci
   cudaDeviceGetAttribute(&ix->num_sms, cudaDevAttrMultiProcessorCount, device);
   cudaDeviceGetAttribute(&ix->smem_reserved, cudaDevAttrReservedSharedMemoryPerBlock, device);
   const size_t units = (size_t)batch * cfg->n_kv_heads;
-  cudaError_t e = cudaMalloc(&ix->ids, (units * capacity + SCAN_SLACK_ROWS) * NB);  // slack: scan prefetch
+  cudaError_t e = cudaMalloc(&ix->ids, units * capacity * NB);
   if (e == cudaSuccess) e = cudaMalloc(&ix->rec, units * capacity * ix->dcfg.rec_bytes);
   if (e == cudaSuccess) e = cudaMalloc(&ix->stats, 4 * sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMemset(ix->stats, 0, 4 * sizeof(unsigned long long));

@@ -15,9 +15,6 @@ namespace pkv {
 
 constexpr int D = PKV_HEAD_DIM;        // 128
 constexpr int NB = PKV_SUBSPACES;      // 16 subspaces
-// id rows allocated past the last (sequence, KV head): the scan prefetches up to two warp rounds (2 x 128 rows)
-// beyond a warp segment without bounds checks
-constexpr int SCAN_SLACK_ROWS = 512;
 constexpr int M = PKV_SUBSPACE_DIM;    // 8
 constexpr int NC = PKV_CENTROIDS;      // 256 analytic centroids per subspace (Eq. 5)
 constexpr int HB = 128;                // histogram bins (max collision score <= 127)

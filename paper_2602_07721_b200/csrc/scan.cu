@@ -12,7 +12,6 @@
 //                  ties in the s* bucket handed out newest first (AMB-12), then the chunk's candidate ids.
 #include <algorithm>
 #include <cstdlib>
-#include <utility>
 
 #include "common.cuh"
 
@@ -25,107 +24,74 @@ constexpr int LUT_WORDS = NC * 64;                 // 64 KB
 constexpr int SCAN_SMEM = LUT_WORDS * 4 + SCAN_WARPS * GMAX * HB * 4;
 constexpr int SCAN_UNROLL = 4;
 
+template <int RES, bool FAST>
+__device__ __forceinline__ uint32_t lut_load(uint32_t addr, uint32_t lut_base) {
+  uint32_t v;
+  if (FAST) {
+    asm volatile("ld.shared.u32 %0, [%1+%2];" : "=r"(v) : "r"(addr), "n"(RES));
+  } else {
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr + lut_base));
+  }
+  return v;
+}
+
 // Warp w of a chunk's CTA owns the contiguous key segment [t_begin + w*seg, +seg), seg a multiple of 128 keys; the
 // select kernel uses the same segments, so the per-warp histograms of the scan give it every warp's output offsets.
 __host__ __device__ __forceinline__ uint32_t warp_seg(uint32_t len) { return ((len + 32 * 128 - 1) / (32 * 128)) * 128; }
 
-// 4 rows of a warp round (keys lane, lane + 32, lane + 64, lane + 96 from p). Never bounds-checked: the id
-// buffer carries SCAN_SLACK_ROWS rows of slack past the last (sequence, KV head), so a prefetch that runs past the
-// end of a warp's segment stays inside the allocation; rows past the segment are never scored.
-__device__ __forceinline__ void load_rows(uint4 (&row)[SCAN_UNROLL], const uint8_t* p) {
+template <bool CHECK>
+__device__ __forceinline__ void load_rows(uint4 (&row)[SCAN_UNROLL], const uint8_t* __restrict__ ids_bh, uint32_t base,
+                                          uint32_t t_end) {
 #pragma unroll
-  for (int u = 0; u < SCAN_UNROLL; ++u) row[u] = ldg_nc_v4_early(p + u * 32 * NB);
+  for (int u = 0; u < SCAN_UNROLL; ++u) {
+    const uint32_t t = base + (uint32_t)u * 32;
+    row[u] = (!CHECK || t < t_end) ? ldg_nc_v4(ids_bh + (size_t)t * NB) : make_uint4(0, 0, 0, 0);
+  }
 }
 
 // Score one key (16 conflict-free LUT reads) and record it; G query heads packed in the bytes of acc.
-// LUT word address of subspace i for lane L: id_i * 64 + (L + i) (table L + i, L + i < 64), i.e. byte address
-// (id_i << 8) | 4L plus the immediate 4i: one PRMT per lookup builds it from the id byte and lane4 = 4L.
-template <int RES, bool FAST, int I>
-__device__ __forceinline__ uint32_t lut_lookup(const uint32_t (&wds)[4], uint32_t lane4, uint32_t lut_base) {
-  const uint32_t a = prmt(wds[I >> 2], lane4, 0x5504u | ((uint32_t)(I & 3) << 4));
-  uint32_t v;
-  if (FAST) {
-    asm volatile("ld.shared.u32 %0, [%1+%2];" : "=r"(v) : "r"(a), "n"(RES + 4 * I));
-  } else {
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a + lut_base + 4u * I));
-  }
-  return v;
-}
-template <int RES, bool FAST, int... I>
-__device__ __forceinline__ void lut_sum(const uint32_t (&wds)[4], uint32_t lane4, uint32_t lut_base, uint32_t& acc,
-                                        std::integer_sequence<int, I...>) {
-  acc = (0u + ... + lut_lookup<RES, FAST, I>(wds, lane4, lut_base));
-}
-template <int H>
-__device__ __forceinline__ void hist_one(uint32_t acc, uint32_t hist_s) {
-  const uint32_t a = hist_s + (prmt(acc, 0u, 0x4440u | (uint32_t)H) << 2);
-  asm volatile("red.shared.add.u32 [%0+%1], 1;" ::"r"(a), "n"(H * HB * 4) : "memory");
-}
-template <int... H>
-__device__ __forceinline__ void hist_add(uint32_t acc, uint32_t hist_s, std::integer_sequence<int, H...>) {
-  (hist_one<H>(acc, hist_s), ...);
-}
-
 template <int RES, bool FAST, int G>
-__device__ __forceinline__ void score_key(const uint4& r, uint32_t lane4, uint32_t lut_base, uint32_t* sp,
-                                          uint32_t hist_s) {
+__device__ __forceinline__ void score_key(const uint4& r, const uint32_t (&p)[16], uint32_t lut_base,
+                                          uint32_t* __restrict__ scores_bh, uint32_t* hist_w, uint32_t t) {
   const uint32_t wds[4] = {r.x, r.y, r.z, r.w};
   uint32_t acc = 0;
-  lut_sum<RES, FAST>(wds, lane4, lut_base, acc, std::make_integer_sequence<int, 16>{});
-#ifndef PKV_EXP_NOSTORE
-  *sp = acc;
-#else
-  if (acc == 0xffffffffu) *sp = acc;
-#endif
-#ifndef PKV_EXP_NOHIST
-  // hist_s: shared-window address of this warp's histograms ([head][HB] u32); bin address = hist_s + 4 * score
-  hist_add(acc, hist_s, std::make_integer_sequence<int, G>{});
-#endif
-}
-
-template <int RES, bool FAST, int G>
-__device__ __forceinline__ void score_round(const uint4 (&row)[SCAN_UNROLL], uint32_t lane4, uint32_t lut_base,
-                                            uint32_t* sp, uint32_t hist_s, int valid) {
 #pragma unroll
-  for (int u = 0; u < SCAN_UNROLL; ++u)
-    if (u * 32 < valid) score_key<RES, FAST, G>(row[u], lane4, lut_base, sp + u * 32, hist_s);
+  for (int i = 0; i < 16; ++i) {
+    const uint32_t a = prmt(wds[i >> 2], p[i], 0x5504u | ((uint32_t)(i & 3) << 4));
+    acc += lut_load<RES, FAST>(a, lut_base);
+  }
+  scores_bh[t] = acc;
+#pragma unroll
+  for (int hh = 0; hh < G; ++hh) atomicAdd(&hist_w[hh * HB + prmt(acc, 0u, 0x4440u | (uint32_t)hh)], 1u);
 }
 
-// Main loop over this warp's segment [seg0, seg1): two row buffers in ping-pong, the next round's rows in flight
-// while this round is scored; pointers advance by a round, so loads and stores use immediate offsets.
+// Main loop over this warp's segment [seg0, seg1), software-pipelined: rows of the next round are in flight while
+// this round is scored. Full rounds run without per-key bounds checks; only the last round checks.
 template <int RES, bool FAST, int G>
-__device__ __forceinline__ void scan_loop(uint4 (&ra)[SCAN_UNROLL], const uint8_t* ip, uint32_t* sp,
-                                          uint32_t hist_s, uint32_t seg0, uint32_t seg1, uint32_t lut_base) {
+__device__ __forceinline__ void scan_loop(uint4 (&row)[SCAN_UNROLL], const uint8_t* __restrict__ ids_bh,
+                                          uint32_t* __restrict__ scores_bh, uint32_t* hist_w, uint32_t seg0,
+                                          uint32_t seg1, uint32_t lut_base) {
   const int lane = threadIdx.x & 31;
-  const uint32_t lane4 = (uint32_t)lane * 4u;
+  uint32_t p[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) p[i] = (uint32_t)(lane + i) * 4u;
   constexpr uint32_t STEP = 32 * SCAN_UNROLL;
-  uint4 rb[SCAN_UNROLL];
-  // keys left in the warp's segment from the round start (warp-uniform, so the branches below never diverge);
-  // lane l scores row u of a partial round iff l + 32u < rem
-  int rem = (int)seg1 - (int)seg0;
-  const int lane_i = lane;
-  while (rem > 0) {
-    load_rows(rb, ip + STEP * NB);
-    if (rem >= (int)STEP) {
-      score_round<RES, FAST, G>(ra, lane4, lut_base, sp, hist_s, (int)STEP);
-    } else {
-      score_round<RES, FAST, G>(ra, lane4, lut_base, sp, hist_s, rem - lane_i);
-      break;
+  uint32_t wbase = seg0;  // warp-uniform
+  for (; wbase + STEP <= seg1; wbase += STEP) {  // all rows of this round in range
+    uint4 nxt[SCAN_UNROLL];
+    load_rows<true>(nxt, ids_bh, wbase + STEP + lane, seg1);
+#pragma unroll
+    for (int u = 0; u < SCAN_UNROLL; ++u)
+      score_key<RES, FAST, G>(row[u], p, lut_base, scores_bh, hist_w, wbase + lane + u * 32);
+#pragma unroll
+    for (int u = 0; u < SCAN_UNROLL; ++u) row[u] = nxt[u];
+  }
+  if (wbase < seg1) {  // last, partial round (no further rows to prefetch)
+#pragma unroll
+    for (int u = 0; u < SCAN_UNROLL; ++u) {
+      const uint32_t t = wbase + lane + u * 32;
+      if (t < seg1) score_key<RES, FAST, G>(row[u], p, lut_base, scores_bh, hist_w, t);
     }
-    rem -= (int)STEP;
-    ip += STEP * NB;
-    sp += STEP;
-    if (rem <= 0) break;
-    load_rows(ra, ip + STEP * NB);
-    if (rem >= (int)STEP) {
-      score_round<RES, FAST, G>(rb, lane4, lut_base, sp, hist_s, (int)STEP);
-    } else {
-      score_round<RES, FAST, G>(rb, lane4, lut_base, sp, hist_s, rem - lane_i);
-      break;
-    }
-    rem -= (int)STEP;
-    ip += STEP * NB;
-    sp += STEP;
   }
 }
 
@@ -147,8 +113,7 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1)
   const uint32_t seg0 = (uint32_t)t_begin + (threadIdx.x >> 5) * seg;
   const uint32_t seg1 = min((uint32_t)t_end, seg0 + seg);
   uint4 row[SCAN_UNROLL];
-  const uint8_t* ip = ids_bh + (size_t)(seg0 + (threadIdx.x & 31)) * NB;
-  if (seg1 > seg0) load_rows(row, ip);  // warp-uniform: an empty segment (short chunk) loads nothing
+  load_rows<true>(row, ids_bh, seg0 + (threadIdx.x & 31), seg1);
   for (int i = threadIdx.x; i < SCAN_WARPS * GMAX * HB; i += SCAN_THREADS) hist[i] = 0u;
   pdl_wait();  // lookup table comes from qprep
   phase_mark(K_SCAN, 1);
@@ -169,15 +134,13 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1)
   phase_mark(K_SCAN, 2);
   uint32_t* scores_bh = scores + (int64_t)bh * sstride;
   uint32_t* hist_w = hist + (threadIdx.x >> 5) * GMAX * HB;
-  const uint32_t hist_s = (uint32_t)__cvta_generic_to_shared(hist_w);
-  uint32_t* sp = scores_bh + seg0 + (threadIdx.x & 31);
   if (lut_base == (uint32_t)RES) {
-    if (G == 4) scan_loop<RES, true, 4>(row, ip, sp, hist_s, seg0, seg1, lut_base);
-    else if (G == 2) scan_loop<RES, true, 2>(row, ip, sp, hist_s, seg0, seg1, lut_base);
-    else if (G == 3) scan_loop<RES, true, 3>(row, ip, sp, hist_s, seg0, seg1, lut_base);
-    else scan_loop<RES, true, 1>(row, ip, sp, hist_s, seg0, seg1, lut_base);
+    if (G == 4) scan_loop<RES, true, 4>(row, ids_bh, scores_bh, hist_w, seg0, seg1, lut_base);
+    else if (G == 2) scan_loop<RES, true, 2>(row, ids_bh, scores_bh, hist_w, seg0, seg1, lut_base);
+    else if (G == 3) scan_loop<RES, true, 3>(row, ids_bh, scores_bh, hist_w, seg0, seg1, lut_base);
+    else scan_loop<RES, true, 1>(row, ids_bh, scores_bh, hist_w, seg0, seg1, lut_base);
   } else {
-    scan_loop<RES, false, 4>(row, ip, sp, hist_s, seg0, seg1, lut_base);  // G <= 4: unused bytes are 0
+    scan_loop<RES, false, 4>(row, ids_bh, scores_bh, hist_w, seg0, seg1, lut_base);  // G <= 4: unused bytes are 0
   }
   if (warp_hist != nullptr) {
     // this warp's cumulative counts cum_w[h][s] = #(score_h >= s) in its segment (u16: a segment holds < 2^16 keys),
