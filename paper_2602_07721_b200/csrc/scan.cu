@@ -425,31 +425,24 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(
   }
 #pragma unroll
   for (int hh = 0; hh < GMAX; ++hh) {
-    uint32_t a1 = tot_gt[hh];
-    uint32_t a2 = tot_eq[hh];
-#pragma unroll
-    for (int x = 16; x > 0; x >>= 1) {
-      a1 += __shfl_xor_sync(0xffffffffu, a1, x);
-      a2 += __shfl_xor_sync(0xffffffffu, a2, x);
-    }
+    const uint32_t a1 = __reduce_add_sync(0xffffffffu, tot_gt[hh]);
+    const uint32_t a2 = __reduce_add_sync(0xffffffffu, tot_eq[hh]);
     if (lane == 0) {
       wcnt[warp][2 * hh] = a1;
       wcnt[warp][2 * hh + 1] = a2;
     }
   }
   __syncthreads();
-  if (warp == 0) {
+  if (warp < 2 * GMAX) {  // warp k scans column k over the 32 warps
+    const int k = warp;
+    const uint32_t v = wcnt[lane][k];
+    uint32_t inc = v;
 #pragma unroll
-    for (int k = 0; k < 2 * GMAX; ++k) {
-      const uint32_t v = wcnt[lane][k];
-      uint32_t inc = v;
-#pragma unroll
-      for (int x = 1; x < 32; x <<= 1) {
-        const uint32_t o = __shfl_up_sync(0xffffffffu, inc, x);
-        if (lane >= x) inc += o;
-      }
-      wcnt[lane][k] = inc - v;  // exclusive base of warp `lane`
+    for (int x = 1; x < 32; x <<= 1) {
+      const uint32_t o = __shfl_up_sync(0xffffffffu, inc, x);
+      if (lane >= x) inc += o;
     }
+    wcnt[lane][k] = inc - v;  // exclusive base of warp `lane`
   }
   __syncthreads();
   // per-head running state in registers (the entry loop below is the select's hot loop; 1024-thread CTAs leave
@@ -472,6 +465,21 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(
   const int32_t idoff = (int32_t)id_offset;
   const uint32_t lt = (1u << lane) - 1u;
   const bool do_prefetch = rec != nullptr, do_union = uid != nullptr;
+  // Fast entry loop: every head of this warp takes all of its s* ties or none of them (true for all warps but at
+  // most one per chunk and head) and no union list is built. A key is then picked for head h iff its flag byte h
+  // has bit 7 (>) or, when the warp takes its ties, bit 6 (==): one mask, no per-head branches (1M: the entry
+  // loop was ~185 instructions per 32 entries with the per-head branches).
+#ifdef PKV_NO_FAST_ENTRY
+  bool fast = false;  // A/B build: the per-head-branch loop for every warp
+#else
+  bool fast = !do_union;
+#endif
+  uint32_t pmask = 0;
+#pragma unroll
+  for (int hh = 0; hh < GMAX; ++hh) {
+    if (hh < G && tw[hh] != 0 && tw[hh] != ew[hh]) fast = false;
+    pmask |= (tw[hh] == 0 ? 0x80u : 0xc0u) << (8 * hh);  // heads >= G never have a flag set
+  }
   phase_mark(K_SELECT, 4);
   // pass 2: keys with score >= s* for at least one head (~4 x beta of them) are first compacted, in key
   // order, into a per-warp list; the per-head ballots then run over that list only. Key (lane l, element e)
@@ -479,11 +487,19 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(
   // of lower lanes (one ballot per element position) plus its own earlier kept elements.
   uint2* wl = sel_list + warp * (VB * 128);
   for (uint32_t g0 = 0; g0 < ngrp; g0 += VB) {
-    if (ngrp > VB) {
+    // vreg holds groups 0..VB-1 from the prologue unless pass 1 streamed the segment (no per-warp histograms)
+    if (ngrp > VB && (g0 > 0 || warp_hist == nullptr)) {
 #pragma unroll
       for (int k2 = 0; k2 < VB; ++k2) {
         const uint32_t t = seg0 + 128u * (g0 + k2) + 4u * lane;
         vreg[k2] = (t < seg1) ? *reinterpret_cast<const uint4*>(sc + t) : make_uint4(0, 0, 0, 0);
+      }
+    }
+    if (g0 + VB < ngrp) {  // the next batch towards L1 while this one is compacted (no registers held)
+#pragma unroll
+      for (int k2 = 0; k2 < VB; ++k2) {
+        const uint32_t t = seg0 + 128u * (g0 + VB + k2) + 4u * lane;
+        if (t < seg1) asm volatile("prefetch.global.L1 [%0];" ::"l"(sc + t));
       }
     }
     uint32_t nl = 0;
@@ -512,7 +528,25 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(
       nl += total;
     }
     __syncwarp();
-    for (uint32_t l0 = 0; l0 < nl; l0 += 32) {
+    for (uint32_t l0 = 0; fast && l0 < nl; l0 += 32) {
+      const bool valid = l0 + lane < nl;
+      const uint2 ent = valid ? wl[l0 + lane] : make_uint2(0u, 0u);  // invalid lanes: no flags
+      if (valid && do_prefetch) {  // warm L2 with the record the rerank kernel will gather for this key
+        const uint8_t* r = rec + (int64_t)bh * rec_head_bytes + (int64_t)ent.x * rec_bytes;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(r));
+        if (rec_bytes != 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(r + rec_bytes - 1));
+      }
+      const uint32_t pk = ent.y & pmask;
+      const int32_t gid = (int32_t)ent.x + idoff;
+#pragma unroll
+      for (int hh = 0; hh < GMAX; ++hh) {
+        const bool pick = (pk & (0xc0u << (8 * hh))) != 0u;
+        const uint32_t m = __ballot_sync(0xffffffffu, pick);
+        if (pick) cd0[hh * cs + base[hh] + __popc(m & lt)] = gid;
+        base[hh] += __popc(m);
+      }
+    }
+    for (uint32_t l0 = 0; !fast && l0 < nl; l0 += 32) {
       const bool valid = l0 + lane < nl;
       const uint2 ent = valid ? wl[l0 + lane] : make_uint2(0u, 0u);
       if (valid && do_prefetch) {  // warm L2 with the record the rerank kernel will gather for this key
