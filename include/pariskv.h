@@ -355,6 +355,38 @@ pkv_status pkv_sparse_attend_sharded_local(pkv_index* const* shards, const int64
                                            const void* K_hot, const void* V_hot, int32_t n_hot, float scale,
                                            void* out, float* lse, cudaStream_t stream);
 
+/* ---------------------------------------------------------------------------------------------------
+ * Append rebalancing across sequence shards (not in the paper). Decode appends (one
+ * update_size flush per 512 steps) land on the last rank, whose shard grows. A boundary shift moves the `count`
+ * OLDEST keys of shard r+1 to the END of shard r: both shards stay contiguous and ordered by position, so the
+ * sharded select's newest-rank-first tie rule (AMB-12) and all sharded results are unchanged (bit-identical to
+ * the unsharded index). The caller moves the matching K/V rows the same way (local row = id - shard_offset).
+ * The index's degenerate-key statistics (pkv_index_get_stats) count the keys encoded INTO that index and are
+ * not moved. Postings / occupancy tables, when enabled, are rebuilt.
+ * ------------------------------------------------------------------------------------------------- */
+/* Bytes of one key's exchange entry over all sequences and KV heads: batch * n_kv * (16 + record bytes). An
+ * entry buffer of `count` keys is laid out [batch][n_kv][count] x (canonical 16-byte centroid-id row — subspace
+ * b in byte b — followed by the key's record). */
+pkv_status pkv_index_entry_bytes(const pkv_index* index, int64_t* bytes_per_key);
+/* Write the entries of keys [0, count) of `index` (its oldest) into the device buffer `buf` (count *
+ * pkv_index_entry_bytes bytes, caller-owned, on the index's device). Stream-ordered; the index is unchanged.
+ * INVALID_ARG: count outside [0, n] or null buffer. */
+pkv_status pkv_index_export_front(const pkv_index* index, int64_t count, void* buf, cudaStream_t stream);
+/* Append `count` entries from the device buffer `buf` after the index's newest key (they become keys
+ * [n, n + count)). CAPACITY if n + count exceeds the capacity (nothing changes). */
+pkv_status pkv_index_import_back(pkv_index* index, const void* buf, int64_t count, cudaStream_t stream);
+/* Remove keys [0, count): the rest move down by count (stream-ordered scratch copy) and shard_offset grows by
+ * count. INVALID_ARG: count outside [0, n]. */
+pkv_status pkv_index_drop_front(pkv_index* index, int64_t count, cudaStream_t stream);
+/* Both indices on one device (same batch, KV heads, record format and rotation): export_front(newer) +
+ * import_back(older) + drop_front(newer) through a stream-ordered buffer. Across GPUs the caller runs the three
+ * steps on the two ranks and moves the buffer between them (NCCL send/recv, a peer copy). */
+pkv_status pkv_index_shift_boundary(pkv_index* older, pkv_index* newer, int64_t count, cudaStream_t stream);
+/* Host-only policy: for P contiguous shards of lengths[0..P), shift[r] (r < P-1) = keys to move from shard r+1 to
+ * shard r so that every boundary moves right, by whole `granule`s, towards the balanced position r*N/P (never
+ * left; boundaries stay ordered). Apply shift[P-2] first and shift[0] last. Touches no device. */
+pkv_status pkv_rebalance_plan(const int64_t* lengths, int32_t P, int64_t granule, int64_t* shift);
+
 /* Total number of kernels this library has launched in the process (host-side counter, for launch
  * accounting in bench.py; graph replays are not counted). */
 pkv_status pkv_launch_count(uint64_t* total);

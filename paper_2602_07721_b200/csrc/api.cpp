@@ -917,4 +917,114 @@ pkv_status pkv_comm_share(pkv_index* ix, pkv_index* donor, int64_t shard_offset)
   return comm_share(ix, donor, shard_offset);
 }
 
+
+// ------------------------------------------------------------------ append rebalancing
+pkv_status pkv_index_entry_bytes(const pkv_index* ix, int64_t* bytes_per_key) {
+  if (!ix || !bytes_per_key) return set_error(PKV_ERR_INVALID_ARG, "pkv_index_entry_bytes: null pointer");
+  *bytes_per_key = (int64_t)ix->batch * ix->cfg.n_kv_heads * (NB + ix->dcfg.rec_bytes);
+  return PKV_OK;
+}
+
+pkv_status pkv_index_export_front(const pkv_index* ix, int64_t count, void* buf, cudaStream_t stream) {
+  if (!ix) return set_error(PKV_ERR_INVALID_ARG, "pkv_index_export_front: null index");
+  if (count < 0 || count > ix->n) return set_error(PKV_ERR_INVALID_ARG, "pkv_index_export_front: count outside [0, n]");
+  if (count > 0 && !buf) return set_error(PKV_ERR_INVALID_ARG, "pkv_index_export_front: null buffer");
+  DeviceGuard g(ix->device);
+  PKV_CUDA(launch_export_entries(ix, 0, count, buf, stream), "export front");
+  return PKV_OK;
+}
+
+// postings and occupancy of an index whose contents changed in [t0, n): rebuilt from the first affected chunk
+static pkv_status refresh_derived(pkv_index* ix, int64_t t0, bool full, cudaStream_t stream) {
+  if (ix->postings)
+    PKV_CUDA(launch_postings_build(ix, full ? 0 : t0 / POST_CHUNK, (ix->n + POST_CHUNK - 1) / POST_CHUNK, stream),
+             "postings (rebalance)");
+  if (ix->occ) {
+    if (full)
+      PKV_CUDA(cudaMemsetAsync(ix->occ, 0, (size_t)ix->batch * ix->cfg.n_kv_heads * NB * NC * 4, stream),
+               "occupancy clear");
+    PKV_CUDA(launch_occupancy(ix, full ? 0 : t0, ix->n, stream), "occupancy (rebalance)");
+  }
+  return PKV_OK;
+}
+
+pkv_status pkv_index_import_back(pkv_index* ix, const void* buf, int64_t count, cudaStream_t stream) {
+  if (!ix) return set_error(PKV_ERR_INVALID_ARG, "pkv_index_import_back: null index");
+  if (count < 0) return set_error(PKV_ERR_INVALID_ARG, "pkv_index_import_back: count < 0");
+  if (count > 0 && !buf) return set_error(PKV_ERR_INVALID_ARG, "pkv_index_import_back: null buffer");
+  if (ix->n + count > ix->cap) return set_error(PKV_ERR_CAPACITY, "pkv_index_import_back: capacity exceeded");
+  if (count == 0) return PKV_OK;
+  DeviceGuard g(ix->device);
+  const int64_t t0 = ix->n;
+  PKV_CUDA(launch_import_entries(ix, t0, count, buf, stream), "import back");
+  ix->n += count;
+  return refresh_derived(ix, t0, false, stream);
+}
+
+pkv_status pkv_index_drop_front(pkv_index* ix, int64_t count, cudaStream_t stream) {
+  if (!ix) return set_error(PKV_ERR_INVALID_ARG, "pkv_index_drop_front: null index");
+  if (count < 0 || count > ix->n) return set_error(PKV_ERR_INVALID_ARG, "pkv_index_drop_front: count outside [0, n]");
+  if (count == 0) return PKV_OK;
+  DeviceGuard g(ix->device);
+  const int64_t keep = ix->n - count;
+  if (keep > 0) {  // the kept keys move down by `count` through a stream-ordered scratch copy (the ranges overlap)
+    int64_t eb = 0;
+    pkv_index_entry_bytes(ix, &eb);
+    void* tmp = nullptr;
+    PKV_CUDA(cudaMallocAsync(&tmp, (size_t)(keep * eb), stream), "drop_front scratch");
+    cudaError_t e = launch_export_entries(ix, count, keep, tmp, stream);
+    if (e == cudaSuccess) e = launch_import_entries(ix, 0, keep, tmp, stream);
+    cudaFreeAsync(tmp, stream);
+    PKV_CUDA(e, "drop front");
+  }
+  ix->n = keep;
+  ix->shard_offset += count;
+  return refresh_derived(ix, 0, true, stream);
+}
+
+pkv_status pkv_index_shift_boundary(pkv_index* older, pkv_index* newer, int64_t count, cudaStream_t stream) {
+  if (!older || !newer || older == newer) return set_error(PKV_ERR_INVALID_ARG, "shift_boundary: two indices needed");
+  if (older->device != newer->device || older->batch != newer->batch ||
+      older->cfg.n_kv_heads != newer->cfg.n_kv_heads || older->dcfg.rec_bytes != newer->dcfg.rec_bytes ||
+      std::memcmp(older->dcfg.sign_mask, newer->dcfg.sign_mask, sizeof(older->dcfg.sign_mask)) != 0)
+    return set_error(PKV_ERR_INVALID_ARG, "shift_boundary: indices of different devices / shapes / rotations");
+  if (count < 0 || count > newer->n) return set_error(PKV_ERR_INVALID_ARG, "shift_boundary: count outside [0, n]");
+  if (older->n + count > older->cap) return set_error(PKV_ERR_CAPACITY, "shift_boundary: capacity exceeded");
+  if (count == 0) return PKV_OK;
+  DeviceGuard g(older->device);
+  int64_t eb = 0;
+  pkv_index_entry_bytes(newer, &eb);
+  void* buf = nullptr;
+  PKV_CUDA(cudaMallocAsync(&buf, (size_t)(count * eb), stream), "shift_boundary buffer");
+  pkv_status st = pkv_index_export_front(newer, count, buf, stream);
+  if (st == PKV_OK) st = pkv_index_import_back(older, buf, count, stream);
+  if (st == PKV_OK) st = pkv_index_drop_front(newer, count, stream);
+  cudaFreeAsync(buf, stream);
+  return st;
+}
+
+pkv_status pkv_rebalance_plan(const int64_t* lengths, int32_t P, int64_t granule, int64_t* shift) {
+  if (!lengths || !shift || P < 1 || P > 64 || granule < 1)
+    return set_error(PKV_ERR_INVALID_ARG, "pkv_rebalance_plan: bad arguments");
+  int64_t N = 0;
+  for (int r = 0; r < P; ++r) {
+    if (lengths[r] < 0) return set_error(PKV_ERR_INVALID_ARG, "pkv_rebalance_plan: negative length");
+    N += lengths[r];
+  }
+  // boundary r (start of shard r, now at b_r) moves right towards the balanced position r*N/P by whole granules,
+  // never left; then min(., next boundary) keeps the boundaries ordered (shard r+1 can always give what r needs
+  // once it has received its own share from r+2: apply shift[P-2] first, shift[0] last)
+  int64_t b[65], nb[65];
+  b[0] = 0;
+  for (int r = 1; r <= P; ++r) b[r] = b[r - 1] + lengths[r - 1];
+  nb[P] = N;
+  for (int r = 1; r < P; ++r) {
+    const int64_t target = (int64_t)((__int128)r * N / P);
+    nb[r] = target > b[r] ? b[r] + (target - b[r]) / granule * granule : b[r];
+  }
+  for (int r = P - 1; r >= 1; --r) nb[r] = std::min(nb[r], nb[r + 1]);
+  for (int r = 1; r < P; ++r) shift[r - 1] = nb[r] - b[r];
+  return PKV_OK;
+}
+
 }  // extern "C"

@@ -174,6 +174,8 @@ cudaError_t launch_export(const pkv_index* ix, int64_t start, int64_t count, uin
 cudaError_t launch_qprep(const pkv_index* ix, const void* q, int T, int64_t rho_keys, float* dbg_q_rot,
                          cudaStream_t stream);
 cudaError_t launch_occupancy(const pkv_index* ix, int64_t t0, int64_t t1, cudaStream_t stream);
+cudaError_t launch_export_entries(const pkv_index* ix, int64_t src0, int64_t count, void* buf, cudaStream_t stream);
+cudaError_t launch_import_entries(pkv_index* ix, int64_t dst0, int64_t count, const void* buf, cudaStream_t stream);
 
 constexpr int POST_CHUNK = 8192;  // keys per inverted-list chunk (u16 offsets)
 

@@ -84,6 +84,12 @@ _sigs = {
     "pkv_stream_state": [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i32), ctypes.POINTER(_i32),
                          ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp)],
     "pkv_index_export": [_vp, _i64, _i64, _vp, _vp, _vp, _vp],
+    "pkv_index_entry_bytes": [_vp, ctypes.POINTER(_i64)],
+    "pkv_index_export_front": [_vp, _i64, _vp, _vp],
+    "pkv_index_import_back": [_vp, _vp, _i64, _vp],
+    "pkv_index_drop_front": [_vp, _i64, _vp],
+    "pkv_index_shift_boundary": [_vp, _vp, _i64, _vp],
+    "pkv_rebalance_plan": [ctypes.POINTER(_i64), _i32, _i64, ctypes.POINTER(_i64)],
     "pkv_index_get_stats": [_vp, ctypes.POINTER(IndexStats), _vp],
     "pkv_index_set_debug_output": [_vp, _vp],
     "pkv_comm_init_host": [_vp, HostAllgatherFn, _vp, _i32, _i32, _i64],
@@ -258,6 +264,40 @@ class Index:
         w = torch.empty(self.batch, self.n_kv, count, 16, dtype=torch.float32, device=dev)
         _check(_lib.pkv_index_export(self.handle, start, count, _ptr(ids), _ptr(codes), _ptr(w), _stream(stream)))
         return ids, codes, w
+
+
+    # ---- append rebalancing across sequence shards (pkv_index_export_front / import_back / drop_front)
+    def entry_bytes(self) -> int:
+        v = _i64(0)
+        _check(_lib.pkv_index_entry_bytes(self.handle, ctypes.byref(v)))
+        return int(v.value)
+
+    def export_front(self, count: int, stream=None) -> torch.Tensor:
+        """Entries of the `count` oldest keys, u8 [count * entry_bytes] on the index's device."""
+        buf = torch.empty(max(1, count * self.entry_bytes()), dtype=torch.uint8, device=torch.device("cuda", self.device))
+        _check(_lib.pkv_index_export_front(self.handle, count, _ptr(buf), _stream(stream)))
+        return buf
+
+    def import_back(self, buf: torch.Tensor, count: int, stream=None):
+        assert buf.dtype == torch.uint8 and buf.is_contiguous() and buf.numel() >= count * self.entry_bytes()
+        _check(_lib.pkv_index_import_back(self.handle, _ptr(buf), count, _stream(stream)))
+
+    def drop_front(self, count: int, stream=None):
+        _check(_lib.pkv_index_drop_front(self.handle, count, _stream(stream)))
+
+
+def shift_boundary(older: Index, newer: Index, count: int, stream=None):
+    """Move the `count` oldest keys of `newer` to the end of `older` (same device)."""
+    _check(_lib.pkv_index_shift_boundary(older.handle, newer.handle, count, _stream(stream)))
+
+
+def rebalance_plan(lengths, granule: int = 512) -> list:
+    """shift[r] = keys to move from shard r+1 to shard r (apply from the last boundary to the first)."""
+    P = len(lengths)
+    arr = (_i64 * P)(*[int(x) for x in lengths])
+    out = (_i64 * max(1, P - 1))()
+    _check(_lib.pkv_rebalance_plan(arr, P, granule, out))
+    return [int(out[i]) for i in range(P - 1)]
 
 
 def _kv_strides(K: torch.Tensor):
