@@ -164,6 +164,90 @@ __global__ void __launch_bounds__(RR_THREADS, OCC) rerank_cpt_kernel(const uint8
   cta_mark(K_RERANK, 0);
 }
 
+// Long lists, balanced per SM (fp32 weights, one candidate per thread pair): a flat grid of exactly (resident CTAs
+// per SM) x (SMs) CTAs, CTA c taking the contiguous range [c*NT/grid, (c+1)*NT/grid) of the NT = heads x tiles
+// flattened (head, 128-candidate tile) space — every SM holds the same number of CTAs with the same number of
+// tiles. rerank_cpt_kernel's grid of 27 CTAs per head puts 6 CTAs on some SMs and 5 on others (864 over 148 x 6
+// slots) and those SMs finish ~20% apart at 1M. A CTA spans at most a few heads; the query table is restaged at
+// each head change. Same decode as rerank_cpt_kernel (the identical instruction sequence): same bits.
+template <int OCC>
+__global__ void __launch_bounds__(RR_THREADS, OCC) rerank_flat_kernel(const uint8_t* __restrict__ rec, const int32_t* cand,
+                                                                  const int32_t* sel, const float* rtab,
+                                                                  const float* qnorm, int64_t cap, int n_q, int n_kv,
+                                                                  int G, int64_t cand_stride, int64_t id_offset,
+                                                                  float* est_out, int tiles_per_head, int64_t n_tiles) {
+  __shared__ __align__(16) float T[RT_ROWS * 16];
+  phase_mark(K_RERANK, 0);
+  pdl_trigger();
+  pdl_wait();
+  phase_mark(K_RERANK, 1);
+  cta_mark(K_RERANK, 1);
+  constexpr int TILE = RR_THREADS / 2;
+  const int64_t f0 = (int64_t)blockIdx.x * n_tiles / gridDim.x, f1 = (int64_t)(blockIdx.x + 1) * n_tiles / gridDim.x;
+  const int half = threadIdx.x & 1;
+  const char* Tb = reinterpret_cast<const char*>(T);
+  const uint32_t hoff = half ? 64u : 0u;
+  auto cid_of = [&](int64_t f) -> int32_t {  // candidate id of this thread pair in flattened tile f (0 if none)
+    if (f >= f1) return 0;
+    const int bhq = (int)(f / tiles_per_head), tile = (int)(f - (int64_t)bhq * tiles_per_head);
+    const int64_t pos = (int64_t)tile * TILE + (threadIdx.x >> 1);
+    return pos < cand_stride ? cand[(int64_t)bhq * cand_stride + pos] : 0;
+  };
+  int32_t cid = cid_of(f0);
+  int cur = -1;  // head whose table is staged
+  int C_local = 0;
+  float qn = 0.f;
+  const uint8_t* rec_bh = nullptr;
+  float* eo = nullptr;
+  for (int64_t f = f0; f < f1; ++f) {
+    const int bhq = (int)(f / tiles_per_head), tile = (int)(f - (int64_t)bhq * tiles_per_head);
+    if (bhq != cur) {  // uniform over the CTA
+      __syncthreads();  // every thread is done with the previous head's table
+      const float4* tsrc = reinterpret_cast<const float4*>(rtab + (int64_t)bhq * D * 16);
+#pragma unroll
+      for (int u = 0; u < D * 4 / RR_THREADS; ++u) {
+        const int i = threadIdx.x + u * RR_THREADS;
+        const int c = i >> 2;
+        reinterpret_cast<float4*>(T)[(2 * (c & 63) + (c >> 6)) * 4 + (i & 3)] = tsrc[i];
+      }
+      cur = bhq;
+      const int b = bhq / n_q, h = bhq - b * n_q;
+      C_local = sel[(int64_t)bhq * SEL_STRIDE + 2];
+      qn = qnorm[bhq];
+      rec_bh = rec + ((int64_t)b * n_kv + h / G) * cap * REC + 32 * half;
+      eo = est_out + (int64_t)bhq * cand_stride;
+      __syncthreads();
+    }
+    const int pos = tile * TILE + (threadIdx.x >> 1);
+    u32x8 cr, wr;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) cr.w[i] = wr.w[i] = 0u;
+    if (pos < C_local) {
+      const uint8_t* r = rec_bh + ((int64_t)cid - id_offset) * REC;
+      cr = ldg_nc_v8_early(r);
+      wr = ldg_nc_v8_early(r + 64);
+    }
+    cid = cid_of(f + 1);  // the next tile's candidate ids, in flight during this tile's lookups
+    if (f == f0) phase_mark(K_RERANK, 2);
+    const uint32_t* cw = cr.w;
+    float e = 0.f;
+#pragma unroll
+    for (int sb = 0; sb < 8; ++sb) {
+      float dot = *reinterpret_cast<const float*>(Tb + (8 * sb) * 128 + (((cw[sb] << 2) & 0x3cu) | hoff));
+#pragma unroll
+      for (int j = 1; j < 8; ++j) {
+        const uint32_t off = (cw[sb] >> (4 * j - 2)) & 0x3cu;
+        dot += *reinterpret_cast<const float*>(Tb + (8 * sb + j) * 128 + (off | hoff));
+      }
+      e = fmaf(__uint_as_float(wr.w[sb]), dot, e);
+    }
+    const float et = e + __shfl_xor_sync(0xffffffffu, e, 1);
+    if (!half && pos < C_local) eo[pos] = et * qn;
+  }
+  phase_mark(K_RERANK, 3);
+  cta_mark(K_RERANK, 0);
+}
+
 // GQA-union rerank: one record read per (key, KV head) for the union of the group's candidate
 // lists. A half-warp per record, lane = subspace b: the lane reads the record's 4-byte nibble word and weight of
 // its subspace (a half-warp reads the 128-byte record in two fully used 64-byte pieces), decodes each nibble to
@@ -1535,6 +1619,28 @@ cudaError_t launch_rerank(const pkv_index* ix, int64_t C_cap, int64_t id_offset,
   const int64_t persist = std::max<int64_t>(1, (int64_t)ix->num_sms * occ / ((int64_t)ix->batch * ix->cfg.n_q_heads));
   // capped only when the tiles exceed two full waves: a short list (128K: 31 tiles per head vs 27 resident CTAs)
   // runs one CTA per tile, a long one (1M: 205+) loops over tiles in resident CTAs
+  static const int flat_env = [] {  // PKV_RR_FLAT=0|1: force the per-head / the flat balanced grid (A/B)
+    const char* e = getenv("PKV_RR_FLAT");
+    return e ? atoi(e) : -1;
+  }();
+  // long lists, fp32 weights, one candidate per pair: the SM-balanced flat grid once every CTA loops over >= 8
+  // tiles (1M: ~15 per CTA, 181.1-181.3 vs 182.3-182.7 us/layer same box; 32K bs 8, ~4.5 per CTA: 85.0 vs 82.7-83.0
+  // — too few tiles to amortise the table restaging at head changes)
+  auto fk = occ8 ? rerank_flat_kernel<8> : rerank_flat_kernel<6>;
+  static int focc[2] = {0, 0};
+  int& o = focc[occ8 ? 1 : 0];
+  if (!o && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fk, RR_THREADS, 0) != cudaSuccess || o < 1)) o = 1;
+  const int64_t heads = (int64_t)ix->batch * ix->cfg.n_q_heads;
+  const int64_t n_tiles = heads * tiles;
+  const int64_t ctas = std::min<int64_t>(n_tiles, (int64_t)ix->num_sms * o);
+  const bool flat = !ix->dcfg.w16 && cpt == 1 && (flat_env == 1 || (flat_env != 0 && n_tiles >= 8 * ctas));
+  if (flat) {
+    ProfScope p_(K_RERANK, stream);
+    return pdl_launch(fk, dim3((unsigned)ctas), dim3(RR_THREADS), 0, stream, (const uint8_t*)ix->rec,
+                      (const int32_t*)ws->cand, (const int32_t*)ws->sel, (const float*)ws->rtab,
+                      (const float*)ws->qnorm, ix->cap, ix->cfg.n_q_heads, ix->cfg.n_kv_heads, ix->dcfg.G, ws->cap,
+                      id_offset, ws->est, (int)tiles, n_tiles);
+  }
   const dim3 grid((unsigned)(tiles > 2 * persist ? persist : tiles), ix->cfg.n_q_heads, ix->batch);
   ProfScope p_(K_RERANK, stream);
   return pdl_launch(kern, grid, dim3(RR_THREADS), 0, stream, (const uint8_t*)ix->rec, (const int32_t*)ws->cand,
