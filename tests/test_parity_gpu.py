@@ -789,3 +789,39 @@ def test_half_warp_encoder_still_exact(pkv, monkeypatch):
     monkeypatch.setenv("PKV_ENCODER", "half")
     K, q, V = make_problem(96, 2, 8, 2, 3001)
     run_and_check(pkv, K, q, V, k=64, n_hot=16)
+
+
+_RR_SCRIPT = r"""
+import sys, torch
+sys.path.insert(0, sys.argv[1])
+import synth
+from paper_2602_07721_b200 import pariskv as pkv
+from tests.test_parity_gpu import make_problem
+from tests.gpu_helpers import SB
+K, q, _ = make_problem(61, 2, 8, 2, 40000, device="cuda")
+cfg = pkv.config_init(8, 2, SB)
+ix = pkv.Index(cfg, 2, 40000)
+pkv.encode_keys(ix, K)
+idx, est, dbg = pkv.retrieve_topk(ix, q, 100, n_cand=12000, debug=True)
+torch.save({"idx": idx.cpu(), "est": est.cpu(), "cand": dbg["cand"].cpu(), "e": dbg["est"].cpu()}, sys.argv[2])
+"""
+
+
+def test_rerank_grids_bit_identical(pkv, tmp_path):
+    """The SM-balanced flat rerank grid and the per-head grid (PKV_RR_FLAT=1 / 0, read once per process, hence the
+    child processes) give the same candidates, estimates and top-k bit for bit (n_cand = 12000 of 40000 keys,
+    batch 2: 94 tiles per head, head changes inside flat CTAs)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = []
+    for env in ("1", "0"):
+        f = tmp_path / f"rr_{env}.pt"
+        r = subprocess.run([sys.executable, "-c", _RR_SCRIPT, root, str(f)], cwd=root, capture_output=True, text=True,
+                           env={**os.environ, "PKV_RR_FLAT": env}, timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        out.append(torch.load(f))
+    a, b = out
+    assert torch.equal(a["cand"], b["cand"]) and torch.equal(a["e"], b["e"])
+    assert torch.equal(a["idx"], b["idx"]) and torch.equal(a["est"], b["est"])
