@@ -41,7 +41,7 @@ struct Workspace {
   int device = -1;
   int batch = 0, n_q = 0, n_kv = 0;
   int64_t cap = 0;
-  uint32_t* lut = nullptr;        // [batch][n_kv][256 c][16 s] packed bonuses (byte j = query head g*G+j)
+  uint32_t* lut = nullptr;        // [batch][n_kv][4 heads][16 s][256 c] bonus bytes (head j = query head g*G+j)
   float* rtab = nullptr;          // [batch][n_q][128 coord][16 nibble] rerank tables sign*L[idx]*q~
   float* qnorm = nullptr;         // [batch][n_q]
   float* qrot = nullptr;          // [batch][n_q][128]

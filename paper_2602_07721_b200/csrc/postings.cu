@@ -89,11 +89,16 @@ __global__ void __launch_bounds__(PS_THREADS, 1) postings_scan_kernel(const uint
   for (int i = threadIdx.x; i < PS_WARPS * GMAX * HB; i += PS_THREADS) hist[i] = 0u;
   __syncthreads();
   pdl_wait();  // lookup table comes from qprep
-  const uint32_t* lg = lut_g + (int64_t)bh * NC * NB;  // [c][s] packed bonuses
-  // each thread: (s, c) pairs p = tid + 1024 u, s = p % 16, c = p / 16 (consecutive threads read consecutive words)
+  const uint8_t* lb = reinterpret_cast<const uint8_t*>(lut_g + (int64_t)bh * NC * NB);  // [hh][s][c] bonus bytes
+  // each thread: (s, c) pairs p = tid + 1024 u, s = p % 16, c = p / 16; word = the 4 query heads' bonus bytes
   uint32_t w[NC * NB / PS_THREADS];
 #pragma unroll
-  for (int u = 0; u < NC * NB / PS_THREADS; ++u) w[u] = lg[threadIdx.x + u * PS_THREADS];
+  for (int u = 0; u < NC * NB / PS_THREADS; ++u) {
+    const int p = threadIdx.x + u * PS_THREADS, s = p & 15, c = p >> 4;
+    w[u] = 0u;
+#pragma unroll
+    for (int hh = 0; hh < GMAX; ++hh) w[u] |= (uint32_t)lb[(hh * NB + s) * NC + c] << (8 * hh);
+  }
 #pragma unroll
   for (int u = 0; u < NC * NB / PS_THREADS; ++u) {
     if (w[u] == 0u) continue;

@@ -21,7 +21,8 @@ namespace {
 constexpr int SCAN_THREADS = 1024;
 constexpr int SCAN_WARPS = SCAN_THREADS / 32;
 constexpr int LUT_WORDS = NC * 64;                 // 64 KB
-constexpr int SCAN_SMEM = LUT_WORDS * 4 + SCAN_WARPS * GMAX * HB * 4;
+constexpr int LUT_STG_STRIDE = 66;  // words per staged (query head, subspace) row: 64 + 2 (conflict-free transposes)
+constexpr int SCAN_SMEM = LUT_WORDS * 4 + SCAN_WARPS * GMAX * HB * 4 + GMAX * NB * LUT_STG_STRIDE * 4;
 constexpr int SCAN_UNROLL = 4;
 
 template <int RES, bool FAST>
@@ -117,17 +118,36 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1)
   for (int i = threadIdx.x; i < SCAN_WARPS * GMAX * HB; i += SCAN_THREADS) hist[i] = 0u;
   pdl_wait();  // lookup table comes from qprep
   phase_mark(K_SCAN, 1);
-  // expand the compact table [c][16] into 4 interleaved replicas: word c*64 + s + 16 r
-  const uint32_t* lg = lut_g + (int64_t)bh * NC * NB;
-  uint32_t lv[NC * NB / SCAN_THREADS];  // all loads in flight before the stores
+  // qprep writes one 256-byte row of bonuses per (query head, subspace): lutb[hh][s][c] (no two CTAs share a
+  // sector). (1) a coalesced copy of the 4 x 16 rows into a staging area, (2) thread (s, 4 centroids) packs the 4
+  // heads' bytes of each centroid into one word (byte hh = head hh) and writes the 4 interleaved replicas
+  // c*64 + s + 16 r, the two half-warps starting one replica apart (conflict-free stores)
+  uint32_t* stg = hist + SCAN_WARPS * GMAX * HB;
+  {
+    const uint32_t* lw = lut_g + (int64_t)bh * NC * NB;  // 4 heads x 16 rows x 64 words
+    uint32_t v[GMAX];
 #pragma unroll
-  for (int u = 0; u < NC * NB / SCAN_THREADS; ++u) lv[u] = lg[threadIdx.x + u * SCAN_THREADS];
+    for (int hh = 0; hh < GMAX; ++hh) v[hh] = lw[hh * NB * (NC / 4) + threadIdx.x];
+    const int s = threadIdx.x >> 6, c4 = threadIdx.x & 63;
 #pragma unroll
-  for (int u = 0; u < NC * NB / SCAN_THREADS; ++u) {
-    const int i = threadIdx.x + u * SCAN_THREADS;
-    const int c = i >> 4, s = i & 15;
+    for (int hh = 0; hh < GMAX; ++hh) stg[(hh * NB + s) * LUT_STG_STRIDE + c4] = v[hh];
+  }
+  __syncthreads();
+  {
+    const int s = threadIdx.x & 15, c4 = threadIdx.x >> 4, rot = c4 & 1;
+    uint32_t h[GMAX];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) lut[c * 64 + s + 16 * ((r + (c & 1)) & 3)] = lv[u];
+    for (int hh = 0; hh < GMAX; ++hh) h[hh] = stg[(hh * NB + s) * LUT_STG_STRIDE + c4];
+    const uint32_t a0 = prmt(h[0], h[1], 0x5140u), a1 = prmt(h[0], h[1], 0x7362u);  // h0.0 h1.0 h0.1 h1.1 | .2 .3
+    const uint32_t b0 = prmt(h[2], h[3], 0x5140u), b1 = prmt(h[2], h[3], 0x7362u);
+    const uint32_t w[4] = {prmt(a0, b0, 0x5410u), prmt(a0, b0, 0x7632u), prmt(a1, b1, 0x5410u),
+                           prmt(a1, b1, 0x7632u)};  // centroid 4 c4 + k: its 4 heads' bonus bytes
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int c = 4 * c4 + k;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) lut[c * 64 + s + 16 * ((r + rot) & 3)] = w[k];
+    }
   }
   __syncthreads();
   const uint32_t lut_base = (uint32_t)__cvta_generic_to_shared(lut);
