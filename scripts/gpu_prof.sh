@@ -14,7 +14,7 @@ if [ "$what" = scan1m ] || [ "$what" = all ]; then
 fi
 if [ "$what" = full ] || [ "$what" = all ]; then
   for c in 128k 1m; do
-    timeout 900 ncu --set full --import-source on --clock-control none -k regex:"qprep_kernel|scan_kernel|select_kernel|rerank_cpt_kernel|topk_cl_kernel" -s 10 -c 5 -o gpurun_out/full_${c}_$tag $B --config $c --layers 4 --no-graph > gpurun_out/ncu_full_${c}_$tag.log 2>&1
+    timeout 900 ncu --set full --import-source on --clock-control none -k regex:"qprep_kernel|scan_kernel|select_kernel|rerank_cpt_kernel|rerank_flat_kernel|topk_cl_kernel" -s 10 -c 5 -o gpurun_out/full_${c}_$tag $B --config $c --layers 4 --no-graph > gpurun_out/ncu_full_${c}_$tag.log 2>&1
     ncu -i gpurun_out/full_${c}_$tag.ncu-rep --page raw --csv > gpurun_out/full_${c}_${tag}_raw.csv 2>/dev/null
   done
 fi

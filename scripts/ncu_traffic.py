@@ -10,7 +10,7 @@ import statistics
 import sys
 
 NAMES = {"qprep_kernel": "qprep", "scan_kernel": "scan", "select_kernel": "select", "rerank_cpt_kernel": "rerank",
-         "rerank_kernel": "rerank", "topk_cl_kernel": "topk", "topk_kernel": "topk", "merge_kernel": "topk_merge",
+         "rerank_kernel": "rerank", "rerank_flat_kernel": "rerank", "topk_cl_kernel": "topk", "topk_kernel": "topk", "merge_kernel": "topk_merge",
          "attend_partial_kernel": "attend"}
 SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
