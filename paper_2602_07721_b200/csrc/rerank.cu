@@ -175,7 +175,8 @@ __global__ void __launch_bounds__(RR_THREADS, OCC) rerank_flat_kernel(const uint
                                                                   const int32_t* sel, const float* rtab,
                                                                   const float* qnorm, int64_t cap, int n_q, int n_kv,
                                                                   int G, int64_t cand_stride, int64_t id_offset,
-                                                                  float* est_out, int tiles_per_head, int64_t n_tiles) {
+                                                                  float* est_out, int tiles_per_head, int64_t n_tiles,
+                                                                  float alpha) {
   __shared__ __align__(16) float T[RT_ROWS * 16];
   phase_mark(K_RERANK, 0);
   pdl_trigger();
@@ -183,7 +184,15 @@ __global__ void __launch_bounds__(RR_THREADS, OCC) rerank_flat_kernel(const uint
   phase_mark(K_RERANK, 1);
   cta_mark(K_RERANK, 1);
   constexpr int TILE = RR_THREADS / 2;
-  const int64_t f0 = (int64_t)blockIdx.x * n_tiles / gridDim.x, f1 = (int64_t)(blockIdx.x + 1) * n_tiles / gridDim.x;
+  // range of CTA c: equal shares (alpha = 0), or shares ~ 1 / (1 + alpha c / P) — CTAs with higher linear ids run
+  // slower when all of them compete for the SM (measured at 1M, see DESIGN), so they get fewer tiles:
+  // f(c) = NT ln(1 + alpha c / P) / ln(1 + alpha)
+  auto edge = [&](int x) -> int64_t {
+    if (x >= (int)gridDim.x) return n_tiles;
+    if (alpha <= 0.f) return (int64_t)x * n_tiles / gridDim.x;
+    return (int64_t)((double)n_tiles * log1p((double)alpha * x / gridDim.x) / log1p((double)alpha));
+  };
+  const int64_t f0 = edge(blockIdx.x), f1 = edge(blockIdx.x + 1);
   const int half = threadIdx.x & 1;
   const char* Tb = reinterpret_cast<const char*>(T);
   const uint32_t hoff = half ? 64u : 0u;
@@ -1567,6 +1576,18 @@ bool union_rerank() {
   return e && std::string(e) == "union";
 }
 
+// Share skew of the flat rerank grid (PKV_RR_ALPHA overrides; 0 = equal ranges). 1M, same box, 200-step graphs:
+// alpha 0 185.7-185.9, 0.7 179.5, 1.0 181.2-181.3, 1.4 182.1, 2.0 183.3 us/layer (another box: 0 183.1-183.8,
+// 0.7 180.8). With equal ranges the CTA end times grow with the linear id (101.6 -> 120.2 us at 1M, independent of
+// which tiles a CTA holds: a permuted id -> range map keeps the spread with the id), so the SMs idle through a tail.
+static float rr_alpha() {
+  static const float a = [] {
+    const char* e = getenv("PKV_RR_ALPHA");
+    return e ? (float)atof(e) : 0.7f;
+  }();
+  return a;
+}
+
 cudaError_t launch_rerank(const pkv_index* ix, int64_t C_cap, int64_t id_offset, cudaStream_t stream) {
   const Workspace* ws = ix->ws;
   if (union_rerank()) {
@@ -1639,7 +1660,7 @@ cudaError_t launch_rerank(const pkv_index* ix, int64_t C_cap, int64_t id_offset,
     return pdl_launch(fk, dim3((unsigned)ctas), dim3(RR_THREADS), 0, stream, (const uint8_t*)ix->rec,
                       (const int32_t*)ws->cand, (const int32_t*)ws->sel, (const float*)ws->rtab,
                       (const float*)ws->qnorm, ix->cap, ix->cfg.n_q_heads, ix->cfg.n_kv_heads, ix->dcfg.G, ws->cap,
-                      id_offset, ws->est, (int)tiles, n_tiles);
+                      id_offset, ws->est, (int)tiles, n_tiles, rr_alpha());
   }
   const dim3 grid((unsigned)(tiles > 2 * persist ? persist : tiles), ix->cfg.n_q_heads, ix->batch);
   ProfScope p_(K_RERANK, stream);
