@@ -107,6 +107,12 @@ def test_gqa_batch_ragged(pkv):
     run_and_check(pkv, K, q, V, k=100, n_hot=37)
 
 
+def test_gqa_group_of_3(pkv):
+    """G = 3 query heads per KV head: the packed bonus word's 4th byte (no head) stays 0 in the scan."""
+    K, q, V = make_problem(5, 1, 6, 2, 3000)
+    run_and_check(pkv, K, q, V, k=64, n_hot=20)
+
+
 def test_llama_shape_small_n(pkv):
     K, q, V = make_problem(3, 1, 32, 8, 3001)
     run_and_check(pkv, K, q, V, k=100, n_hot=272, check_all_heads=False)
