@@ -34,13 +34,13 @@ __global__ void __launch_bounds__(EF_THREADS, 4) encode_fast_kernel(const uint16
                                                                      uint8_t* __restrict__ rec, int32_t* fb_list,
                                                                      int32_t* fb_n) {
   extern __shared__ __align__(16) uint8_t rows[];  // EF_SMEM bytes
-  __shared__ float sLs[16];                        // nibble (sign << 3 | idx) -> sign * L[idx]
-  __shared__ float sB[EF_BUCKETS];  // magnitude buckets of r = y^2 / S: threshold, with the idx below in its 3 low bits
+  // magnitude buckets of r = y^2 / S: (threshold with the idx below it in its 3 low bits, L[idx below],
+  // L[idx above]) — the decision and its level come from one load
+  __shared__ float4 sB[EF_BUCKETS];
   __shared__ __align__(16) uint4 sS[16];           // per 32-bit word of a key row: the rotation signs of its two bf16
   const int tid = threadIdx.x, bh = blockIdx.y, half = tid & 1;
   const int b = bh / n_kv, h = bh - b * n_kv;
   const int64_t tile0 = (int64_t)blockIdx.x * EF_KEYS;
-  if (tid < 16) sLs[tid] = (tid & 8) ? cfg.levels[tid & 7] : -cfg.levels[tid & 7];
   if (tid < EF_BUCKETS) {
     // bucket k: r in [2^-9 (1 + (k&7)/8) 2^(k>>3), next edge); bucket 0 also takes everything below
     const float lo = ldexpf(1.f + (float)(tid & 7) * 0.125f, (tid >> 3) - 9);
@@ -53,7 +53,8 @@ __global__ void __launch_bounds__(EF_THREADS, 4) encode_fast_kernel(const uint16
       below += m < lo;
       if (m >= lo && m < hi) thr = m;
     }
-    sB[tid] = __uint_as_float((__float_as_uint(thr) & ~7u) | (uint32_t)below);
+    sB[tid] = make_float4(__uint_as_float((__float_as_uint(thr) & ~7u) | (uint32_t)below), cfg.levels[below],
+                          cfg.levels[below < 7 ? below + 1 : 7], 0.f);
   }
   if (tid < 64) {  // word i holds coordinates 2i (low half) and 2i + 1 (high half)
     const uint32_t w = cfg.sign_mask[tid >> 4];
@@ -160,13 +161,16 @@ __global__ void __launch_bounds__(EF_THREADS, 4) encode_fast_kernel(const uint16
       const uint32_t pos = v[8 * s + j] >= 0 ? 1u : 0u;
       const float r = q[j] * invS;
       const int k = min(EF_BUCKETS - 1, max(0, (int)(__float_as_uint(r) >> 20) - (118 << 3)));
-      const float thr = sB[k];
-      const uint32_t idx = (__float_as_uint(thr) & 7u) + (r >= thr ? 1u : 0u);
+      const float4 bt = sB[k];
+      const float thr = bt.x;
+      const bool up = r >= thr;
+      const uint32_t idx = (__float_as_uint(thr) & 7u) + (up ? 1u : 0u);
       dmin = fminf(dmin, fabsf(r - thr) - EF_MARGIN * thr);
       const uint32_t nib = (pos << 3) | idx;
       idb |= pos << j;
       cw |= nib << (4 * j);
-      const float Ls = sLs[nib];  // sign * L[idx]
+      const float Lm = up ? bt.z : bt.y;
+      const float Ls = pos ? Lm : -Lm;  // sign * L[idx]
       dot = fmaf(Ls, f[j], dot);
       vn2 = fmaf(Ls, Ls, vn2);
     }
