@@ -27,6 +27,60 @@ constexpr int EF_SMEM = EF_KEYS * EF_ROW;          // the bf16 rows; then each w
 constexpr float EF_MARGIN = 96.f * 5.9604645e-8f;  // 96 u, relative to a threshold of r (64u + the 3 packed bits)
 constexpr int EF_BUCKETS = 72;                     // r in [2^-9, 1): 9 binades x 8
 
+// One subspace's decisions and weight (8 exact coordinates y): id bits, magnitude codes, certification slack, w'.
+// Not inlined: the eight call sites share one copy of the code (the fully unrolled loop was 8 copies and the
+// kernel stalled on instruction fetch 19% of the time).
+struct EfSub {
+  uint32_t idb, cw;
+  float wp, dmin;
+  int sok;
+};
+__device__ __noinline__ EfSub ef_subspace(int4 ya, int4 yb, const float4* sB, double unscale) {
+  const int v[8] = {ya.x, ya.y, ya.z, ya.w, yb.x, yb.y, yb.z, yb.w};
+  EfSub o;
+  float f[8], q[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    f[j] = (float)v[j];
+    q[j] = f[j] * f[j];
+  }
+  const float S = ((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]));
+  o.sok = S > 0.f;  // a zero subspace takes the exact path (AMB-7 encoding + stats)
+  // r = q / S: relative error <= ~16u (q 3u, S 7u, reciprocal 2u)
+  const float invS = 1.0f / S;
+  uint32_t idb = 0u, cw = 0u;
+  float dot = 0.f, vn2 = 0.f, dmin = 3.0e38f;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint32_t pos = v[j] >= 0 ? 1u : 0u;
+    const float r = q[j] * invS;
+    const int k = min(EF_BUCKETS - 1, max(0, (int)(__float_as_uint(r) >> 20) - (118 << 3)));
+    const float4 bt = sB[k];
+    const float thr = bt.x;
+    const bool up = r >= thr;
+    const uint32_t idx = (__float_as_uint(thr) & 7u) + (up ? 1u : 0u);
+    dmin = fminf(dmin, fabsf(r - thr) - EF_MARGIN * thr);
+    const uint32_t nib = (pos << 3) | idx;
+    idb |= pos << j;
+    cw |= nib << (4 * j);
+    const float Lm = up ? bt.z : bt.y;
+    const float Ls = pos ? Lm : -Lm;  // sign * L[idx]
+    dot = fmaf(Ls, f[j], dot);
+    vn2 = fmaf(Ls, Ls, vn2);
+  }
+  dot *= 4.656612873077393e-10f;  // y' 2^(119 - emax) = v 2^-31: encode.cu's scaled coordinates, |.| < 1
+  // w' = w / ||sign L[idx]|| (encode.cu): alpha = dot / (||v~|| sqrt(S)), floor 1e-3 (AMB-6)
+  const float Sf = S * 2.168404344971009e-19f;  // (2^-31)^2
+  const bool clamped = (dot <= 0.f) || (dot * dot < 1e-6f * vn2 * Sf);
+  const float w_rel =
+      clamped ? sqrtf(Sf * (1.0f / 128.0f)) / (1e-3f * sqrtf(vn2)) : Sf / (11.313708498984761f * dot);
+  o.wp = (float)((double)w_rel * unscale);
+  o.idb = idb;
+  o.cw = cw;
+  o.dmin = dmin;
+  return o;
+}
+
 __global__ void __launch_bounds__(EF_THREADS, 4) encode_fast_kernel(const uint16_t* __restrict__ K, int64_t sb,
                                                                      int64_t sh, int64_t st, int64_t count, int n_kv,
                                                                      int64_t cap, int64_t t0, DevCfg cfg,
@@ -144,45 +198,13 @@ __global__ void __launch_bounds__(EF_THREADS, 4) encode_fast_kernel(const uint16
   float dmin = 3.0e38f;  // smallest |r - threshold| / threshold margin slack over the thread's coordinates
 #pragma unroll
   for (int s = 0; s < 8; ++s) {
-    float f[8], q[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      f[j] = (float)v[8 * s + j];
-      q[j] = f[j] * f[j];
-    }
-    const float S = ((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]));
-    ok &= S > 0.f;  // a zero subspace takes the exact path (AMB-7 encoding + stats)
-    // r = q / S: relative error <= ~16u (q 3u, S 7u, reciprocal 2u)
-    const float invS = 1.0f / S;
-    uint32_t idb = 0u, cw = 0u;
-    float dot = 0.f, vn2 = 0.f;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const uint32_t pos = v[8 * s + j] >= 0 ? 1u : 0u;
-      const float r = q[j] * invS;
-      const int k = min(EF_BUCKETS - 1, max(0, (int)(__float_as_uint(r) >> 20) - (118 << 3)));
-      const float4 bt = sB[k];
-      const float thr = bt.x;
-      const bool up = r >= thr;
-      const uint32_t idx = (__float_as_uint(thr) & 7u) + (up ? 1u : 0u);
-      dmin = fminf(dmin, fabsf(r - thr) - EF_MARGIN * thr);
-      const uint32_t nib = (pos << 3) | idx;
-      idb |= pos << j;
-      cw |= nib << (4 * j);
-      const float Lm = up ? bt.z : bt.y;
-      const float Ls = pos ? Lm : -Lm;  // sign * L[idx]
-      dot = fmaf(Ls, f[j], dot);
-      vn2 = fmaf(Ls, Ls, vn2);
-    }
-    dot *= 4.656612873077393e-10f;  // y' 2^(119 - emax) = v 2^-31: encode.cu's scaled coordinates, |.| < 1
-    id8 |= (unsigned long long)idb << (8 * s);
-    code[s] = cw;
-    // w' = w / ||sign L[idx]|| (encode.cu): alpha = dot / (||v~|| sqrt(S)), floor 1e-3 (AMB-6)
-    const float Sf = S * 2.168404344971009e-19f;  // (2^-31)^2
-    const bool clamped = (dot <= 0.f) || (dot * dot < 1e-6f * vn2 * Sf);
-    const float w_rel =
-        clamped ? sqrtf(Sf * (1.0f / 128.0f)) / (1e-3f * sqrtf(vn2)) : Sf / (11.313708498984761f * dot);
-    wp[s] = (float)((double)w_rel * unscale);
+    const EfSub o = ef_subspace(make_int4(v[8 * s], v[8 * s + 1], v[8 * s + 2], v[8 * s + 3]),
+                                make_int4(v[8 * s + 4], v[8 * s + 5], v[8 * s + 6], v[8 * s + 7]), sB, unscale);
+    ok &= o.sok != 0;
+    dmin = fminf(dmin, o.dmin);
+    id8 |= (unsigned long long)o.idb << (8 * s);
+    code[s] = o.cw;
+    wp[s] = o.wp;
   }
   ok &= dmin > 0.f;
   {
