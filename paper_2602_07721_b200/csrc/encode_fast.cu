@@ -30,6 +30,12 @@ constexpr int EF_BUCKETS = 72;                     // r in [2^-9, 1): 9 binades 
 // One subspace's decisions and weight (8 exact coordinates y): id bits, magnitude codes, certification slack, w'.
 // Not inlined: the eight call sites share one copy of the code (the fully unrolled loop was 8 copies and the
 // kernel stalled on instruction fetch 19% of the time).
+__device__ __forceinline__ uint32_t umad(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
 struct EfSub {
   uint32_t idb, cw;
   float wp, dmin;
@@ -52,7 +58,7 @@ __device__ __noinline__ EfSub ef_subspace(int4 ya, int4 yb, const float4* sB, do
   float dot = 0.f, vn2 = 0.f, dmin = 3.0e38f;
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    const uint32_t pos = v[j] >= 0 ? 1u : 0u;
+    const uint32_t pos = (uint32_t)(~v[j]) >> 31;  // y >= 0 (an int has no -0)
     const float r = q[j] * invS;
     const int k = min(EF_BUCKETS - 1, max(0, (int)(__float_as_uint(r) >> 20) - (118 << 3)));
     const float4 bt = sB[k];
@@ -60,11 +66,12 @@ __device__ __noinline__ EfSub ef_subspace(int4 ya, int4 yb, const float4* sB, do
     const bool up = r >= thr;
     const uint32_t idx = (__float_as_uint(thr) & 7u) + (up ? 1u : 0u);
     dmin = fminf(dmin, fabsf(r - thr) - EF_MARGIN * thr);
-    const uint32_t nib = (pos << 3) | idx;
-    idb |= pos << j;
-    cw |= nib << (4 * j);
+    // disjoint bit fields packed by multiply-adds (FMA pipe; the ALU pipe is this kernel's bound)
+    const uint32_t nib = umad(pos, 8u, idx);
+    idb = umad(pos, 1u << j, idb);
+    cw = umad(nib, 1u << (4 * j), cw);
     const float Lm = up ? bt.z : bt.y;
-    const float Ls = pos ? Lm : -Lm;  // sign * L[idx]
+    const float Ls = __uint_as_float(__float_as_uint(Lm) | (__float_as_uint(f[j]) & 0x80000000u));  // sign * L[idx]
     dot = fmaf(Ls, f[j], dot);
     vn2 = fmaf(Ls, Ls, vn2);
   }
