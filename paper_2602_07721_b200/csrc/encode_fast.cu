@@ -64,7 +64,7 @@ __device__ __noinline__ EfSub ef_subspace(int4 ya, int4 yb, const float4* sB, do
     const float4 bt = sB[k];
     const float thr = bt.x;
     const bool up = r >= thr;
-    const uint32_t idx = (__float_as_uint(thr) & 7u) + (up ? 1u : 0u);
+    const uint32_t idx = __float_as_uint(bt.w) + (up ? 1u : 0u);  // = (thr bits & 7) + up
     dmin = fminf(dmin, fabsf(r - thr) - EF_MARGIN * thr);
     // disjoint bit fields packed by multiply-adds (FMA pipe; the ALU pipe is this kernel's bound)
     const uint32_t nib = umad(pos, 8u, idx);
@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(EF_THREADS, PKV_EF_MINB) encode_fast_kernel(co
       if (m >= lo && m < hi) thr = m;
     }
     sB[tid] = make_float4(__uint_as_float((__float_as_uint(thr) & ~7u) | (uint32_t)below), cfg.levels[below],
-                          cfg.levels[below < 7 ? below + 1 : 7], 0.f);
+                          cfg.levels[below < 7 ? below + 1 : 7], __uint_as_float((uint32_t)below));
   }
   if (tid < 64) {  // word i holds coordinates 2i (low half) and 2i + 1 (high half)
     const uint32_t w = cfg.sign_mask[tid >> 4];
