@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(RR_THREADS, OCC) rerank_flat_kernel(const uint
   const uint32_t hoff = half ? 64u : 0u;
   auto cid_of = [&](int64_t f) -> int32_t {  // candidate id of this thread pair in flattened tile f (0 if none)
     if (f >= f1) return 0;
-    const int bhq = (int)(f / tiles_per_head), tile = (int)(f - (int64_t)bhq * tiles_per_head);
+    const int bhq = (int)f / tiles_per_head, tile = (int)f - bhq * tiles_per_head;  // 32-bit: < 2^31 tiles
     const int64_t pos = (int64_t)tile * TILE + (threadIdx.x >> 1);
     return pos < cand_stride ? cand[(int64_t)bhq * cand_stride + pos] : 0;
   };
@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(RR_THREADS, OCC) rerank_flat_kernel(const uint
   const uint8_t* rec_bh = nullptr;
   float* eo = nullptr;
   for (int64_t f = f0; f < f1; ++f) {
-    const int bhq = (int)(f / tiles_per_head), tile = (int)(f - (int64_t)bhq * tiles_per_head);
+    const int bhq = (int)f / tiles_per_head, tile = (int)f - bhq * tiles_per_head;
     if (bhq != cur) {  // uniform over the CTA
       __syncthreads();  // every thread is done with the previous head's table
       const float4* tsrc = reinterpret_cast<const float4*>(rtab + (int64_t)bhq * D * 16);
