@@ -16,14 +16,15 @@ pkv._lib.pkv_phase_profile.argtypes = [ctypes.c_void_p]
 dev = torch.device("cuda", 0)
 n = int(os.environ.get("PHASE_CTX", "131072")) - 272  # PHASE_CTX=1048576 PHASE_UVA=1: the 1M configuration
 stats = synth.head_stats(0, 8, device=dev)
-K = synth.llm_keys(0, 1, 8, n, device=dev, stats=stats)
-q = synth.llm_queries(0, 1, 32, 8, device=dev, stats=stats)
+B = int(os.environ.get("PHASE_BATCH", "1"))  # PHASE_CTX=32768 PHASE_BATCH=8: configuration 3
+K = synth.llm_keys(0, B, 8, n, device=dev, stats=stats)
+q = synth.llm_queries(0, B, 32, 8, device=dev, stats=stats)
 synth.plant(K, q, 0)
-V = synth.values(0, 1, 8, n, device=dev)
-Kh = synth.isotropic(7, (1, 8, 272, 128), device=dev)
-Vh = synth.isotropic(8, (1, 8, 272, 128), device=dev)
+V = synth.values(0, B, 8, n, device=dev)
+Kh = synth.isotropic(7, (B, 8, 272, 128), device=dev)
+Vh = synth.isotropic(8, (B, 8, 272, 128), device=dev)
 cfg = pkv.config_init(32, 8, synth.rotation_sign_bits())
-ix = pkv.Index(cfg, 1, n)
+ix = pkv.Index(cfg, B, n)
 pkv.encode_keys(ix, K)
 if os.environ.get("PHASE_UVA") == "1":  # K/V rows read through UVA from pinned host memory
     torch.cuda.synchronize()
